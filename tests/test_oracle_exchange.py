@@ -1,0 +1,207 @@
+"""Pins of the oracle's ghost exchange (O7), restriction/prolongation staging and remesh (O9)."""
+import itertools
+
+import numpy as np
+import pytest
+
+
+def _global_from_blocks(m, root, n):
+    G = np.zeros((5, root[2] * n, root[1] * n, root[0] * n))
+    for b in m.blocks():
+        i, j, k = b["lx"]
+        G[:, k * n:(k + 1) * n, j * n:(j + 1) * n, i * n:(i + 1) * n] = m.get_state(b["gid"])
+    return G
+
+
+def test_periodic_ghosts_equal_wrapped_interior(oracle_mod):
+    root, n, g = (3, 2, 4), 4, 2
+    m = oracle_mod.Mesh(mesh_nx=tuple(r * n for r in root), block_nx=(n,) * 3)
+    rng = np.random.default_rng(7)
+    for b in range(m.num_blocks()):
+        m.set_state_full(b, rng.normal(size=(5, n + 2 * g, n + 2 * g, n + 2 * g)))  # garbage ghosts
+    m.exchange()
+    G = _global_from_blocks(m, root, n)
+    P = np.pad(G, ((0, 0), (g, g), (g, g), (g, g)), mode="wrap")
+    for b in m.blocks():
+        i, j, k = b["lx"]
+        exp = P[:, k * n:k * n + n + 2 * g, j * n:j * n + n + 2 * g, i * n:i * n + n + 2 * g]
+        assert np.array_equal(m.get_state_full(b["gid"]), exp)
+
+
+def test_corner_buffer_is_8_cells(oracle_mod):
+    """a corner buffer of a 3D block with 2 ghost zones holds 8 numbers (per variable)."""
+    n, g = 4, 2
+    m = oracle_mod.Mesh(mesh_nx=(3 * n,) * 3, block_nx=(n,) * 3)
+    ids = {b["lx"]: b["gid"] for b in m.blocks()}
+    for lx, gid in ids.items():
+        m.set_state_full(gid, np.full((5, n + 2 * g, n + 2 * g, n + 2 * g), 1.0 if lx == (2, 2, 2) else 0.0))
+    m.exchange()
+    A = m.get_state_full(ids[(0, 0, 0)])
+    assert int((A[0] == 1.0).sum()) == 8
+    assert np.all(A[0, :g, :g, :g] == 1.0)
+
+
+@pytest.mark.parametrize("bc", ["outflow", "reflect", "mixed"])
+def test_physical_bcs(oracle_mod, bc):
+    root, n, g = (2, 2, 1), 4, 2
+    O = oracle_mod
+    if bc == "outflow":
+        bi, bo = (O.OUTFLOW,) * 3, (O.OUTFLOW,) * 3
+    elif bc == "reflect":
+        bi, bo = (O.REFLECT,) * 3, (O.REFLECT,) * 3
+    else:
+        bi, bo = (O.REFLECT, O.PERIODIC, O.OUTFLOW), (O.OUTFLOW, O.PERIODIC, O.REFLECT)
+    m = O.Mesh(mesh_nx=tuple(r * n for r in root), block_nx=(n,) * 3, bc_inner=bi, bc_outer=bo)
+    rng = np.random.default_rng(8)
+    for b in range(m.num_blocks()):
+        m.set_state_full(b, rng.normal(size=(5, n + 2 * g, n + 2 * g, n + 2 * g)))
+    m.exchange()
+    G = _global_from_blocks(m, root, n)
+    # expected: pad dimension by dimension x1, x2, x3 (numpy axes 3, 2, 1)
+    P = G
+    for d, ax in ((0, 3), (1, 2), (2, 1)):
+        padw = [(0, 0)] * 4
+        padw[ax] = (g, g)
+        if bi[d] == O.PERIODIC:
+            P = np.pad(P, padw, mode="wrap")
+            continue
+        lo = np.pad(P, padw, mode="symmetric" if bi[d] == O.REFLECT else "edge")
+        hi = np.pad(P, padw, mode="symmetric" if bo[d] == O.REFLECT else "edge")
+        sl_lo = [slice(None)] * 4
+        sl_lo[ax] = slice(0, g)
+        sl_hi = [slice(None)] * 4
+        sl_hi[ax] = slice(-g, None)
+        Q = lo.copy()
+        Q[tuple(sl_hi)] = hi[tuple(sl_hi)]
+        if bi[d] == O.REFLECT:
+            idx = list(sl_lo)
+            idx[0] = 1 + d
+            Q[tuple(idx)] *= -1
+        if bo[d] == O.REFLECT:
+            idx = list(sl_hi)
+            idx[0] = 1 + d
+            Q[tuple(idx)] *= -1
+        P = Q
+    for b in m.blocks():
+        i, j, k = b["lx"]
+        exp = P[:, k * n:k * n + n + 2 * g, j * n:j * n + n + 2 * g, i * n:i * n + n + 2 * g]
+        assert np.array_equal(m.get_state_full(b["gid"]), exp), b
+
+
+def _two_level_mesh(O, bc):
+    return O.Mesh(mesh_nx=(32, 32, 32), block_nx=(8, 8, 8), max_level=1, refinement=O.REF_STATIC,
+                  regions=[(1, 0.3, 0.55, 0.45, 0.8, 0.3, 0.6)], bc_inner=(bc,) * 3, bc_outer=(bc,) * 3)
+
+
+def test_constant_across_level_jump(oracle_mod):
+    O = oracle_mod
+    for bc in (O.PERIODIC, O.OUTFLOW, O.REFLECT):
+        m = _two_level_mesh(O, bc)
+        assert set(b["level"] for b in m.blocks()) == {0, 1}
+        c = np.array([1.25, 0.0, 0.0, 0.0, 2.5])
+        for b in range(m.num_blocks()):
+            m.set_state_full(b, np.broadcast_to(c[:, None, None, None], (5, 12, 12, 12)) * 1.0)
+        m.exchange()
+        for b in range(m.num_blocks()):
+            F = m.get_state_full(b)
+            for v in range(5):
+                assert np.all(F[v] == c[v])
+
+
+def test_linear_field_reproduced_across_level_jump(oracle_mod):
+    """restriction is exact on linear data and minmod prolongation reproduces it where slopes agree."""
+    O = oracle_mod
+    m = _two_level_mesh(O, O.OUTFLOW)
+    coef = np.array([[1.0, 0.3, -0.2, 0.5], [0.1, -0.4, 0.25, 0.7], [2.0, 0.05, 0.6, -0.3],
+                     [-1.0, 0.2, 0.2, 0.2], [3.0, -0.6, 0.1, 0.9]])
+    n, g = 8, 2
+    for b in m.blocks():
+        dx = [(b["xmax"][d] - b["xmin"][d]) / n for d in range(3)]
+        c = [b["xmin"][d] + (np.arange(-g, n + g) + 0.5) * dx[d] for d in range(3)]
+        Z, Y, X = np.meshgrid(c[2], c[1], c[0], indexing="ij")
+        F = np.stack([a[0] + a[1] * X + a[2] * Y + a[3] * Z for a in coef])
+        F[:, g:-g, g:-g, g:-g] += 0.0
+        garbage = np.where(np.pad(np.zeros((n, n, n), bool), g, constant_values=True), 1e30, 1.0)
+        m.set_state_full(b["gid"], np.where(garbage == 1e30, 1e30, F))
+    m.exchange()
+    checked = 0
+    for b in m.blocks():
+        dx = [(b["xmax"][d] - b["xmin"][d]) / n for d in range(3)]
+        c = [b["xmin"][d] + (np.arange(-g, n + g) + 0.5) * dx[d] for d in range(3)]
+        Z, Y, X = np.meshgrid(c[2], c[1], c[0], indexing="ij")
+        exp = np.stack([a[0] + a[1] * X + a[2] * Y + a[3] * Z for a in coef])
+        got = m.get_state_full(b["gid"])
+        # stay 3 coarse cells away from the physical boundary where outflow breaks linearity
+        margin = 3 * (1.0 / 32) * 2
+        ok = ((X > margin) & (X < 1 - margin) & (Y > margin) & (Y < 1 - margin) & (Z > margin) & (Z < 1 - margin))
+        assert np.all(np.abs(got - exp)[:, ok] <= 1e-13), b
+        if b["level"] == 1 and any(e["dlevel"] == -1 for e in m.neighbors(b["gid"])):
+            ghost = np.pad(np.zeros((n, n, n), bool), g, constant_values=True)
+            checked += int((ok & ghost).sum())    # prolongated ghost cells
+    assert checked > 1000, checked
+
+
+def test_multilevel_periodic_ghosts_are_finite(oracle_mod):
+    """every ghost cell of every block (incl. corners) is written by the exchange"""
+    O = oracle_mod
+    m = _two_level_mesh(O, O.PERIODIC)
+    for b in range(m.num_blocks()):
+        F = np.full((5, 12, 12, 12), np.nan)
+        F[:, 2:-2, 2:-2, 2:-2] = 1.0
+        m.set_state_full(b, F)
+    m.exchange()
+    for b in range(m.num_blocks()):
+        assert np.all(np.isfinite(m.get_state_full(b)))
+
+
+# ---------------------------------------------------------------- AMR (O9)
+def test_amr_blast_prerefinement_and_balance(oracle_mod):
+    O = oracle_mod
+    m = O.Mesh(mesh_nx=(32, 32, 32), block_nx=(8, 8, 8), xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=2,
+               refinement=O.REF_ADAPTIVE, refine_tol=0.1, derefine_tol=0.025, derefine_interval=2)
+    m.set_problem(O.BLAST, [10.0, 0.1, 0.1])
+    lc = m.level_counts(3)
+    assert lc[2] > 0, lc
+    # the blocks containing the blast edge are at the finest level
+    for b in m.blocks():
+        inside = all(b["xmin"][d] < 0.1 and b["xmax"][d] > -0.1 for d in range(3))
+        if inside:
+            assert b["level"] >= 1
+        for e in m.neighbors(b["gid"]):
+            assert abs(e["dlevel"]) <= 1
+    t0 = m.totals()
+    m.step(8)
+    t1 = m.totals()
+    assert abs(t1[0] - t0[0]) <= 1e-12 * t0[0]
+    assert abs(t1[4] - t0[4]) <= 1e-12 * t0[4]
+    flags = m.refine_flags()
+    assert set(np.unique(flags)) <= {-1, 0, 1}
+
+
+def test_derefinement_gate(oracle_mod):
+    """A16: derefinement only when cycle % derefine_interval == 0."""
+    O = oracle_mod
+    m = O.Mesh(mesh_nx=(16, 16, 16), block_nx=(4, 4, 4), max_level=1, refinement=O.REF_ADAPTIVE,
+               regions=[(1, 0.3, 0.7, 0.3, 0.7, 0.3, 0.7)], derefine_interval=3)
+    n0 = m.num_blocks()
+    assert m.level_counts(2)[1] > 0
+    U = O.prim_to_cons([1.0, 0.1, 0.0, 0.0, 1.0], 5 / 3)
+    for b in range(n0):
+        m.set_state(b, np.broadcast_to(U[:, None, None, None], (5, 4, 4, 4)))
+    m.exchange()
+    m.compute_dt()
+    counts = []
+    for c in range(4):
+        m.step(1)
+        counts.append(m.num_blocks())
+        if c == 0:
+            fl = m.refine_flags()
+            lv = [b["level"] for b in m.blocks()]
+            assert all(f == (-1 if l == 1 else 0) for f, l in zip(fl, lv))
+    assert counts[0] == n0 and counts[1] == n0
+    assert counts[2] == 64 and counts[3] == 64
+    # uniform state survives remesh bitwise
+    for b in range(m.num_blocks()):
+        S = m.get_state(b)
+        for v in range(5):
+            assert np.all(S[v] == U[v])
