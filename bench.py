@@ -1,0 +1,319 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 Parthenon-hydro hot path: zone-cycles/s (BASELINE.json metric).
+
+One step = one full RK2 cycle of the hot path (stage 1, ghost exchange, stage 2, ghost
+exchange, CFL dt reduction + conserved totals) over all blocks of every GPU.
+
+Default workload (N=1): BASELINE configs[1] in reading 2b (SURVEY finding 1): 3D blast wave,
+512^3 mesh of 64^3 blocks (512 blocks), all blocks in one launch, fp64.  For N>1 the per-GPU
+work is fixed (weak scaling): the global mesh grows along the Morton axes (1024x512x512, ...),
+so every GPU owns a contiguous Morton range of 512 blocks.  --config 4 selects BASELINE
+configs[3] (256^3 cells per GPU).
+
+    python bench.py --gpus N --steps K --warmup W [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PER_GPU_ROOT = {"2b": (8, 8, 8), "4": (4, 4, 4)}
+SCALE_AXES = [(1, 1, 1), (2, 1, 1), (2, 2, 1), (2, 2, 2), (4, 2, 2), (4, 4, 2), (4, 4, 4), (8, 4, 4)]
+
+
+def workload(cfg, ngpu, n=64):
+    root = PER_GPU_ROOT[cfg]
+    k = {1: 0, 2: 1, 4: 2, 8: 3}.get(ngpu)
+    if k is None:
+        raise SystemExit(f"--gpus {ngpu}: use 1, 2, 4 or 8")
+    ax = SCALE_AXES[k]
+    groot = tuple(root[d] * ax[d] for d in range(3))
+    mesh = tuple(n * r for r in groot)
+    # unit cell width in every direction: domain extents proportional to the mesh
+    L = tuple(m / (n * root[0]) for m in mesh)
+    xmin = tuple(-0.5 * l for l in L)
+    xmax = tuple(0.5 * l for l in L)
+    return dict(mesh_nx=mesh, block_nx=(n, n, n), xmin=xmin, xmax=xmax)
+
+
+BLAST = [10.0, 0.1, 0.1]  # p_in, p_out, radius (A21), centred in the global domain
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler during the timed region (the recipe's clocks line)."""
+
+    def __init__(self, idx):
+        self.idx = idx
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], 0, set()
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"], f[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------------------ oracle legs
+def oracle_sample(cfg_name, steps, warmup, threads):
+    """The CPU oracle (as it stands) on a bounded sample of the workload: the same 64^3 blocks,
+    method and blast problem on a 128^3 periodic mesh (8 blocks); one oracle cycle per step."""
+    import oracle
+    oracle.build()
+    kw = dict(mesh_nx=(128, 128, 128), block_nx=(64, 64, 64), xmin=(-0.25,) * 3, xmax=(0.25,) * 3,
+              nthreads=threads)
+    m = oracle.Mesh(**kw)
+    m.set_problem(oracle.BLAST, BLAST)
+    cells = 128 ** 3
+    for _ in range(warmup):
+        m.step(1)
+    ts = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        m.step(1)
+        ts.append(time.perf_counter() - t0)
+    total = sum(ts)
+    return cells * steps / total, total / steps, "blast, 128^3 periodic mesh of 64^3 blocks (8 blocks), 1 oracle cycle per step"
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = len(os.sched_getaffinity(0))
+    zcs, sec, sample = oracle_sample(args.config, args.steps, args.warmup, threads)
+    line = {
+        "impl": "reference", "metric": "zone-cycles/s", "value": zcs, "unit": "zone-cycles/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": f"oracle sample of {args.config}", "sample": sample},
+        "cpu_baseline": {"value": zcs, "unit": "zone-cycles/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "e2e": {"value": zcs, "unit": "zone-cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ GPU leg
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2202_12309_b200 as P
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            raise SystemExit("launch with torchrun --nproc-per-node N for --gpus N > 1")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.current_stream()
+    W = workload(args.config, world)
+    mesh = P.Mesh(device=local, rank=rank, nranks=world, stream=stream, **W)
+    nglob = mesh.num_blocks()
+    n = W["block_nx"][0]
+    cells = nglob * n ** 3
+    mesh.set_problem(P.BLAST, BLAST)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        mesh.step(1)
+    barrier()
+    l0 = mesh.launch_count()
+    mesh.kernel_timing(True)
+    clk = Clocks(local)
+    clk.start()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    mesh.step(args.steps)
+    e1.record(stream)
+    barrier()
+    clocks = clk.stop()
+    ms = e0.elapsed_time(e1)
+    stage_ms, stage_n, exch_ms, exch_n = mesh.kernel_timing(False)
+    launches = mesh.launch_count() - l0
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = cells * args.steps / (ms_max * 1e-3)
+
+    # correctness guard: the run must still be physical and conserve mass
+    hist = mesh.history()
+    t0 = hist[0, 2] if len(hist) else 0.0
+    mass_drift = abs(hist[-1, 2] - t0) / t0 if len(hist) else 0.0
+
+    # ---- end-to-end through the public host-buffer call (H2D + cycle + D2H every step)
+    nloc = mesh.num_local()
+    e2e = None
+    if not args.no_e2e:
+        hin = torch.empty((nloc, 5, n, n, n), dtype=torch.float64).pin_memory()
+        hout = torch.empty_like(hin).pin_memory()
+        # initial state from the device (rank-local gather)
+        gids = [b["gid"] for b in mesh.blocks() if b["rank"] == rank]
+        for i, g in enumerate(gids):
+            hin[i].copy_(torch.from_numpy(mesh.get_state(g)))
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        mesh.step_host(hin, hout, 1)  # warm-up
+        barrier()
+        t_0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            mesh.step_host(hin, hout, 1)
+        torch.cuda.synchronize()
+        dt_e2e = time.perf_counter() - t_0
+        tt = torch.tensor([dt_e2e], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        nbytes = hin.numel() * 8
+        e2e = {"value": cells * e2e_steps / float(tt.item()), "unit": "zone-cycles/s",
+               "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+               "note": "each step: H2D of the rank's whole state, refresh + 1 cycle, D2H of the state (ph_step_host)"}
+
+    # ---- roofline of the dominant kernel (the fused stage kernel)
+    peak, peak_kind = measured_peaks()
+    r = ((n + 4) / n) ** 3
+    nloc_cells = nloc * n ** 3
+    # algorithmic bytes per stage launch: read U with halo (r*40 B/cell), write 40 B/cell,
+    # stage 2 also reads U^n at the cell (40 B/cell): averaged over the two stages
+    stage_bytes = nloc_cells * (r * 40.0 + 60.0)
+    stage_avg_ms = stage_ms / max(stage_n, 1)
+    achieved = stage_bytes / (stage_avg_ms * 1e-3) / 1e9 if stage_n else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "stage_kernel_traffic.json")
+    if os.path.exists(tp):
+        try:
+            d = json.load(open(tp))
+            if d.get("workload") == args.config and d.get("n") == n:
+                traffic = d.get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    b_ghost = (6 * r - 1) * 40.0
+    line = {
+        "metric": "zone-cycles/s", "value": value, "unit": "zone-cycles/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"blast 3D, {'512^3' if args.config == '2b' else '256^3'} cells per GPU in 64^3 blocks "
+                               f"(BASELINE configs[{1 if args.config == '2b' else 3}]"
+                               f"{', reading 2b' if args.config == '2b' else ''}), global mesh {W['mesh_nx']}, "
+                               f"{nglob} blocks, all local blocks per launch, PLM-minmod + HLLE + RK2, CFL 0.3",
+                   "global_blocks": nglob, "block": n, "nghost": 2,
+                   "l2": "inputs larger than L2 (state %.1f GB per GPU vs 126 MB L2)" % (2 * nloc * 5 * (n + 4) ** 3 * 8 / 1e9),
+                   "parallelism": f"morton-partition dp{world}"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                     "kernel": "stage_kernel (fused cons->prim, PLM, HLLE x/y/z, divergence, RK combine)",
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                     "algorithmic_bytes_per_launch": stage_bytes,
+                     "stage_ms_avg": stage_avg_ms, "stage_share_of_step": stage_ms / ms if ms else None,
+                     "exchange_ms_per_step": exch_ms / args.steps,
+                     "cycle_hbm_frac_B_ghost": value / world * b_ghost / (peak * 1e9),
+                     "B_ghost_bytes_per_zone_cycle": b_ghost},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "e2e": e2e,
+        "mass_drift": mass_drift,
+    }
+    # ---- CPU baseline: the oracle on the host cores, rank 0 at N=1 only
+    if world == 1 and not args.no_cpu:
+        threads = len(os.sched_getaffinity(0))
+        zcs, sec, sample = oracle_sample(args.config, args.cpu_steps, 0, threads)
+        line["cpu_baseline"] = {"value": zcs, "unit": "zone-cycles/s", "cores": threads, "kind": "oracle",
+                                "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    mesh.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="2b", choices=["2b", "4"])
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: W >= 3 warm-up steps required by the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,1093 @@
+// api.cu -- C ABI (include/ph.h): mesh/plan construction, device block pool, the per-cycle
+// schedule (O5) and NCCL plumbing.  Hot work runs in kernels.cu.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <array>
+#include <vector>
+
+#include "../../include/ph.h"
+#include "device.cuh"
+#include "mesh.hpp"
+
+namespace ph {
+constexpr int TX = TILE_X, TY = TILE_Y;
+}
+
+using namespace ph;
+
+static thread_local std::string g_err;
+static ph_status fail(ph_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+#define CU(x)                                                                                         \
+  do {                                                                                                \
+    cudaError_t e_ = (x);                                                                             \
+    if (e_ != cudaSuccess) return fail(PH_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define NC(x)                                                                                          \
+  do {                                                                                                 \
+    ncclResult_t r_ = (x);                                                                             \
+    if (r_ != ncclSuccess) return fail(PH_ERR_COMM, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+#define TRY(x)                    \
+  do {                            \
+    ph_status s_ = (x);           \
+    if (s_ != PH_OK) return s_;   \
+  } while (0)
+
+struct Phase {
+  std::vector<XTask> tasks;
+  std::vector<Chunk> chunks;
+  XTask* d_tasks = nullptr;
+  Chunk* d_chunks = nullptr;
+  int nchunks() const { return (int)chunks.size(); }
+};
+
+struct ph_mesh {
+  ph_config cfg;
+  std::vector<double> regions;
+  MeshCfg mc;
+  Tree* tree = nullptr;
+  std::vector<BlockInfo> blocks;
+  std::unordered_map<LocKey, int64_t> gid_of;
+  std::vector<int64_t> local_gids;  // slot -> gid
+  Geom G;
+  int rank = 0, nranks = 1;
+  bool host_only = false;
+  bool multilevel = false;
+  bool cross_rank_reflux = false;
+  cudaStream_t stream = nullptr, comm_stream = nullptr;
+  cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
+  ncclComm_t comm = nullptr;
+  // device memory
+  std::vector<void*> allocs;
+  double *U0 = nullptr, *U1 = nullptr, *C = nullptr, *fbuf = nullptr;
+  double *partials = nullptr, *my6 = nullptr, *all6 = nullptr, *tot5 = nullptr, *hist = nullptr, *stage_buf = nullptr;
+  BlockMeta* d_meta = nullptr;
+  int* d_slots = nullptr;
+  CycleState* d_st = nullptr;
+  ErrWord* d_err = nullptr;
+  double *sbuf = nullptr, *rbuf = nullptr;
+  int64_t sbuf_n = 0, rbuf_n = 0;
+  int hist_cap = 1 << 16;
+  int n_cslots = 0, n_fslots = 0;
+  std::vector<BlockMeta> meta;
+  // plan
+  Phase pack, local, unpack, b1, b2, pro, bcf;
+  std::vector<int64_t> send_off, send_cnt, recv_off, recv_cnt;  // per peer, doubles
+  std::vector<uint64_t> send_hash, recv_hash;
+  std::vector<RefluxTask> reflux[3];
+  RefluxTask* d_reflux[3] = {nullptr, nullptr, nullptr};
+  // stage launch geometry
+  int ntx = 1, nty = 1, nkc = 1, KC = 1;
+  int stage_ctas = 0;
+  int pack_size = 0;
+  int64_t partials_n = 0;
+  // bookkeeping
+  int64_t launches = 0;
+  bool have_state = false;
+  std::vector<int8_t> last_flags;
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> t_stage, t_exch;
+  std::vector<cudaEvent_t> ev_pool;
+};
+
+/* ------------------------------------------------------------------------------- helpers */
+static ph_status dalloc(ph_mesh* m, void** p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) return PH_OK;
+  if (m->cfg.dev_alloc) {
+    *p = m->cfg.dev_alloc(bytes, m->cfg.alloc_ctx);
+    if (!*p) return fail(PH_ERR_OOM, "dev_alloc returned NULL for " + std::to_string(bytes) + " bytes");
+  } else {
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) return fail(PH_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  }
+  m->allocs.push_back(*p);
+  return PH_OK;
+}
+
+template <class T>
+static ph_status upload(ph_mesh* m, T** d, const std::vector<T>& h) {
+  *d = nullptr;
+  if (h.empty()) return PH_OK;
+  TRY(dalloc(m, (void**)d, h.size() * sizeof(T)));
+  CU(cudaMemcpy(*d, h.data(), h.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return PH_OK;
+}
+
+static void free_all(ph_mesh* m) {
+  if (m->host_only) return;
+  cudaStreamSynchronize(m->stream);
+  for (void* p : m->allocs) {
+    if (m->cfg.dev_free) m->cfg.dev_free(p, m->cfg.alloc_ctx);
+    else cudaFree(p);
+  }
+  m->allocs.clear();
+}
+
+static uint64_t mix(uint64_t h, uint64_t x) {
+  h ^= x + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+  return h;
+}
+
+static void add_chunks(Phase& P, const XTask& t) {
+  int id = (int)P.tasks.size();
+  P.tasks.push_back(t);
+  for (int b = 0; b < t.ncell; b += XCHUNK) P.chunks.push_back(Chunk{id, b});
+}
+
+static int bc_bits(const ph_mesh* m, const BlockInfo& b) {
+  int bits = 0;
+  for (int d = 0; d < 3; ++d) {
+    int lo = b.phys_lo[d] ? (m->cfg.bc_inner[d] == PH_BC_REFLECT ? 2 : 1) : 0;
+    int hi = b.phys_hi[d] ? (m->cfg.bc_outer[d] == PH_BC_REFLECT ? 2 : 1) : 0;
+    bits |= (lo | (hi << 2)) << (4 * d);
+  }
+  return bits;
+}
+
+/* geometry of one neighbour entry as seen by destination block b (O7 phase A) */
+static XTask entry_task(const ph_mesh* m, const BlockInfo& b, const Neighbor& e) {
+  XTask t{};
+  const int* n = m->G.n;
+  const int g = m->G.g, cg = m->G.cg;
+  if (e.dlevel == 0) {
+    t.kind = T_COPY;
+    for (int d = 0; d < 3; ++d) {
+      if (e.off[d] < 0) { t.lo[d] = -g; t.ext[d] = g; t.so[d] = n[d]; }
+      else if (e.off[d] > 0) { t.lo[d] = n[d]; t.ext[d] = g; t.so[d] = -n[d]; }
+      else { t.lo[d] = 0; t.ext[d] = n[d]; t.so[d] = 0; }
+    }
+  } else if (e.dlevel == 1) {
+    t.kind = T_RESTRICT;
+    int f = 0;
+    for (int d = 0; d < 3; ++d) {
+      int ch = e.off[d] ? (e.off[d] == 1 ? 0 : 1) : e.fine[f++];
+      if (e.off[d] < 0) { t.lo[d] = -g; t.ext[d] = g; }
+      else if (e.off[d] > 0) { t.lo[d] = n[d]; t.ext[d] = g; }
+      else { t.lo[d] = ch * n[d] / 2; t.ext[d] = n[d] / 2; }
+      t.so[d] = (2 * e.off[d] + ch) * n[d];
+    }
+  } else {
+    t.kind = T_CCOPY;
+    for (int d = 0; d < 3; ++d) {
+      int nc = m->G.nc[d];
+      if (e.off[d] < 0) { t.lo[d] = -cg; t.ext[d] = cg; }
+      else if (e.off[d] > 0) { t.lo[d] = nc; t.ext[d] = cg; }
+      else { t.lo[d] = 0; t.ext[d] = nc; }
+      int64_t lx = b.loc.x[d];
+      int64_t a = lx + e.off[d];
+      int64_t P = (a >= 0) ? a / 2 : -((-a + 1) / 2);
+      t.so[d] = (int)(lx * nc - P * n[d]);
+    }
+  }
+  t.ncell = t.ext[0] * t.ext[1] * t.ext[2];
+  return t;
+}
+
+static bool region_physical(const BlockInfo& b, const int o[3]) {
+  for (int d = 0; d < 3; ++d) {
+    if (o[d] < 0 && b.phys_lo[d]) return true;
+    if (o[d] > 0 && b.phys_hi[d]) return true;
+  }
+  return false;
+}
+
+/* Build the per-exchange plan of this rank (fill-in-one phases A-D, remote first). */
+static ph_status build_plan(ph_mesh* m) {
+  const int R = m->nranks, me = m->rank;
+  for (Phase* P : {&m->pack, &m->local, &m->unpack, &m->b1, &m->b2, &m->pro, &m->bcf}) {
+    P->tasks.clear();
+    P->chunks.clear();
+  }
+  m->send_off.assign(R, 0);
+  m->send_cnt.assign(R, 0);
+  m->recv_off.assign(R, 0);
+  m->recv_cnt.assign(R, 0);
+  m->send_hash.assign(R, 0);
+  m->recv_hash.assign(R, 0);
+  for (int d = 0; d < 3; ++d) m->reflux[d].clear();
+  m->cross_rank_reflux = false;
+  // slots
+  m->local_gids.clear();
+  for (auto& b : m->blocks)
+    if (b.rank == me) m->local_gids.push_back(b.gid);
+  const int64_t nloc = (int64_t)m->local_gids.size();
+  // coarse staging and face-flux slots
+  std::vector<int> cslot(m->blocks.size(), -1);
+  std::vector<std::array<int, 6>> fslot(m->blocks.size());
+  m->n_cslots = 0;
+  m->n_fslots = 0;
+  m->multilevel = false;
+  for (auto& b : m->blocks) {
+    fslot[b.gid].fill(-1);
+    for (auto& e : b.nbrs)
+      if (e.dlevel != 0) m->multilevel = true;
+  }
+  for (auto& b : m->blocks) {
+    if (b.rank != me) continue;
+    if (b.has_coarser) cslot[b.gid] = m->n_cslots++;
+    for (auto& e : b.nbrs) {
+      int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
+      if (nz != 1 || e.dlevel == 0) continue;
+      int d = e.off[0] ? 0 : (e.off[1] ? 1 : 2);
+      int face = 2 * d + (e.off[d] > 0 ? 1 : 0);
+      if (fslot[b.gid][face] < 0) fslot[b.gid][face] = m->n_fslots++;
+    }
+  }
+  // ---- phase A: per destination block (gid order), entries in canonical order
+  std::vector<int64_t> soff(R, 0), roff(R, 0);
+  std::vector<int> pack_peer, unpack_peer;
+  for (auto& b : m->blocks) {
+    for (auto& e : b.nbrs) {
+      const BlockInfo& s = m->blocks[e.gid];
+      bool dst_here = (b.rank == me), src_here = (s.rank == me);
+      if (!dst_here && !src_here) continue;
+      XTask t = entry_task(m, b, e);
+      int cs = (t.kind == T_CCOPY) ? cslot[b.gid] : (int)b.local;
+      if (dst_here && src_here) {
+        t.dst_slot = cs;
+        t.src_slot = (int)s.local;
+        add_chunks(m->local, t);
+      } else if (src_here) {  // pack for b.rank
+        int peer = b.rank;
+        t.dst_slot = -1;
+        t.src_slot = (int)s.local;
+        t.buf = soff[peer];
+        soff[peer] += (int64_t)NVAR * t.ncell;
+        m->send_hash[peer] = mix(m->send_hash[peer], (uint64_t)b.gid * 64 + (uint64_t)(&e - &b.nbrs[0]));
+        pack_peer.push_back(peer);
+        add_chunks(m->pack, t);
+      } else {  // unpack from s.rank
+        int peer = s.rank;
+        t.kind = (t.kind == T_CCOPY) ? T_UNPACK_C : T_UNPACK_U;
+        t.dst_slot = cs;
+        t.src_slot = -1;
+        t.buf = roff[peer];
+        roff[peer] += (int64_t)NVAR * t.ncell;
+        m->recv_hash[peer] = mix(m->recv_hash[peer], (uint64_t)b.gid * 64 + (uint64_t)(&e - &b.nbrs[0]));
+        unpack_peer.push_back(peer);
+        add_chunks(m->unpack, t);
+      }
+    }
+  }
+  // per-peer buffer offsets (peer-major)
+  int64_t so = 0, ro = 0;
+  for (int p = 0; p < R; ++p) {
+    m->send_off[p] = so;
+    m->send_cnt[p] = soff[p];
+    so += soff[p];
+    m->recv_off[p] = ro;
+    m->recv_cnt[p] = roff[p];
+    ro += roff[p];
+  }
+  for (size_t i = 0; i < m->pack.tasks.size(); ++i) m->pack.tasks[i].buf += m->send_off[pack_peer[i]];
+  for (size_t i = 0; i < m->unpack.tasks.size(); ++i) m->unpack.tasks[i].buf += m->recv_off[unpack_peer[i]];
+  m->sbuf_n = so;
+  m->rbuf_n = ro;
+  // ---- phases B, C, D per local block
+  const int* n = m->G.n;
+  const int g = m->G.g, cg = m->G.cg;
+  for (int64_t gid : m->local_gids) {
+    const BlockInfo& b = m->blocks[gid];
+    int kind[27];
+    for (int q = 0; q < 27; ++q) kind[q] = -2;
+    for (auto& e : b.nbrs) kind[(e.off[2] + 1) * 9 + (e.off[1] + 1) * 3 + (e.off[0] + 1)] = e.dlevel;
+    bool anyphys = false;
+    for (int d = 0; d < 3; ++d) anyphys = anyphys || b.phys_lo[d] || b.phys_hi[d];
+    int bits = bc_bits(m, b);
+    if (b.has_coarser) {
+      int cs = cslot[gid];
+      XTask t{};
+      t.kind = T_CRESTRICT;
+      t.dst_slot = cs;
+      t.src_slot = (int)b.local;
+      for (int d = 0; d < 3; ++d) { t.lo[d] = 0; t.ext[d] = m->G.nc[d]; t.so[d] = 0; }
+      t.ncell = t.ext[0] * t.ext[1] * t.ext[2];
+      add_chunks(m->b1, t);
+      for (int q = 0; q < 27; ++q) {
+        if (q == 13 || kind[q] == -2 || kind[q] == -1) continue;
+        int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
+        XTask r{};
+        r.kind = T_CRESTRICT;
+        r.dst_slot = cs;
+        r.src_slot = (int)b.local;
+        for (int d = 0; d < 3; ++d) {
+          if (o[d] < 0) { r.lo[d] = -1; r.ext[d] = 1; }
+          else if (o[d] > 0) { r.lo[d] = m->G.nc[d]; r.ext[d] = 1; }
+          else { r.lo[d] = 0; r.ext[d] = m->G.nc[d]; }
+          r.so[d] = 0;
+        }
+        r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
+        add_chunks(m->b1, r);
+      }
+      for (int q = 0; q < 27 && anyphys; ++q) {
+        if (q == 13) continue;
+        int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
+        if (!region_physical(b, o)) continue;
+        XTask r{};
+        r.kind = T_BC_COARSE;
+        r.dst_slot = cs;
+        r.src_slot = cs;
+        r.bc = bits;
+        for (int d = 0; d < 3; ++d) {
+          if (o[d] < 0) { r.lo[d] = -cg; r.ext[d] = cg; }
+          else if (o[d] > 0) { r.lo[d] = m->G.nc[d]; r.ext[d] = cg; }
+          else { r.lo[d] = 0; r.ext[d] = m->G.nc[d]; }
+        }
+        r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
+        add_chunks(m->b2, r);
+      }
+      for (int q = 0; q < 27; ++q) {
+        if (q == 13 || kind[q] != -1) continue;
+        int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
+        XTask r{};
+        r.kind = T_PROLONG;
+        r.dst_slot = (int)b.local;
+        r.src_slot = cs;
+        for (int d = 0; d < 3; ++d) {
+          if (o[d] < 0) { r.lo[d] = -1; r.ext[d] = 1; }
+          else if (o[d] > 0) { r.lo[d] = m->G.nc[d]; r.ext[d] = 1; }
+          else { r.lo[d] = 0; r.ext[d] = m->G.nc[d]; }
+        }
+        r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
+        add_chunks(m->pro, r);
+      }
+    }
+    if (anyphys) {
+      for (int q = 0; q < 27; ++q) {
+        if (q == 13) continue;
+        int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
+        if (!region_physical(b, o)) continue;
+        XTask r{};
+        r.kind = T_BC_FINE;
+        r.dst_slot = (int)b.local;
+        r.src_slot = (int)b.local;
+        r.bc = bits;
+        for (int d = 0; d < 3; ++d) {
+          if (o[d] < 0) { r.lo[d] = -g; r.ext[d] = g; }
+          else if (o[d] > 0) { r.lo[d] = n[d]; r.ext[d] = g; }
+          else { r.lo[d] = 0; r.ext[d] = n[d]; }
+        }
+        r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
+        add_chunks(m->bcf, r);
+      }
+    }
+    // reflux tasks (coarse side)
+    for (auto& e : b.nbrs) {
+      int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
+      if (nz != 1 || e.dlevel != 1) continue;
+      int d = e.off[0] ? 0 : (e.off[1] ? 1 : 2);
+      const BlockInfo& f = m->blocks[e.gid];
+      if (f.rank != me) {  // needs a per-stage flux message between ranks (not built yet)
+        m->cross_rank_reflux = true;
+        continue;
+      }
+      int ta = (d == 0) ? 1 : 0, tb = (d == 2) ? 1 : 2;
+      RefluxTask rt{};
+      rt.cslot = (int)b.local;
+      rt.dir = d;
+      rt.side = e.off[d];
+      rt.cfs = fslot[gid][2 * d + (e.off[d] > 0 ? 1 : 0)];
+      rt.ffs = fslot[e.gid][2 * d + (e.off[d] > 0 ? 0 : 1)];
+      rt.t0lo = e.fine[0] * n[ta] / 2;
+      rt.t1lo = e.fine[1] * n[tb] / 2;
+      m->reflux[d].push_back(rt);
+    }
+  }
+  // block metadata
+  m->meta.assign(nloc, BlockMeta{});
+  for (int64_t s = 0; s < nloc; ++s) {
+    const BlockInfo& b = m->blocks[m->local_gids[s]];
+    BlockMeta& M = m->meta[s];
+    for (int d = 0; d < 3; ++d) {
+      M.idx[d] = 1.0 / b.dx[d];
+      M.dx[d] = b.dx[d];
+      M.xmin[d] = b.xmin[d];
+    }
+    M.dV = (b.dx[0] * b.dx[1]) * b.dx[2];
+    M.gid = b.gid;
+    M.level = b.loc.level;
+    M.cslot = cslot[b.gid];
+    for (int f = 0; f < 6; ++f) M.fslot[f] = fslot[b.gid][f];
+  }
+  return PH_OK;
+}
+
+static ph_status upload_phase(ph_mesh* m, Phase& P) {
+  TRY(upload(m, &P.d_tasks, P.tasks));
+  TRY(upload(m, &P.d_chunks, P.chunks));
+  return PH_OK;
+}
+
+/* (Re)allocate every device structure that depends on the mesh (creation and remesh). */
+static ph_status setup_device(ph_mesh* m) {
+  const int64_t nloc = (int64_t)m->local_gids.size();
+  const Geom& G = m->G;
+  TRY(dalloc(m, (void**)&m->U0, (size_t)std::max<int64_t>(nloc, 1) * G.bstride * sizeof(double)));
+  TRY(dalloc(m, (void**)&m->U1, (size_t)std::max<int64_t>(nloc, 1) * G.bstride * sizeof(double)));
+  CU(cudaMemsetAsync(m->U0, 0, (size_t)std::max<int64_t>(nloc, 1) * G.bstride * sizeof(double), m->stream));
+  CU(cudaMemsetAsync(m->U1, 0, (size_t)std::max<int64_t>(nloc, 1) * G.bstride * sizeof(double), m->stream));
+  if (m->n_cslots) TRY(dalloc(m, (void**)&m->C, (size_t)m->n_cslots * G.cbstride * sizeof(double)));
+  if (m->n_fslots) TRY(dalloc(m, (void**)&m->fbuf, (size_t)m->n_fslots * G.fstride * sizeof(double)));
+  TRY(upload(m, &m->d_meta, m->meta));
+  std::vector<int> slots(nloc);
+  for (int64_t s = 0; s < nloc; ++s) slots[s] = (int)s;
+  TRY(upload(m, &m->d_slots, slots));
+  for (Phase* P : {&m->pack, &m->local, &m->unpack, &m->b1, &m->b2, &m->pro, &m->bcf}) TRY(upload_phase(m, *P));
+  for (int d = 0; d < 3; ++d) TRY(upload(m, &m->d_reflux[d], m->reflux[d]));
+  if (m->sbuf_n) TRY(dalloc(m, (void**)&m->sbuf, m->sbuf_n * sizeof(double)));
+  if (m->rbuf_n) TRY(dalloc(m, (void**)&m->rbuf, m->rbuf_n * sizeof(double)));
+  // stage launch geometry
+  m->ntx = (G.n[0] + TX - 1) / TX;
+  m->nty = (G.n[1] + TY - 1) / TY;
+  int64_t base = std::max<int64_t>(nloc, 1) * m->ntx * m->nty;
+  int nkc = 1;
+  while (base * nkc < 1184 && G.n[2] / (nkc * 2) >= 4) nkc *= 2;
+  m->KC = (G.n[2] + nkc - 1) / nkc;
+  m->nkc = (G.n[2] + m->KC - 1) / m->KC;
+  m->pack_size = (m->cfg.pack_size > 0) ? (int)std::min<int64_t>(m->cfg.pack_size, nloc) : (int)nloc;
+  m->stage_ctas = (int)(nloc * m->ntx * m->nty * m->nkc);
+  m->partials_n = std::max<int64_t>({(int64_t)m->stage_ctas, nloc * G.n[2], 1});
+  TRY(dalloc(m, (void**)&m->partials, m->partials_n * 6 * sizeof(double)));
+  CU(cudaMemsetAsync(m->partials, 0, m->partials_n * 6 * sizeof(double), m->stream));
+  TRY(dalloc(m, (void**)&m->stage_buf, (size_t)std::max<int64_t>(nloc, 1) * NVAR * G.n[0] * G.n[1] * G.n[2] * sizeof(double)));
+  return PH_OK;
+}
+
+static ph_status setup_persistent(ph_mesh* m) {
+  TRY(dalloc(m, (void**)&m->my6, 8 * sizeof(double)));
+  TRY(dalloc(m, (void**)&m->all6, (size_t)6 * m->nranks * sizeof(double)));
+  TRY(dalloc(m, (void**)&m->tot5, 8 * sizeof(double)));
+  TRY(dalloc(m, (void**)&m->hist, (size_t)m->hist_cap * 7 * sizeof(double)));
+  TRY(dalloc(m, (void**)&m->d_st, sizeof(CycleState)));
+  TRY(dalloc(m, (void**)&m->d_err, sizeof(ErrWord)));
+  CU(cudaMemsetAsync(m->d_st, 0, sizeof(CycleState), m->stream));
+  CU(cudaMemsetAsync(m->d_err, 0, sizeof(ErrWord), m->stream));
+  return PH_OK;
+}
+
+static ph_status check_err(const ph_mesh* m) {
+  if (m->host_only) return PH_OK;
+  CU(cudaStreamSynchronize(m->stream));
+  ErrWord e;
+  CU(cudaMemcpy(&e, m->d_err, sizeof(e), cudaMemcpyDeviceToHost));
+  if (e.flag) {
+    char buf[256];
+    snprintf(buf, sizeof buf, "non-positive density or pressure at gid %lld cell (k,j,i)=(%d,%d,%d) stage %d",
+             (long long)e.gid, e.k, e.j, e.i, e.stage);
+    return fail(PH_ERR_PHYSICS, buf);
+  }
+  return PH_OK;
+}
+
+/* ------------------------------------------------------------------------------- exchange */
+static cudaEvent_t pool_event(ph_mesh* m) {
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  m->ev_pool.push_back(e);
+  return e;
+}
+
+static ph_status exchange(ph_mesh* m, double* U) {
+  const Geom& G = m->G;
+  XArgs a{};
+  a.U = U;
+  a.C = m->C;
+  a.sbuf = m->sbuf;
+  a.rbuf = m->rbuf;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  if (m->timing) {
+    t0 = pool_event(m);
+    t1 = pool_event(m);
+    CU(cudaEventRecord(t0, m->stream));
+  }
+  auto run = [&](Phase& P, cudaStream_t s) -> ph_status {
+    if (P.nchunks() == 0) return PH_OK;
+    a.tasks = P.d_tasks;
+    a.chunks = P.d_chunks;
+    CU(launch_xfill(P.nchunks(), a, G, s));
+    m->launches++;
+    return PH_OK;
+  };
+  const bool remote = (m->nranks > 1) && (m->sbuf_n > 0 || m->rbuf_n > 0);
+  if (remote) {
+    // remote buffers first, then the local copies overlap the NCCL transfer
+    TRY(run(m->pack, m->stream));
+    CU(cudaEventRecord(m->ev_pack, m->stream));
+    CU(cudaStreamWaitEvent(m->comm_stream, m->ev_pack, 0));
+    NC(ncclGroupStart());
+    for (int p = 0; p < m->nranks; ++p) {
+      if (p == m->rank) continue;
+      if (m->send_cnt[p]) NC(ncclSend(m->sbuf + m->send_off[p], m->send_cnt[p], ncclDouble, p, m->comm, m->comm_stream));
+      if (m->recv_cnt[p]) NC(ncclRecv(m->rbuf + m->recv_off[p], m->recv_cnt[p], ncclDouble, p, m->comm, m->comm_stream));
+    }
+    NC(ncclGroupEnd());
+    CU(cudaEventRecord(m->ev_comm, m->comm_stream));
+  }
+  TRY(run(m->local, m->stream));
+  if (remote) {
+    CU(cudaStreamWaitEvent(m->stream, m->ev_comm, 0));
+    TRY(run(m->unpack, m->stream));
+  }
+  TRY(run(m->b1, m->stream));
+  TRY(run(m->b2, m->stream));
+  TRY(run(m->pro, m->stream));
+  TRY(run(m->bcf, m->stream));
+  if (m->timing) {
+    CU(cudaEventRecord(t1, m->stream));
+    m->t_exch.push_back({t0, t1});
+  }
+  return PH_OK;
+}
+
+/* rank reduce -> allgather -> finalize (dt min and totals) */
+static ph_status reduce_finalize(ph_mesh* m, int ncta, int mode) {
+  CU(launch_rank_reduce(m->partials, ncta, m->nranks > 1 ? m->my6 : m->all6, m->stream));
+  m->launches++;
+  if (m->nranks > 1) NC(ncclAllGather(m->my6, m->all6, 6, ncclDouble, m->comm, m->stream));
+  CU(launch_finalize(m->all6, m->nranks, m->d_st, m->hist, m->hist_cap, m->G.cfl, mode, m->tot5, m->stream));
+  m->launches++;
+  return PH_OK;
+}
+
+static ph_status standalone_reduce(ph_mesh* m, double* U, int mode) {
+  int nloc = (int)m->local_gids.size();
+  if (nloc > 0) {
+    CU(launch_reduce(U, m->d_meta, nloc, m->partials, m->d_err, m->G, m->stream));
+    m->launches++;
+  }
+  return reduce_finalize(m, nloc * m->G.n[2], mode);
+}
+
+/* one stage over all local blocks, pack by pack (a2-a5) */
+static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a0, double b1, double cdt,
+                           bool reduce, int stage) {
+  const int nloc = (int)m->local_gids.size();
+  const int per_blk = m->ntx * m->nty * m->nkc;
+  for (int p0 = 0; p0 < nloc; p0 += m->pack_size) {
+    int np = std::min(m->pack_size, nloc - p0);
+    StageArgs A{};
+    A.Uin = Uin;
+    A.U0 = m->U0;
+    A.Uout = Uout;
+    A.meta = m->d_meta;
+    A.slots = m->d_slots + p0;
+    A.st = m->d_st;
+    A.fbuf = m->fbuf;
+    A.partials = m->partials;
+    A.err = m->d_err;
+    A.a0 = a0;
+    A.b1 = b1;
+    A.cdt = cdt;
+    A.ntx = m->ntx;
+    A.nty = m->nty;
+    A.nkc = m->nkc;
+    A.KC = m->KC;
+    A.cta_base = p0 * per_blk;
+    A.stage = stage;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (m->timing) {
+      t0 = pool_event(m);
+      t1 = pool_event(m);
+      CU(cudaEventRecord(t0, m->stream));
+    }
+    CU(launch_stage(m->cfg.recon, reduce, a0 != 0.0, np * per_blk, A, m->G, m->stream));
+    m->launches++;
+    if (m->timing) {
+      CU(cudaEventRecord(t1, m->stream));
+      m->t_stage.push_back({t0, t1});
+    }
+  }
+  if (m->multilevel) {
+    for (int d = 0; d < 3; ++d) {
+      if (m->reflux[d].empty()) continue;
+      CU(launch_reflux((int)m->reflux[d].size(), m->d_reflux[d], Uout, m->d_meta, m->fbuf, m->d_st, cdt, m->G,
+                       m->stream));
+      m->launches++;
+    }
+  }
+  return PH_OK;
+}
+
+static ph_status one_cycle(ph_mesh* m) {
+  CU(launch_cycle_begin(m->d_st, 0.0, 0, m->stream));
+  m->launches++;
+  const bool fuse_reduce = !m->multilevel;
+  const int nloc = (int)m->local_gids.size();
+  if (m->cfg.integrator == PH_INT_VL2) {
+    TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, 0.5, false, 1));
+    TRY(exchange(m, m->U1));
+    TRY(run_stage(m, m->U1, m->U0, 1.0, 0.0, 1.0, fuse_reduce, 2));
+  } else {
+    TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, 1.0, false, 1));
+    TRY(exchange(m, m->U1));
+    TRY(run_stage(m, m->U1, m->U0, 0.5, 0.5, 0.5, fuse_reduce, 2));
+  }
+  TRY(exchange(m, m->U0));
+  if (fuse_reduce) TRY(reduce_finalize(m, nloc > 0 ? m->stage_ctas : 0, 1));
+  else TRY(standalone_reduce(m, m->U0, 1));
+  return PH_OK;
+}
+
+/* ------------------------------------------------------------------------------- C ABI */
+extern "C" {
+
+const char* ph_last_error(void) { return g_err.c_str(); }
+
+ph_status ph_nccl_unique_id(void* out, int32_t cap) {
+  if (!out || cap < (int32_t)sizeof(ncclUniqueId)) return fail(PH_ERR_INVALID_ARG, "need 128 bytes");
+  ncclUniqueId id;
+  NC(ncclGetUniqueId(&id));
+  memcpy(out, &id, sizeof id);
+  return PH_OK;
+}
+
+ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
+  if (!cfg || !out) return fail(PH_ERR_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (cfg->abi_version != PH_ABI_VERSION) return fail(PH_ERR_INVALID_ARG, "abi_version mismatch");
+  if (cfg->nghost != 2) return fail(PH_ERR_CONFIG, "nghost must be 2 (PLM, A8)");
+  if (!(cfg->gamma > 1.0) || !(cfg->cfl > 0.0)) return fail(PH_ERR_CONFIG, "gamma must exceed 1 and cfl be positive");
+  if (cfg->nranks < 1 || cfg->nranks > 64 || cfg->rank < 0 || cfg->rank >= cfg->nranks)
+    return fail(PH_ERR_INVALID_ARG, "bad rank / nranks");
+  if (cfg->recon < 0 || cfg->recon > 2 || cfg->integrator < 0 || cfg->integrator > 1)
+    return fail(PH_ERR_CONFIG, "unknown recon / integrator");
+  if (cfg->max_level < 0 || cfg->max_level > 10) return fail(PH_ERR_CONFIG, "max_level out of range");
+  MeshCfg mc{};
+  for (int d = 0; d < 3; ++d) {
+    if (cfg->block_nx[d] < cfg->nghost || cfg->mesh_nx[d] <= 0 || cfg->mesh_nx[d] % cfg->block_nx[d] != 0)
+      return fail(PH_ERR_CONFIG, "block size does not tile the root grid (S:144)");
+    if ((cfg->bc_inner[d] == PH_BC_PERIODIC) != (cfg->bc_outer[d] == PH_BC_PERIODIC))
+      return fail(PH_ERR_CONFIG, "periodic boundaries must be paired");
+    for (int bc : {cfg->bc_inner[d], cfg->bc_outer[d]})
+      if (bc < 0 || bc > 2) return fail(PH_ERR_CONFIG, "unknown boundary tag (S:414)");
+    if (cfg->max_level > 0 && (cfg->block_nx[d] % 2 || cfg->block_nx[d] < 2 * cfg->nghost))
+      return fail(PH_ERR_CONFIG, "refinement needs even block sizes >= 2*nghost");
+    mc.n[d] = cfg->block_nx[d];
+    mc.nrb[d] = cfg->mesh_nx[d] / cfg->block_nx[d];
+    mc.periodic[d] = cfg->bc_inner[d] == PH_BC_PERIODIC;
+    mc.bc_in[d] = cfg->bc_inner[d];
+    mc.bc_out[d] = cfg->bc_outer[d];
+    mc.xmin[d] = cfg->xmin[d];
+    mc.xmax[d] = cfg->xmax[d];
+    if (!(cfg->xmax[d] > cfg->xmin[d])) return fail(PH_ERR_CONFIG, "empty domain");
+    if ((mc.nrb[d] << cfg->max_level) >= (1 << 19)) return fail(PH_ERR_CONFIG, "too many blocks per dim");
+  }
+  mc.max_level = cfg->max_level;
+  ph_mesh* m = new ph_mesh();
+  m->cfg = *cfg;
+  if (cfg->nregions > 0 && cfg->regions) m->regions.assign(cfg->regions, cfg->regions + 7 * cfg->nregions);
+  m->cfg.regions = nullptr;
+  m->mc = mc;
+  m->rank = cfg->rank;
+  m->nranks = cfg->nranks;
+  m->host_only = cfg->host_only != 0;
+  Geom& G = m->G;
+  G.g = cfg->nghost;
+  G.cg = (G.g + 1) / 2 + 1;
+  int64_t maxface = 0;
+  for (int d = 0; d < 3; ++d) {
+    G.n[d] = (int)cfg->block_nx[d];
+    G.N[d] = G.n[d] + 2 * G.g;
+    G.nc[d] = G.n[d] / 2;
+    G.NC[d] = G.nc[d] + 2 * G.cg;
+  }
+  maxface = std::max<int64_t>({(int64_t)G.n[1] * G.n[2], (int64_t)G.n[0] * G.n[2], (int64_t)G.n[0] * G.n[1]});
+  G.vstride = (int64_t)G.N[0] * G.N[1] * G.N[2];
+  G.bstride = NVAR * G.vstride;
+  G.cvstride = (int64_t)G.NC[0] * G.NC[1] * G.NC[2];
+  G.cbstride = NVAR * G.cvstride;
+  G.fstride = NVAR * maxface;
+  G.gamma = cfg->gamma;
+  G.gm1 = cfg->gamma - 1.0;
+  G.inv_gm1 = 1.0 / (cfg->gamma - 1.0);
+  G.cfl = cfg->cfl;
+  try {
+    m->tree = new Tree(mc);
+    if (cfg->refinement != PH_REF_NONE && cfg->max_level > 0) m->tree->refine_regions(m->regions);
+    build_blocks(*m->tree, m->nranks, m->rank, m->blocks, m->gid_of);
+  } catch (const std::exception& e) {
+    delete m->tree;
+    delete m;
+    return fail(PH_ERR_CONFIG, e.what());
+  }
+  ph_status st = build_plan(m);
+  if (st != PH_OK) {
+    delete m->tree;
+    delete m;
+    return st;
+  }
+  if (!m->host_only) {
+    cudaError_t e = cudaSetDevice(cfg->device);
+    if (e != cudaSuccess) {
+      delete m->tree;
+      delete m;
+      return fail(PH_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    }
+    m->stream = (cudaStream_t)cfg->stream;
+    cudaStreamCreateWithFlags(&m->comm_stream, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&m->ev_pack, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&m->ev_comm, cudaEventDisableTiming);
+    if (m->nranks > 1) {
+      if (!cfg->nccl_id) {
+        delete m->tree;
+        delete m;
+        return fail(PH_ERR_INVALID_ARG, "nranks > 1 needs nccl_id");
+      }
+      ncclUniqueId id;
+      memcpy(&id, cfg->nccl_id, sizeof id);
+      ncclResult_t r = ncclCommInitRank(&m->comm, m->nranks, id, m->rank);
+      if (r != ncclSuccess) {
+        delete m->tree;
+        delete m;
+        return fail(PH_ERR_COMM, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+      }
+    }
+    st = setup_persistent(m);
+    if (st == PH_OK) st = setup_device(m);
+    if (st == PH_OK) {
+      cudaError_t e2 = cudaStreamSynchronize(m->stream);
+      if (e2 != cudaSuccess) st = fail(PH_ERR_CUDA, cudaGetErrorString(e2));
+    }
+    if (st != PH_OK) {
+      std::string msg = g_err;
+      ph_mesh_destroy(m);
+      g_err = msg;
+      return st;
+    }
+  }
+  *out = m;
+  return PH_OK;
+}
+
+ph_status ph_mesh_destroy(ph_mesh* m) {
+  if (!m) return PH_OK;
+  free_all(m);
+  for (auto& p : m->t_stage) (void)p;
+  for (cudaEvent_t e : m->ev_pool) cudaEventDestroy(e);
+  if (m->ev_pack) cudaEventDestroy(m->ev_pack);
+  if (m->ev_comm) cudaEventDestroy(m->ev_comm);
+  if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
+  if (m->comm) ncclCommDestroy(m->comm);
+  delete m->tree;
+  delete m;
+  return PH_OK;
+}
+
+static ph_status need_device(const ph_mesh* m) {
+  if (!m) return fail(PH_ERR_INVALID_ARG, "null mesh");
+  if (m->host_only) return fail(PH_ERR_STATE, "host-only mesh has no device state");
+  return PH_OK;
+}
+
+ph_status ph_exchange(ph_mesh* m) {
+  TRY(need_device(m));
+  TRY(exchange(m, m->U0));
+  return check_err(m);
+}
+
+ph_status ph_refresh(ph_mesh* m) {
+  TRY(need_device(m));
+  TRY(exchange(m, m->U0));
+  TRY(standalone_reduce(m, m->U0, 0));
+  m->have_state = true;
+  return check_err(m);
+}
+
+ph_status ph_set_problem(ph_mesh* m, int32_t problem, const double* p, int32_t np) {
+  TRY(need_device(m));
+  PgenArgs P{};
+  P.problem = problem;
+  for (int d = 0; d < 3; ++d) {
+    P.xmin[d] = m->cfg.xmin[d];
+    P.L[d] = m->cfg.xmax[d] - m->cfg.xmin[d];
+  }
+  if (np > 8) return fail(PH_ERR_INVALID_ARG, "too many problem parameters");
+  for (int i = 0; i < np; ++i) P.p[i] = p[i];
+  if (problem == PH_PROB_LINEAR_WAVE) {
+    if (np < 4) return fail(PH_ERR_INVALID_ARG, "linear wave needs {A,k1,k2,k3}");
+  } else if (problem == PH_PROB_SOD) {
+    if (np < 1) P.p[0] = 0.5 * (m->cfg.xmin[0] + m->cfg.xmax[0]);
+  } else if (problem == PH_PROB_BLAST) {
+    if (np < 3) return fail(PH_ERR_INVALID_ARG, "blast needs {p_in,p_out,r[,cx,cy,cz]}");
+    if (np < 6)
+      for (int d = 0; d < 3; ++d) P.p[3 + d] = 0.5 * (m->cfg.xmin[d] + m->cfg.xmax[d]);
+    if (!(P.p[0] > 0 && P.p[1] > 0 && P.p[2] > 0)) return fail(PH_ERR_INVALID_ARG, "blast parameters out of range");
+  } else {
+    return fail(PH_ERR_INVALID_ARG, "unknown problem");
+  }
+  if (m->cfg.refinement == PH_REF_ADAPTIVE) return fail(PH_ERR_UNSUPPORTED, "adaptive refinement not yet on the GPU path");
+  CU(launch_pgen(m->U0, m->d_meta, (int)m->local_gids.size(), P, m->G, m->stream));
+  m->launches++;
+  CU(cudaMemsetAsync(m->d_st, 0, sizeof(CycleState), m->stream));
+  TRY(exchange(m, m->U0));
+  TRY(standalone_reduce(m, m->U0, 0));
+  m->have_state = true;
+  return check_err(m);
+}
+
+static int64_t slot_of(const ph_mesh* m, int64_t gid) {
+  if (gid < 0 || gid >= (int64_t)m->blocks.size()) return -2;
+  const BlockInfo& b = m->blocks[gid];
+  return b.rank == m->rank ? b.local : -1;
+}
+
+ph_status ph_set_state(ph_mesh* m, int64_t gid, const double* cons, int64_t nelem) {
+  TRY(need_device(m));
+  int64_t s = slot_of(m, gid);
+  if (s == -2) return fail(PH_ERR_INVALID_ARG, "bad gid");
+  const Geom& G = m->G;
+  int64_t ni = (int64_t)NVAR * G.n[0] * G.n[1] * G.n[2];
+  if (nelem != ni) return fail(PH_ERR_INVALID_ARG, "bad nelem");
+  if (s < 0) return PH_OK;
+  CU(cudaMemcpyAsync(m->stage_buf, cons, ni * sizeof(double), cudaMemcpyHostToDevice, m->stream));
+  CU(launch_interior_copy(m->U0, m->stage_buf, (int)s, 1, 1, G, m->stream));
+  m->launches++;
+  CU(cudaStreamSynchronize(m->stream));
+  m->have_state = true;
+  return PH_OK;
+}
+
+ph_status ph_get_state(const ph_mesh* mc, int64_t gid, double* cons, int64_t nelem) {
+  ph_mesh* m = const_cast<ph_mesh*>(mc);
+  TRY(need_device(m));
+  int64_t s = slot_of(m, gid);
+  if (s == -2) return fail(PH_ERR_INVALID_ARG, "bad gid");
+  const Geom& G = m->G;
+  int64_t ni = (int64_t)NVAR * G.n[0] * G.n[1] * G.n[2];
+  if (nelem != ni) return fail(PH_ERR_INVALID_ARG, "bad nelem");
+  TRY(check_err(m));
+  if (s < 0) return PH_OK;
+  CU(launch_interior_copy(m->U0, m->stage_buf, (int)s, 1, 0, G, m->stream));
+  m->launches++;
+  CU(cudaMemcpyAsync(cons, m->stage_buf, ni * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  return PH_OK;
+}
+
+ph_status ph_get_state_full(const ph_mesh* mc, int64_t gid, double* out, int64_t nelem) {
+  ph_mesh* m = const_cast<ph_mesh*>(mc);
+  TRY(need_device(m));
+  int64_t s = slot_of(m, gid);
+  if (s == -2) return fail(PH_ERR_INVALID_ARG, "bad gid");
+  if (nelem != m->G.bstride) return fail(PH_ERR_INVALID_ARG, "bad nelem");
+  TRY(check_err(m));
+  if (s < 0) return PH_OK;
+  CU(cudaMemcpyAsync(out, m->U0 + s * m->G.bstride, nelem * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  return PH_OK;
+}
+
+ph_status ph_set_state_full(ph_mesh* m, int64_t gid, const double* in, int64_t nelem) {
+  TRY(need_device(m));
+  int64_t s = slot_of(m, gid);
+  if (s == -2) return fail(PH_ERR_INVALID_ARG, "bad gid");
+  if (nelem != m->G.bstride) return fail(PH_ERR_INVALID_ARG, "bad nelem");
+  if (s < 0) return PH_OK;
+  CU(cudaMemcpyAsync(m->U0 + s * m->G.bstride, in, nelem * sizeof(double), cudaMemcpyHostToDevice, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  m->have_state = true;
+  return PH_OK;
+}
+
+ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) {
+  TRY(need_device(m));
+  if (!m->have_state) return fail(PH_ERR_STATE, "no state: call ph_set_problem or ph_set_state + ph_refresh");
+  if (m->cfg.refinement == PH_REF_ADAPTIVE) return fail(PH_ERR_UNSUPPORTED, "adaptive refinement not yet on the GPU path");
+  if (m->cross_rank_reflux)
+    return fail(PH_ERR_UNSUPPORTED, "flux correction across ranks is not implemented yet (multilevel + nranks > 1)");
+  CU(launch_cycle_begin(m->d_st, tlim, 1, m->stream));
+  m->launches++;
+  for (int c = 0; c < ncycles; ++c) TRY(one_cycle(m));
+  if (info) {
+    TRY(check_err(m));
+    CycleState st;
+    CU(cudaMemcpy(&st, m->d_st, sizeof st, cudaMemcpyDeviceToHost));
+    info->cycle = st.cycle;
+    info->t = st.t;
+    info->dt = st.dt;
+    int64_t cells = (int64_t)m->blocks.size() * m->G.n[0] * m->G.n[1] * m->G.n[2];
+    info->zone_cycles = cells * ncycles;
+  }
+  return PH_OK;
+}
+
+ph_status ph_step_host(ph_mesh* m, const double* host_in, double* host_out, int64_t nelem, int32_t ncycles,
+                       double tlim) {
+  TRY(need_device(m));
+  const Geom& G = m->G;
+  int64_t nloc = (int64_t)m->local_gids.size();
+  int64_t ni = nloc * NVAR * G.n[0] * G.n[1] * G.n[2];
+  if (nelem != ni) return fail(PH_ERR_INVALID_ARG, "bad nelem (expect nlocal*5*n3*n2*n1)");
+  if (ni) CU(cudaMemcpyAsync(m->stage_buf, host_in, ni * sizeof(double), cudaMemcpyHostToDevice, m->stream));
+  if (nloc) {
+    CU(launch_interior_copy(m->U0, m->stage_buf, 0, (int)nloc, 1, G, m->stream));
+    m->launches++;
+  }
+  m->have_state = true;
+  TRY(exchange(m, m->U0));
+  TRY(standalone_reduce(m, m->U0, 0));
+  TRY(ph_step(m, ncycles, tlim, nullptr));
+  if (nloc) {
+    CU(launch_interior_copy(m->U0, m->stage_buf, 0, (int)nloc, 0, G, m->stream));
+    m->launches++;
+  }
+  if (ni) CU(cudaMemcpyAsync(host_out, m->stage_buf, ni * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
+  return check_err(m);
+}
+
+ph_status ph_num_blocks(const ph_mesh* m, int64_t* nglobal, int64_t* nlocal) {
+  if (!m) return fail(PH_ERR_INVALID_ARG, "null mesh");
+  if (nglobal) *nglobal = (int64_t)m->blocks.size();
+  if (nlocal) *nlocal = (int64_t)m->local_gids.size();
+  return PH_OK;
+}
+
+ph_status ph_get_blocks(const ph_mesh* m, ph_block* out, int64_t cap, int64_t* n) {
+  if (!m || !n) return fail(PH_ERR_INVALID_ARG, "null argument");
+  *n = (int64_t)m->blocks.size();
+  for (int64_t g = 0; g < *n && g < cap; ++g) {
+    const BlockInfo& b = m->blocks[g];
+    out[g].gid = b.gid;
+    out[g].level = b.loc.level;
+    out[g].rank = b.rank;
+    for (int d = 0; d < 3; ++d) {
+      out[g].lx[d] = b.loc.x[d];
+      out[g].xmin[d] = b.xmin[d];
+      out[g].xmax[d] = b.xmax[d];
+    }
+  }
+  return PH_OK;
+}
+
+ph_status ph_get_neighbors(const ph_mesh* m, int64_t gid, ph_neighbor* out, int32_t cap, int32_t* n) {
+  if (!m || !n) return fail(PH_ERR_INVALID_ARG, "null argument");
+  if (gid < 0 || gid >= (int64_t)m->blocks.size()) return fail(PH_ERR_INVALID_ARG, "bad gid");
+  const BlockInfo& b = m->blocks[gid];
+  *n = (int32_t)b.nbrs.size();
+  for (int32_t q = 0; q < *n && q < cap; ++q) {
+    const Neighbor& e = b.nbrs[q];
+    out[q].gid = e.gid;
+    out[q].rank = e.rank;
+    for (int d = 0; d < 3; ++d) out[q].off[d] = e.off[d];
+    out[q].dlevel = e.dlevel;
+    out[q].fine[0] = e.fine[0];
+    out[q].fine[1] = e.fine[1];
+  }
+  return PH_OK;
+}
+
+ph_status ph_get_refine_flags(const ph_mesh* m, int8_t* out, int64_t cap, int64_t* n) {
+  if (!m || !n) return fail(PH_ERR_INVALID_ARG, "null argument");
+  *n = (int64_t)m->last_flags.size();
+  for (int64_t i = 0; i < *n && i < cap; ++i) out[i] = m->last_flags[i];
+  return PH_OK;
+}
+
+ph_status ph_get_history(const ph_mesh* mc, double* out, int64_t cap_rows, int64_t* nrows) {
+  ph_mesh* m = const_cast<ph_mesh*>(mc);
+  TRY(need_device(m));
+  TRY(check_err(m));
+  CycleState st;
+  CU(cudaMemcpy(&st, m->d_st, sizeof st, cudaMemcpyDeviceToHost));
+  int64_t n = std::min<int64_t>(st.hist_count, m->hist_cap);
+  *nrows = n;
+  std::vector<double> h((size_t)m->hist_cap * 7);
+  CU(cudaMemcpy(h.data(), m->hist, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  int64_t first = st.hist_count - n;
+  for (int64_t r = 0; r < n && r < cap_rows; ++r) {
+    int64_t q = (first + r) % m->hist_cap;
+    for (int c = 0; c < 7; ++c) out[r * 7 + c] = h[q * 7 + c];
+  }
+  return PH_OK;
+}
+
+ph_status ph_get_time(const ph_mesh* mc, double* t, double* dt, int64_t* cycle) {
+  ph_mesh* m = const_cast<ph_mesh*>(mc);
+  TRY(need_device(m));
+  TRY(check_err(m));
+  CycleState st;
+  CU(cudaMemcpy(&st, m->d_st, sizeof st, cudaMemcpyDeviceToHost));
+  if (t) *t = st.t;
+  if (dt) *dt = st.dt;
+  if (cycle) *cycle = st.cycle;
+  return PH_OK;
+}
+
+ph_status ph_totals(ph_mesh* m, double out[5]) {
+  TRY(need_device(m));
+  int nloc = (int)m->local_gids.size();
+  if (nloc > 0) {
+    CU(launch_reduce(m->U0, m->d_meta, nloc, m->partials, m->d_err, m->G, m->stream));
+    m->launches++;
+  }
+  CU(launch_rank_reduce(m->partials, nloc * m->G.n[2], m->nranks > 1 ? m->my6 : m->all6, m->stream));
+  m->launches++;
+  if (m->nranks > 1) NC(ncclAllGather(m->my6, m->all6, 6, ncclDouble, m->comm, m->stream));
+  CU(launch_finalize(m->all6, m->nranks, m->d_st, m->hist, m->hist_cap, m->G.cfl, 2, m->tot5, m->stream));
+  m->launches++;
+  TRY(check_err(m));
+  CU(cudaMemcpy(out, m->tot5, 5 * sizeof(double), cudaMemcpyDeviceToHost));
+  return PH_OK;
+}
+
+ph_status ph_get_plan_info(const ph_mesh* m, ph_plan_info* out) {
+  if (!m || !out) return fail(PH_ERR_INVALID_ARG, "null argument");
+  memset(out, 0, sizeof *out);
+  out->n_local_tasks = (int64_t)m->local.tasks.size();
+  out->n_send_tasks = (int64_t)m->pack.tasks.size();
+  out->n_recv_tasks = (int64_t)m->unpack.tasks.size();
+  for (int p = 0; p < m->nranks && p < 64; ++p) {
+    out->send_doubles_to[p] = m->send_cnt[p];
+    out->recv_doubles_from[p] = m->recv_cnt[p];
+    out->send_hash_to[p] = m->send_hash[p];
+    out->recv_hash_from[p] = m->recv_hash[p];
+  }
+  return PH_OK;
+}
+
+ph_status ph_launch_count(const ph_mesh* m, int64_t* n) {
+  if (!m || !n) return fail(PH_ERR_INVALID_ARG, "null argument");
+  *n = m->launches;
+  return PH_OK;
+}
+
+ph_status ph_kernel_timing(ph_mesh* m, int32_t enable, double* stage_ms, int64_t* stage_launches, double* exch_ms,
+                           int64_t* exch_launches) {
+  TRY(need_device(m));
+  CU(cudaStreamSynchronize(m->stream));
+  double s = 0, x = 0;
+  for (auto& p : m->t_stage) {
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, p.first, p.second));
+    s += ms;
+  }
+  for (auto& p : m->t_exch) {
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, p.first, p.second));
+    x += ms;
+  }
+  if (stage_ms) *stage_ms = s;
+  if (stage_launches) *stage_launches = (int64_t)m->t_stage.size();
+  if (exch_ms) *exch_ms = x;
+  if (exch_launches) *exch_launches = (int64_t)m->t_exch.size();
+  m->t_stage.clear();
+  m->t_exch.clear();
+  for (cudaEvent_t e : m->ev_pool) cudaEventDestroy(e);
+  m->ev_pool.clear();
+  m->timing = enable != 0;
+  return PH_OK;
+}
+
+}  // extern "C"

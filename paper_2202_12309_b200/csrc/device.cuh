@@ -1,0 +1,148 @@
+// device.cuh -- plain structs shared by the host orchestration (api.cu) and the sm_100a
+// kernels (kernels.cu).  Product code only; nothing here is shared with oracle/.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ph {
+
+constexpr int NVAR = 5;  // rho, m1, m2, m3, E
+
+// Per-launch geometry of the block pool.  Pool layout (a1): U[slot][v][k][j][i], fp64,
+// i fastest, extents (n+2g) -- the paper's slowest-first index order.
+struct Geom {
+  int n[3];        // interior cells per dim
+  int g;           // ghost width (2)
+  int N[3];        // n + 2g
+  int64_t vstride; // N1*N2*N3
+  int64_t bstride; // 5*vstride
+  int nc[3];       // coarse staging interior (n/2)
+  int cg;          // coarse staging ghosts
+  int NC[3];       // nc + 2cg
+  int64_t cvstride, cbstride;
+  int64_t fstride; // doubles per face-flux slot (5 * max face cells)
+  double gamma, gm1, inv_gm1;
+  double cfl;
+};
+
+// Per local block slot.
+struct BlockMeta {
+  double idx[3];     // 1/dx
+  double dV;
+  double xmin[3];
+  double dx[3];
+  int64_t gid;
+  int level;
+  int cslot;         // coarse staging slot, -1 if none
+  int fslot[6];      // face-flux slot for faces -x,+x,-y,+y,-z,+z (coarse-fine faces), else -1
+};
+
+// Ghost-exchange task (fill-in-one).  One task fills one destination box.
+enum TaskKind : int {
+  T_COPY = 0,       // same level: U_dst[d] = U_src[d + so]
+  T_RESTRICT = 1,   // finer source: U_dst[d] = mean8(U_src[2d - so ...])
+  T_CCOPY = 2,      // coarser source into my staging: C_dst[d] = U_src[d + so]
+  T_CRESTRICT = 3,  // own fine cells into own staging: C[d] = mean8(U[2d ...])
+  T_PROLONG = 4,    // staging first layer -> 8 fine ghosts
+  T_BC_FINE = 5,    // physical BC on fine ghosts (direct composition of x1,x2,x3 passes)
+  T_BC_COARSE = 6,  // physical BC on staging ghosts
+  T_UNPACK_U = 7,   // recv buffer -> U box
+  T_UNPACK_C = 8    // recv buffer -> C box
+};
+
+struct XTask {
+  int kind;
+  int dst_slot;      // pool slot (U or C by kind); -1 = send buffer (pack)
+  int src_slot;      // pool slot; -1 = recv buffer (unpack)
+  int lo[3];         // first destination cell
+  int ext[3];        // box extents
+  int so[3];         // source shift (see kinds)
+  int bc;            // BC kinds: per dim d, bits [4d,4d+2) low face, [4d+2,4d+4) high face: 0 none, 1 outflow, 2 reflect
+  int ncell;
+  int64_t buf;       // offset (doubles) into the send / recv buffer; payload [v][cell]
+};
+
+struct Chunk {
+  int task;
+  int begin;
+};
+
+// Reflux (flux correction, O8 / a8): one coarse face with 4 finer face neighbours.
+struct RefluxTask {
+  int cslot;         // coarse block slot
+  int dir, side;     // face dim, -1 low / +1 high
+  int cfs;           // coarse face-flux slot
+  int ffs;           // fine face-flux slot
+  int t0lo, t1lo;    // coarse tangential start of this fine block's quarter
+};
+
+struct ErrWord {
+  int flag;
+  int stage;
+  long long gid;
+  int k, j, i;
+};
+
+// Device-resident cycle state (dt, t, history).  Updated only by kernels.
+struct CycleState {
+  double t, dt, dt_used, tlim;
+  long long cycle;
+  int active;
+  int pad;
+  long long hist_count;
+};
+
+constexpr int TILE_X = 32, TILE_Y = 8;  // stage-kernel tile (i, j); 256 threads
+
+struct StageArgs {
+  const double* Uin;   // pool with valid ghosts (stage input)
+  const double* U0;    // base state U^n (interior reads), may alias Uout
+  double* Uout;        // output pool (interior writes)
+  const BlockMeta* meta;
+  const int* slots;    // pack: list of block slots
+  const CycleState* st;
+  double* fbuf;        // face-flux slots (multilevel)
+  double* partials;    // [ncta][6] (max speed/dx, 5 totals) when REDUCE
+  ErrWord* err;
+  double a0, b1, cdt;  // out = a0*U0 + b1*Uin + cdt*dt*L
+  int ntx, nty, nkc, KC;
+  int cta_base;        // offset of this launch's CTAs in partials
+  int stage;
+};
+
+struct XArgs {
+  const XTask* tasks;
+  const Chunk* chunks;
+  double* U;           // fine pool (read and write)
+  double* C;           // coarse staging pool
+  double* sbuf;        // send buffer (pack tasks)
+  const double* rbuf;  // recv buffer (unpack tasks)
+};
+
+struct PgenArgs {
+  int problem;
+  double p[8];
+  double xmin[3], L[3];
+};
+
+constexpr int XCHUNK = 512;  // cells per exchange chunk (one CTA)
+
+// launchers (kernels.cu)
+cudaError_t launch_stage(int recon, bool reduce, bool use_u0, int nblk_cta, const StageArgs& a, const Geom& G,
+                         cudaStream_t s);
+cudaError_t launch_xfill(int nchunks, const XArgs& a, const Geom& G, cudaStream_t s);
+cudaError_t launch_reflux(int ntasks, const RefluxTask* t, double* U, const BlockMeta* meta, const double* fbuf,
+                          const CycleState* st, double w, const Geom& G, cudaStream_t s);
+cudaError_t launch_pgen(double* U, const BlockMeta* meta, int nslots, const PgenArgs& P, const Geom& G,
+                        cudaStream_t s);
+cudaError_t launch_reduce(const double* U, const BlockMeta* meta, int nslots, double* partials, ErrWord* err,
+                          const Geom& G, cudaStream_t s);
+cudaError_t launch_rank_reduce(const double* partials, int n, double* out, cudaStream_t s);
+cudaError_t launch_finalize(const double* all, int nranks, CycleState* st, double* hist, int hist_cap, double cfl,
+                            int mode, double* tot_out, cudaStream_t s);
+cudaError_t launch_cycle_begin(CycleState* st, double tlim, int set_tlim, cudaStream_t s);
+cudaError_t launch_interior_copy(double* U, double* buf, int slot0, int nslots, int to_pool, const Geom& G,
+                                 cudaStream_t s);
+size_t stage_smem_bytes();
+
+}  // namespace ph

@@ -1,0 +1,828 @@
+// kernels.cu -- sm_100a kernels of the Parthenon-hydro hot path.
+//
+// Paper: Parthenon-hydro update = RK2 + PLM + HLLE over packs of
+// MeshBlocks in one launch; fill-in-one boundary kernels incl. restriction and
+// prolongation; flux correction; CFL dt as a global reduction
+// (P:640-650).  Formulas and their operation order follow SURVEY.md §8(c) O5-O8.
+//
+// No tensor cores: every kernel here is an fp64 stencil or copy (bandwidth / fp64-issue bound).
+#include <cstdio>
+
+#include "device.cuh"
+
+namespace ph {
+
+// ------------------------------------------------------------------------------ point math
+// textbook minmod on the integer pipe: same sign bit -> the smaller magnitude
+__device__ __forceinline__ double minmod_i(double a, double b) {
+  long long ia = __double_as_longlong(a), ib = __double_as_longlong(b);
+  long long ma = ia & 0x7fffffffffffffffLL, mb = ib & 0x7fffffffffffffffLL;
+  long long m = (ma < mb) ? ia : ib;
+  return ((ia ^ ib) >= 0) ? __longlong_as_double(m) : 0.0;
+}
+
+template <int RECON>
+__device__ __forceinline__ double slope(double dl, double dr) {
+  if (RECON == 0) return minmod_i(dl, dr);
+  bool same = (dl > 0.0 && dr > 0.0) || (dl < 0.0 && dr < 0.0);
+  if (!same) return 0.0;
+  if (RECON == 1) return 2.0 * dl * dr / (dl + dr);  // van Leer (A3)
+  double s = dl > 0.0 ? 1.0 : -1.0;                  // MC
+  double m = fmin(fmin(2.0 * fabs(dl), 2.0 * fabs(dr)), 0.5 * fabs(dl + dr));
+  return s * m;
+}
+
+// PLM face states of the face between cells c-1 and c from q0=W(c-2) .. q3=W(c+1) (a3, O5)
+template <int RECON>
+__device__ __forceinline__ void plm_face(double q0, double q1, double q2, double q3, double& wl, double& wr) {
+  double d0 = q1 - q0, d1 = q2 - q1, d2 = q3 - q2;
+  double s1 = slope<RECON>(d0, d1);
+  double s2 = slope<RECON>(d1, d2);
+  wl = fma(0.5, s1, q1);   // == q1 + 0.5*s1 exactly (0.5*s1 is exact)
+  wr = fma(-0.5, s2, q2);
+}
+
+// HLLE, Davis speeds, clamped branch-free form (a4; A4, A5).  w = (rho, u_n, v_t1, v_t2, p).
+__device__ __forceinline__ void hlle(const double* wl, const double* wr, const Geom& G, double* F) {
+  double cl = sqrt(G.gamma * wl[4] / wl[0]);
+  double cr = sqrt(G.gamma * wr[4] / wr[0]);
+  double sl = fmin(wl[1] - cl, wr[1] - cr);
+  double sr = fmax(wl[1] + cl, wr[1] + cr);
+  double bp = fmax(sr, 0.0);
+  double bm = fmin(sl, 0.0);
+  double inv = 1.0 / (bp - bm);
+  double bb = bp * bm;
+  // left state
+  double mul = wl[0] * wl[1];
+  double El = wl[4] * G.inv_gm1 + (0.5 * wl[0]) * (wl[1] * wl[1] + (wl[2] * wl[2] + wl[3] * wl[3]));
+  double mur = wr[0] * wr[1];
+  double Er = wr[4] * G.inv_gm1 + (0.5 * wr[0]) * (wr[1] * wr[1] + (wr[2] * wr[2] + wr[3] * wr[3]));
+  // F = ((bp FL - bm FR) + bb (UR - UL)) * inv
+  F[0] = ((bp * mul - bm * mur) + bb * (wr[0] - wl[0])) * inv;
+  F[1] = ((bp * (mul * wl[1] + wl[4]) - bm * (mur * wr[1] + wr[4])) + bb * (mur - mul)) * inv;
+  F[2] = ((bp * (mul * wl[2]) - bm * (mur * wr[2])) + bb * (wr[0] * wr[2] - wl[0] * wl[2])) * inv;
+  F[3] = ((bp * (mul * wl[3]) - bm * (mur * wr[3])) + bb * (wr[0] * wr[3] - wl[0] * wl[3])) * inv;
+  F[4] = ((bp * ((El + wl[4]) * wl[1]) - bm * ((Er + wr[4]) * wr[1])) + bb * (Er - El)) * inv;
+}
+
+__device__ __forceinline__ void set_error(ErrWord* err, int stage, long long gid, int k, int j, int i) {
+  if (atomicCAS(&err->flag, 0, 1) == 0) {
+    err->stage = stage;
+    err->gid = gid;
+    err->k = k;
+    err->j = j;
+    err->i = i;
+    __threadfence();
+  }
+}
+
+// ------------------------------------------------------------------------------ stage kernel
+// One CTA = a TX x TY tile of (i,j) columns of one block, marching over a k-range of KC planes.
+// Per plane: the plus-shaped halo plane is converted to primitives into smem (a2); x and y face
+// fluxes (a3+a4) go to smem; the z direction is carried in registers per column; each cell is
+// finished two planes later with the flux divergence and the RK stage combine (a5).  The final
+// stage also produces the CFL dt term and the conserved totals (a6, a10) per CTA.
+constexpr int TX = TILE_X, TY = TILE_Y, NT = TX * TY;
+constexpr int SWX = TX + 4, SWY = TY + 4;
+
+
+
+template <int RECON, bool REDUCE, bool USE_U0>
+__global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
+  extern __shared__ double smem[];
+  double* sW = smem;                          // [5][SWY][SWX]
+  double* sFx = sW + NVAR * SWY * SWX;        // [5][TY][TX+1]
+  double* sFy = sFx + NVAR * TY * (TX + 1);   // [5][TY+1][TX]
+  double* sS = sFy + NVAR * (TY + 1) * TX;    // [3][5][TY][TX]
+
+  const int tid = threadIdx.x;
+  const int tx = tid % TX, ty = tid / TX;
+  int bid = blockIdx.x;
+  const int kc = bid % A.nkc;
+  bid /= A.nkc;
+  const int tyi = bid % A.nty;
+  bid /= A.nty;
+  const int txi = bid % A.ntx;
+  const int pb = bid / A.ntx;
+  const int slot = A.slots[pb];
+  const BlockMeta& M = A.meta[slot];
+  const int x0 = txi * TX, y0 = tyi * TY;
+  const int nxt = min(TX, G.n[0] - x0), nyt = min(TY, G.n[1] - y0);
+  const int k0 = kc * A.KC;
+  const int k1 = min(k0 + A.KC, G.n[2]);
+  const int g = G.g;
+  const int64_t plane = (int64_t)G.N[0] * G.N[1];
+  const double* Ub = A.Uin + (int64_t)slot * G.bstride;
+  const double dt = A.st->dt_used;
+  const double idx1 = M.idx[0], idx2 = M.idx[1], idx3 = M.idx[2];
+  const bool own = (tx < nxt) && (ty < nyt);
+
+  // ---- load-slot geometry (two cells per thread for interior planes) ----
+  int sl_i[2], sl_j[2];
+  bool sl_ok[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    int c = tid + s * NT;
+    int i, j;
+    bool ok;
+    if (c < SWX * TY) {
+      j = c / SWX;
+      i = c % SWX - 2;
+      ok = (j < nyt) && (i < nxt + 2);
+    } else {
+      int c2 = c - SWX * TY;
+      int r = c2 / TX;
+      i = c2 % TX;
+      j = (r < 2) ? r - 2 : TY + r - 2;
+      ok = (c2 < 4 * TX) && (i < nxt) && ((r < 2) || (nyt == TY));
+    }
+    // rows j in [nyt, nyt+2) of a ragged tile live in the first region
+    if (c < SWX * TY && j >= nyt && j < nyt + 2 && i >= 0 && i < nxt) ok = true;
+    sl_i[s] = i;
+    sl_j[s] = j;
+    sl_ok[s] = ok;
+  }
+
+  double pf[2][NVAR];
+  auto issue_load = [&](int q) {
+    bool halo = (q < k0) || (q >= k1);
+    const double* base = Ub + (int64_t)(q + g) * plane;
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      int i = halo ? tx : sl_i[s], j = halo ? ty : sl_j[s];
+      bool ok = halo ? (s == 0 && own) : sl_ok[s];
+      if (ok) {
+        const double* p = base + (int64_t)(y0 + j + g) * G.N[0] + (x0 + i + g);
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) pf[s][v] = __ldg(p + v * G.vstride);
+      }
+    }
+  };
+  auto store_prims = [&](int q) {
+    bool halo = (q < k0) || (q >= k1);
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      int i = halo ? tx : sl_i[s], j = halo ? ty : sl_j[s];
+      bool ok = halo ? (s == 0 && own) : sl_ok[s];
+      if (ok) {
+        double rho = pf[s][0];
+        double ir = 1.0 / rho;
+        double v1 = pf[s][1] * ir, v2 = pf[s][2] * ir, v3 = pf[s][3] * ir;
+        double ke = 0.5 * ((pf[s][1] * v1 + pf[s][2] * v2) + pf[s][3] * v3);
+        double p = G.gm1 * (pf[s][4] - ke);
+        if (!(rho > 0.0) || !(p > 0.0)) set_error(A.err, A.stage, M.gid, q, y0 + j, x0 + i);
+        int o = (j + 2) * SWX + (i + 2);
+        sW[o] = rho;
+        sW[SWY * SWX + o] = v1;
+        sW[2 * SWY * SWX + o] = v2;
+        sW[3 * SWY * SWX + o] = v3;
+        sW[4 * SWY * SWX + o] = p;
+      }
+    }
+  };
+
+  // z-direction state of my column
+  double wprev[NVAR], dprev[NVAR], topprev[NVAR], fzprev[NVAR];
+  double tmax = 0.0, tsum[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const int qbeg = k0 - 2, qend = k1 + 2;
+  issue_load(qbeg);
+  for (int q = qbeg; q < qend; ++q) {
+    __syncthreads();
+    store_prims(q);
+    if (q + 1 < qend) issue_load(q + 1);
+    __syncthreads();
+    const bool interior = (q >= k0) && (q < k1);
+    if (interior) {
+      // x faces: (nxt+1) per row
+      const int nfx = (nxt + 1) * nyt;
+      for (int f = tid; f < nfx; f += NT) {
+        int j = f / (nxt + 1), fi = f % (nxt + 1);
+        const double* w = sW + (j + 2) * SWX + fi;  // w[0..3] = cells fi-2 .. fi+1
+        double wl[NVAR], wr[NVAR], F[NVAR];
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) {
+          const double* c = w + v * SWY * SWX;
+          plm_face<RECON>(c[0], c[1], c[2], c[3], wl[v], wr[v]);
+        }
+        double a[NVAR] = {wl[0], wl[1], wl[2], wl[3], wl[4]};
+        double b[NVAR] = {wr[0], wr[1], wr[2], wr[3], wr[4]};
+        hlle(a, b, G, F);  // normal = x1: (rho, v1, v2, v3, p)
+        double* o = sFx + j * (TX + 1) + fi;
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) o[v * TY * (TX + 1)] = F[v];
+        int gi = x0 + fi;
+        int fs = (gi == 0) ? M.fslot[0] : ((gi == G.n[0]) ? M.fslot[1] : -1);
+        if (fs >= 0) {
+          double* fb = A.fbuf + (int64_t)fs * G.fstride + (int64_t)q * G.n[1] + (y0 + j);
+          int64_t fst = (int64_t)G.n[1] * G.n[2];
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) fb[v * fst] = F[v];
+        }
+      }
+      // y faces: (nyt+1) rows of nxt
+      const int nfy = nxt * (nyt + 1);
+      for (int f = tid; f < nfy; f += NT) {
+        int jf = f / nxt, i = f % nxt;
+        const double* w = sW + jf * SWX + (i + 2);  // rows jf-2 .. jf+1
+        double wl[NVAR], wr[NVAR], Fn[NVAR];
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) {
+          const double* c = w + v * SWY * SWX;
+          plm_face<RECON>(c[0], c[SWX], c[2 * SWX], c[3 * SWX], wl[v], wr[v]);
+        }
+        double a[NVAR] = {wl[0], wl[2], wl[3], wl[1], wl[4]};  // normal = x2: (v2, v3, v1)
+        double b[NVAR] = {wr[0], wr[2], wr[3], wr[1], wr[4]};
+        hlle(a, b, G, Fn);
+        double F[NVAR] = {Fn[0], Fn[3], Fn[1], Fn[2], Fn[4]};
+        double* o = sFy + jf * TX + i;
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) o[v * (TY + 1) * TX] = F[v];
+        int gj = y0 + jf;
+        int fs = (gj == 0) ? M.fslot[2] : ((gj == G.n[1]) ? M.fslot[3] : -1);
+        if (fs >= 0) {
+          double* fb = A.fbuf + (int64_t)fs * G.fstride + (int64_t)q * G.n[0] + (x0 + i);
+          int64_t fst = (int64_t)G.n[0] * G.n[2];
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) fb[v * fst] = F[v];
+        }
+      }
+    }
+    // ---- z direction for my column ----
+    double wz[NVAR];
+    if (own) {
+      int o = (ty + 2) * SWX + (tx + 2);
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) wz[v] = sW[v * SWY * SWX + o];
+    }
+    __syncthreads();  // sFx / sFy complete
+    if (own) {
+      if (interior) {
+        int r = ((q % 3) + 3) % 3;
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) {
+          double d1 = (sFx[v * TY * (TX + 1) + ty * (TX + 1) + tx + 1] - sFx[v * TY * (TX + 1) + ty * (TX + 1) + tx]) * idx1;
+          double d2 = (sFy[v * (TY + 1) * TX + (ty + 1) * TX + tx] - sFy[v * (TY + 1) * TX + ty * TX + tx]) * idx2;
+          sS[(r * NVAR + v) * NT + tid] = d1 + d2;
+        }
+      }
+      if (q >= qbeg + 1) {
+        double d[NVAR];
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) d[v] = wz[v] - wprev[v];
+        if (q >= qbeg + 2) {
+          // slope of cell q-1, its bottom / top states
+          double bot[NVAR], top[NVAR];
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) {
+            double s = slope<RECON>(dprev[v], d[v]);
+            bot[v] = fma(-0.5, s, wprev[v]);
+            top[v] = fma(0.5, s, wprev[v]);
+          }
+          if (q >= qbeg + 3) {
+            // face between q-2 and q-1 (global face index q-1)
+            double a[NVAR] = {topprev[0], topprev[3], topprev[1], topprev[2], topprev[4]};  // normal = x3
+            double b[NVAR] = {bot[0], bot[3], bot[1], bot[2], bot[4]};
+            double Fn[NVAR];
+            hlle(a, b, G, Fn);
+            double Fz[NVAR] = {Fn[0], Fn[2], Fn[3], Fn[1], Fn[4]};
+            int gk = q - 1;
+            int fs = (gk == 0) ? M.fslot[4] : ((gk == G.n[2]) ? M.fslot[5] : -1);
+            if (fs >= 0) {
+              double* fb = A.fbuf + (int64_t)fs * G.fstride + (int64_t)(y0 + ty) * G.n[0] + (x0 + tx);
+              int64_t fst = (int64_t)G.n[0] * G.n[1];
+#pragma unroll
+              for (int v = 0; v < NVAR; ++v) fb[v * fst] = Fz[v];
+            }
+            if (q >= qbeg + 4) {
+              // finish cell c = q-2
+              const int c = q - 2;
+              const int r = ((c % 3) + 3) % 3;
+              const int64_t cell = (int64_t)slot * G.bstride + (int64_t)(c + g) * plane +
+                                   (int64_t)(y0 + ty + g) * G.N[0] + (x0 + tx + g);
+              double un[NVAR];
+#pragma unroll
+              for (int v = 0; v < NVAR; ++v) {
+                double dz = (Fz[v] - fzprev[v]) * idx3;
+                double L = -(sS[(r * NVAR + v) * NT + tid] + dz);
+                double uin = A.Uin[cell + v * G.vstride];
+                double out = fma(A.b1, uin, (A.cdt * dt) * L);
+                if (USE_U0) out = fma(A.a0, A.U0[cell + v * G.vstride], out);
+                un[v] = out;
+                A.Uout[cell + v * G.vstride] = out;
+              }
+              if (REDUCE) {
+                double ir = 1.0 / un[0];
+                double v1 = un[1] * ir, v2 = un[2] * ir, v3 = un[3] * ir;
+                double ke = 0.5 * ((un[1] * v1 + un[2] * v2) + un[3] * v3);
+                double p = G.gm1 * (un[4] - ke);
+                double cs = sqrt(G.gamma * p * ir);
+                double s1 = (fabs(v1) + cs) * idx1, s2 = (fabs(v2) + cs) * idx2, s3 = (fabs(v3) + cs) * idx3;
+                tmax = fmax(tmax, fmax(s1, fmax(s2, s3)));
+#pragma unroll
+                for (int v = 0; v < NVAR; ++v) tsum[v] += un[v];
+              }
+            }
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) fzprev[v] = Fz[v];
+          }
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) topprev[v] = top[v];
+        }
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) dprev[v] = d[v];
+      }
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) wprev[v] = wz[v];
+    }
+  }
+  if (REDUCE) {
+    // deterministic CTA reduction: warp shuffles then warp 0 in fixed order
+    __syncthreads();
+    double* red = smem;  // reuse sW
+    for (int off = 16; off > 0; off >>= 1) {
+      tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) tsum[v] += __shfl_xor_sync(0xffffffffu, tsum[v], off);
+    }
+    int warp = tid / 32, lane = tid % 32;
+    if (lane == 0) {
+      red[warp * 6] = tmax;
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) red[warp * 6 + 1 + v] = tsum[v];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double m = 0.0, s[NVAR] = {0, 0, 0, 0, 0};
+      for (int w = 0; w < NT / 32; ++w) {
+        m = fmax(m, red[w * 6]);
+        for (int v = 0; v < NVAR; ++v) s[v] += red[w * 6 + 1 + v];
+      }
+      double* o = A.partials + (int64_t)(A.cta_base + blockIdx.x) * 6;
+      o[0] = m;
+      for (int v = 0; v < NVAR; ++v) o[1 + v] = s[v] * M.dV;
+    }
+  }
+}
+
+size_t stage_smem_bytes() {
+  return sizeof(double) * (NVAR * SWY * SWX + NVAR * TY * (TX + 1) + NVAR * (TY + 1) * TX + 3 * NVAR * NT);
+}
+
+// ------------------------------------------------------------------------------ exchange kernel
+// One CTA per chunk of <= XCHUNK cells of one task; all tasks of one phase in one launch
+// ("fill-in-one").
+constexpr int XT = 128;
+
+
+
+__device__ __forceinline__ double mean8(const double* p, int64_t sj, int64_t sk) {
+  double a = p[0], b = p[1], c = p[sj], d = p[sj + 1];
+  double e = p[sk], f = p[sk + 1], gg = p[sk + sj], h = p[sk + sj + 1];
+  return (((a + b) + (c + d)) + ((e + f) + (gg + h))) * 0.125;  // pairwise, (k,j,i) order (A10)
+}
+
+__device__ __forceinline__ int bc_map(int idx, int n, int lo_kind, int hi_kind, bool& flip) {
+  if (idx < 0 && lo_kind) {
+    if (lo_kind == 2) { flip = !flip; return -1 - idx; }
+    return 0;
+  }
+  if (idx >= n && hi_kind) {
+    if (hi_kind == 2) { flip = !flip; return 2 * n - 1 - idx; }
+    return n - 1;
+  }
+  return idx;
+}
+
+__global__ void __launch_bounds__(XT) xfill_kernel(XArgs A, Geom G) {
+  const Chunk ch = A.chunks[blockIdx.x];
+  const XTask t = A.tasks[ch.task];
+  const int end = min(ch.begin + XCHUNK, t.ncell);
+  const int e0 = t.ext[0], e01 = t.ext[0] * t.ext[1];
+  for (int c = ch.begin + threadIdx.x; c < end; c += XT) {
+    const int ck = c / e01, rem = c - ck * e01;
+    const int cj = rem / e0, ci = rem - cj * e0;
+    const int i = t.lo[0] + ci, j = t.lo[1] + cj, k = t.lo[2] + ck;
+    switch (t.kind) {
+      case T_COPY:
+      case T_CCOPY: {
+        const double* s = A.U + (int64_t)t.src_slot * G.bstride +
+                          ((int64_t)(k + t.so[2] + G.g) * G.N[1] + (j + t.so[1] + G.g)) * G.N[0] + (i + t.so[0] + G.g);
+        if (t.dst_slot < 0) {
+          double* d = A.sbuf + t.buf + c;
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) d[(int64_t)v * t.ncell] = s[v * G.vstride];
+        } else if (t.kind == T_COPY) {
+          double* d = A.U + (int64_t)t.dst_slot * G.bstride + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) d[v * G.vstride] = s[v * G.vstride];
+        } else {
+          double* d = A.C + (int64_t)t.dst_slot * G.cbstride + ((int64_t)(k + G.cg) * G.NC[1] + (j + G.cg)) * G.NC[0] + (i + G.cg);
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) d[v * G.cvstride] = s[v * G.vstride];
+        }
+        break;
+      }
+      case T_RESTRICT:
+      case T_CRESTRICT: {
+        const int fi = 2 * i - t.so[0], fj = 2 * j - t.so[1], fk = 2 * k - t.so[2];
+        const double* s = A.U + (int64_t)t.src_slot * G.bstride + ((int64_t)(fk + G.g) * G.N[1] + (fj + G.g)) * G.N[0] + (fi + G.g);
+        const int64_t sj = G.N[0], sk = (int64_t)G.N[0] * G.N[1];
+        if (t.dst_slot < 0) {
+          double* d = A.sbuf + t.buf + c;
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) d[(int64_t)v * t.ncell] = mean8(s + v * G.vstride, sj, sk);
+        } else if (t.kind == T_RESTRICT) {
+          double* d = A.U + (int64_t)t.dst_slot * G.bstride + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) d[v * G.vstride] = mean8(s + v * G.vstride, sj, sk);
+        } else {
+          double* d = A.C + (int64_t)t.dst_slot * G.cbstride + ((int64_t)(k + G.cg) * G.NC[1] + (j + G.cg)) * G.NC[0] + (i + G.cg);
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) d[v * G.cvstride] = mean8(s + v * G.vstride, sj, sk);
+        }
+        break;
+      }
+      case T_UNPACK_U: {
+        const double* s = A.rbuf + t.buf + c;
+        double* d = A.U + (int64_t)t.dst_slot * G.bstride + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) d[v * G.vstride] = s[(int64_t)v * t.ncell];
+        break;
+      }
+      case T_UNPACK_C: {
+        const double* s = A.rbuf + t.buf + c;
+        double* d = A.C + (int64_t)t.dst_slot * G.cbstride + ((int64_t)(k + G.cg) * G.NC[1] + (j + G.cg)) * G.NC[0] + (i + G.cg);
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) d[v * G.cvstride] = s[(int64_t)v * t.ncell];
+        break;
+      }
+      case T_PROLONG: {
+        // staging cell (i,j,k) -> fine cells 2i..2i+1 (A11): C + (s1/4)d1 + (s2/4)d2 + (s3/4)d3
+        const double* cc = A.C + (int64_t)t.src_slot * G.cbstride + ((int64_t)(k + G.cg) * G.NC[1] + (j + G.cg)) * G.NC[0] + (i + G.cg);
+        double* d = A.U + (int64_t)t.dst_slot * G.bstride + ((int64_t)(2 * k + G.g) * G.N[1] + (2 * j + G.g)) * G.N[0] + (2 * i + G.g);
+        const int64_t cj = G.NC[0], ckk = (int64_t)G.NC[0] * G.NC[1];
+        const int64_t fj = G.N[0], fk = (int64_t)G.N[0] * G.N[1];
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) {
+          const double* p = cc + v * G.cvstride;
+          double c0 = p[0];
+          double s1 = minmod_i(c0 - p[-1], p[1] - c0);
+          double s2 = minmod_i(c0 - p[-cj], p[cj] - c0);
+          double s3 = minmod_i(c0 - p[-ckk], p[ckk] - c0);
+          double* q = d + v * G.vstride;
+#pragma unroll
+          for (int a = 0; a < 2; ++a)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                double val = __dadd_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(e ? 0.25 : -0.25, s1)),
+                                                 __dmul_rn(b ? 0.25 : -0.25, s2)),
+                                       __dmul_rn(a ? 0.25 : -0.25, s3));
+                q[a * fk + b * fj + e] = val;
+              }
+        }
+        break;
+      }
+      case T_BC_FINE:
+      case T_BC_COARSE: {
+        const bool coarse = (t.kind == T_BC_COARSE);
+        const int n0 = coarse ? G.nc[0] : G.n[0], n1 = coarse ? G.nc[1] : G.n[1], n2 = coarse ? G.nc[2] : G.n[2];
+        bool f0 = false, f1 = false, f2 = false;
+        int si = bc_map(i, n0, t.bc & 3, (t.bc >> 2) & 3, f0);
+        int sj = bc_map(j, n1, (t.bc >> 4) & 3, (t.bc >> 6) & 3, f1);
+        int sk = bc_map(k, n2, (t.bc >> 8) & 3, (t.bc >> 10) & 3, f2);
+        if (coarse) {
+          double* base = A.C + (int64_t)t.dst_slot * G.cbstride;
+          int64_t dq = ((int64_t)(k + G.cg) * G.NC[1] + (j + G.cg)) * G.NC[0] + (i + G.cg);
+          int64_t sq = ((int64_t)(sk + G.cg) * G.NC[1] + (sj + G.cg)) * G.NC[0] + (si + G.cg);
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) {
+            double val = base[v * G.cvstride + sq];
+            bool fl = (v == 1 && f0) || (v == 2 && f1) || (v == 3 && f2);
+            base[v * G.cvstride + dq] = fl ? -val : val;
+          }
+        } else {
+          double* base = A.U + (int64_t)t.dst_slot * G.bstride;
+          int64_t dq = ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+          int64_t sq = ((int64_t)(sk + G.g) * G.N[1] + (sj + G.g)) * G.N[0] + (si + G.g);
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) {
+            double val = base[v * G.vstride + sq];
+            bool fl = (v == 1 && f0) || (v == 2 && f1) || (v == 3 && f2);
+            base[v * G.vstride + dq] = fl ? -val : val;
+          }
+        }
+        break;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------------------ reflux (O8 / a8)
+// U_c(adjacent cell) += w dt s (F_own - F_corr) / dx, F_corr = pairwise mean of 4 fine fluxes.
+__global__ void reflux_kernel(const RefluxTask* tasks, double* U, const BlockMeta* meta, const double* fbuf,
+                              const CycleState* st, double w, Geom G) {
+  const RefluxTask t = tasks[blockIdx.y];
+  const int d = t.dir;
+  const int ta = (d == 0) ? 1 : 0, tb = (d == 2) ? 1 : 2;  // tangential dims, increasing
+  const int na = G.n[ta], nb = G.n[tb];
+  const int qa = na / 2, qb = nb / 2;
+  const int idxc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idxc >= qa * qb) return;
+  const int A0 = idxc % qa, B0 = idxc / qa;
+  const int Ac = t.t0lo + A0, Bc = t.t1lo + B0;
+  const double dt = st->dt_used;
+  const double fac = w * dt * meta[t.cslot].idx[d] * (double)t.side;
+  const int64_t fst = (int64_t)na * nb;
+  const double* ff = fbuf + (int64_t)t.ffs * G.fstride;
+  const double* cf = fbuf + (int64_t)t.cfs * G.fstride;
+  int c[3];
+  c[d] = (t.side < 0) ? 0 : G.n[d] - 1;
+  c[ta] = Ac;
+  c[tb] = Bc;
+  double* u = U + (int64_t)t.cslot * G.bstride + ((int64_t)(c[2] + G.g) * G.N[1] + (c[1] + G.g)) * G.N[0] + (c[0] + G.g);
+  const int a0 = 2 * A0, b0 = 2 * B0;
+#pragma unroll
+  for (int v = 0; v < NVAR; ++v) {
+    const double* f = ff + v * fst;
+    double f00 = f[(int64_t)b0 * na + a0], f10 = f[(int64_t)b0 * na + a0 + 1];
+    double f01 = f[(int64_t)(b0 + 1) * na + a0], f11 = f[(int64_t)(b0 + 1) * na + a0 + 1];
+    double corr = ((f00 + f10) + (f01 + f11)) * 0.25;
+    double own = cf[v * fst + (int64_t)Bc * na + Ac];
+    u[v * G.vstride] += fac * (own - corr);
+  }
+}
+
+// ------------------------------------------------------------------------------ problem generators (O4)
+
+
+__global__ void pgen_kernel(double* U, const BlockMeta* meta, int nslots, PgenArgs P, Geom G) {
+  const int row = blockIdx.x;  // (slot, k, j)
+  const int j = row % G.n[1];
+  const int k = (row / G.n[1]) % G.n[2];
+  const int slot = row / (G.n[1] * G.n[2]);
+  if (slot >= nslots) return;
+  const BlockMeta& M = meta[slot];
+  const double gamma = G.gamma;
+  for (int i = threadIdx.x; i < G.n[0]; i += blockDim.x) {
+    double x = __dadd_rn(M.xmin[0], __dmul_rn((double)i + 0.5, M.dx[0]));
+    double y = __dadd_rn(M.xmin[1], __dmul_rn((double)j + 0.5, M.dx[1]));
+    double z = __dadd_rn(M.xmin[2], __dmul_rn((double)k + 0.5, M.dx[2]));
+    double W[5];
+    if (P.problem == 0) {  // linear wave, right-going acoustic eigenvector (A20)
+      double A = P.p[0];
+      double K1 = P.p[1] / P.L[0], K2 = P.p[2] / P.L[1], K3 = P.p[3] / P.L[2];
+      double kn = sqrt(__dadd_rn(__dadd_rn(__dmul_rn(K1, K1), __dmul_rn(K2, K2)), __dmul_rn(K3, K3)));
+      double ph = __dadd_rn(__dadd_rn(__dmul_rn(K1, __dsub_rn(x, P.xmin[0])), __dmul_rn(K2, __dsub_rn(y, P.xmin[1]))),
+                            __dmul_rn(K3, __dsub_rn(z, P.xmin[2])));
+      double s = sin(__dmul_rn(2.0 * 3.14159265358979323846, ph));
+      W[0] = __dadd_rn(1.0, __dmul_rn(A, s));
+      double va = __dmul_rn(A, s);  // c0 = 1
+      W[1] = __dmul_rn(va, K1 / kn);
+      W[2] = __dmul_rn(va, K2 / kn);
+      W[3] = __dmul_rn(va, K3 / kn);
+      W[4] = __dadd_rn(1.0 / gamma, __dmul_rn(A, s));
+    } else if (P.problem == 1) {  // Sod (A22)
+      bool left = x < P.p[0];
+      W[0] = left ? 1.0 : 0.125;
+      W[4] = left ? 1.0 : 0.1;
+      W[1] = W[2] = W[3] = 0.0;
+    } else {  // blast (A21)
+      double dx = __dsub_rn(x, P.p[3]), dy = __dsub_rn(y, P.p[4]), dz = __dsub_rn(z, P.p[5]);
+      double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+      W[0] = 1.0;
+      W[1] = W[2] = W[3] = 0.0;
+      W[4] = (r2 < __dmul_rn(P.p[2], P.p[2])) ? P.p[0] : P.p[1];
+    }
+    double* u = U + (int64_t)slot * G.bstride + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+    double rho = W[0];
+    u[0] = rho;
+    u[G.vstride] = __dmul_rn(rho, W[1]);
+    u[2 * G.vstride] = __dmul_rn(rho, W[2]);
+    u[3 * G.vstride] = __dmul_rn(rho, W[3]);
+    double ke = __dadd_rn(__dadd_rn(__dmul_rn(W[1], W[1]), __dmul_rn(W[2], W[2])), __dmul_rn(W[3], W[3]));
+    u[4 * G.vstride] = __dadd_rn(W[4] / G.gm1, __dmul_rn(__dmul_rn(0.5, rho), ke));
+  }
+}
+
+// ------------------------------------------------------------------------------ reductions (a6, a10)
+// Standalone dt / totals pass over interiors (initial dt, multilevel after reflux, ph_totals).
+__global__ void reduce_kernel(const double* U, const BlockMeta* meta, int nslots, double* partials, int cta_base,
+                              ErrWord* err, Geom G) {
+  const int row = blockIdx.x;  // (slot, k)
+  const int k = row % G.n[2];
+  const int slot = row / G.n[2];
+  double tmax = 0.0, ts[NVAR] = {0, 0, 0, 0, 0};
+  if (slot < nslots) {
+    const BlockMeta& M = meta[slot];
+    const int nij = G.n[0] * G.n[1];
+    for (int c = threadIdx.x; c < nij; c += blockDim.x) {
+      int j = c / G.n[0], i = c % G.n[0];
+      const double* u = U + (int64_t)slot * G.bstride + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+      double un[NVAR];
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) un[v] = u[v * G.vstride];
+      double ir = 1.0 / un[0];
+      double v1 = un[1] * ir, v2 = un[2] * ir, v3 = un[3] * ir;
+      double ke = 0.5 * ((un[1] * v1 + un[2] * v2) + un[3] * v3);
+      double p = G.gm1 * (un[4] - ke);
+      if (!(un[0] > 0.0) || !(p > 0.0)) set_error(err, 0, M.gid, k, j, i);
+      double cs = sqrt(G.gamma * p * ir);
+      double s1 = (fabs(v1) + cs) * M.idx[0], s2 = (fabs(v2) + cs) * M.idx[1], s3 = (fabs(v3) + cs) * M.idx[2];
+      tmax = fmax(tmax, fmax(s1, fmax(s2, s3)));
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) ts[v] += un[v];
+    }
+  }
+  __shared__ double red[32][6];
+  for (int off = 16; off > 0; off >>= 1) {
+    tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) ts[v] += __shfl_xor_sync(0xffffffffu, ts[v], off);
+  }
+  int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (lane == 0) {
+    red[warp][0] = tmax;
+    for (int v = 0; v < NVAR; ++v) red[warp][1 + v] = ts[v];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0, s[NVAR] = {0, 0, 0, 0, 0};
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) {
+      m = fmax(m, red[w][0]);
+      for (int v = 0; v < NVAR; ++v) s[v] += red[w][1 + v];
+    }
+    double dV = slot < nslots ? meta[slot].dV : 0.0;
+    double* o = partials + (int64_t)(cta_base + blockIdx.x) * 6;
+    o[0] = m;
+    for (int v = 0; v < NVAR; ++v) o[1 + v] = s[v] * dV;
+  }
+}
+
+// partials [n][6] -> out[6] (max, 5 sums), deterministic for fixed n
+__global__ void rank_reduce_kernel(const double* partials, int n, double* out) {
+  __shared__ double sm[256][6];
+  double m = 0.0, s[NVAR] = {0, 0, 0, 0, 0};
+  for (int c = threadIdx.x; c < n; c += 256) {
+    const double* p = partials + (int64_t)c * 6;
+    m = fmax(m, p[0]);
+    for (int v = 0; v < NVAR; ++v) s[v] += p[1 + v];
+  }
+  sm[threadIdx.x][0] = m;
+  for (int v = 0; v < NVAR; ++v) sm[threadIdx.x][1 + v] = s[v];
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      sm[threadIdx.x][0] = fmax(sm[threadIdx.x][0], sm[threadIdx.x + w][0]);
+      for (int v = 0; v < NVAR; ++v) sm[threadIdx.x][1 + v] += sm[threadIdx.x + w][1 + v];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int v = 0; v < 6; ++v) out[v] = sm[0][v];
+}
+
+// mode 0: initial dt (no history); mode 1: end of cycle; mode 2: totals only (out6 -> tot)
+__global__ void finalize_kernel(const double* all, int nranks, CycleState* st, double* hist, int hist_cap,
+                                double cfl, int mode, double* tot_out) {
+  double m = 0.0, s[NVAR] = {0, 0, 0, 0, 0};
+  for (int r = 0; r < nranks; ++r) {
+    m = fmax(m, all[r * 6]);
+    for (int v = 0; v < NVAR; ++v) s[v] += all[r * 6 + 1 + v];
+  }
+  if (tot_out)
+    for (int v = 0; v < NVAR; ++v) tot_out[v] = s[v];
+  if (mode == 2) return;
+  double dt_new = cfl / m;  // cfl * min(dx/(|v|+c)) (O6)
+  if (mode == 0) {
+    st->dt = dt_new;
+    return;
+  }
+  if (!st->active) return;
+  st->t += st->dt_used;
+  st->cycle += 1;
+  st->dt = dt_new;
+  long long r = st->hist_count % hist_cap;
+  double* h = hist + r * 7;
+  h[0] = st->t;
+  h[1] = st->dt_used;
+  for (int v = 0; v < NVAR; ++v) h[2 + v] = s[v];
+  st->hist_count += 1;
+}
+
+__global__ void cycle_begin_kernel(CycleState* st, double tlim, int set_tlim) {
+  if (set_tlim) st->tlim = tlim;
+  double t = st->t, dt = st->dt, tl = st->tlim;
+  int active = !(tl > 0.0 && t >= tl);
+  double du = dt;
+  if (tl > 0.0 && t + dt > tl) du = tl - t;
+  st->active = active;
+  st->dt_used = active ? du : 0.0;
+}
+
+// ------------------------------------------------------------------------------ interior copies
+// buf [slot][5][n3][n2][n1] <-> pool interiors (host-state upload / download, e2e path)
+__global__ void interior_copy_kernel(double* U, double* buf, int slot0, int to_pool, Geom G) {
+  const int row = blockIdx.x;  // (slot, v, k, j)
+  const int j = row % G.n[1];
+  const int k = (row / G.n[1]) % G.n[2];
+  const int v = (row / (G.n[1] * G.n[2])) % NVAR;
+  const int s = row / (G.n[1] * G.n[2] * NVAR);
+  double* u = U + (int64_t)(slot0 + s) * G.bstride + v * G.vstride + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + G.g;
+  double* b = buf + (int64_t)row * G.n[0];
+  for (int i = threadIdx.x; i < G.n[0]; i += blockDim.x) {
+    if (to_pool) u[i] = b[i];
+    else b[i] = u[i];
+  }
+}
+
+// ------------------------------------------------------------------------------ launchers
+#define PH_CHECK_LAUNCH() cudaGetLastError()
+
+cudaError_t launch_stage(int recon, bool reduce, bool use_u0, int nblk_cta, const StageArgs& a, const Geom& G,
+                         cudaStream_t s) {
+  size_t sm = stage_smem_bytes();
+  dim3 grid(nblk_cta), block(NT);
+#define PH_STAGE_CASE(R, RD, U0)                                                                    \
+  if (recon == R && reduce == RD && use_u0 == U0) {                                                 \
+    static bool attr = false;                                                                       \
+    if (!attr) {                                                                                    \
+      cudaFuncSetAttribute(stage_kernel<R, RD, U0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+      attr = true;                                                                                  \
+    }                                                                                               \
+    stage_kernel<R, RD, U0><<<grid, block, sm, s>>>(a, G);                                          \
+    return PH_CHECK_LAUNCH();                                                                       \
+  }
+  PH_STAGE_CASE(0, false, false)
+  PH_STAGE_CASE(0, false, true)
+  PH_STAGE_CASE(0, true, false)
+  PH_STAGE_CASE(0, true, true)
+  PH_STAGE_CASE(1, false, false)
+  PH_STAGE_CASE(1, false, true)
+  PH_STAGE_CASE(1, true, false)
+  PH_STAGE_CASE(1, true, true)
+  PH_STAGE_CASE(2, false, false)
+  PH_STAGE_CASE(2, false, true)
+  PH_STAGE_CASE(2, true, false)
+  PH_STAGE_CASE(2, true, true)
+#undef PH_STAGE_CASE
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_xfill(int nchunks, const XArgs& a, const Geom& G, cudaStream_t s) {
+  if (nchunks <= 0) return cudaSuccess;
+  xfill_kernel<<<nchunks, XT, 0, s>>>(a, G);
+  return PH_CHECK_LAUNCH();
+}
+
+cudaError_t launch_reflux(int ntasks, const RefluxTask* t, double* U, const BlockMeta* meta, const double* fbuf,
+                          const CycleState* st, double w, const Geom& G, cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  int qa = G.n[1] / 2 * G.n[2] / 2;  // upper bound of face quarter cells over dirs
+  int q2 = G.n[0] / 2 * G.n[2] / 2, q3 = G.n[0] / 2 * G.n[1] / 2;
+  int q = qa > q2 ? qa : q2;
+  q = q > q3 ? q : q3;
+  dim3 grid((q + 127) / 128, ntasks);
+  reflux_kernel<<<grid, 128, 0, s>>>(t, U, meta, fbuf, st, w, G);
+  return PH_CHECK_LAUNCH();
+}
+
+cudaError_t launch_pgen(double* U, const BlockMeta* meta, int nslots, const PgenArgs& P, const Geom& G,
+                        cudaStream_t s) {
+  if (nslots <= 0) return cudaSuccess;
+  pgen_kernel<<<nslots * G.n[1] * G.n[2], 128, 0, s>>>(U, meta, nslots, P, G);
+  return PH_CHECK_LAUNCH();
+}
+
+cudaError_t launch_reduce(const double* U, const BlockMeta* meta, int nslots, double* partials, ErrWord* err,
+                          const Geom& G, cudaStream_t s) {
+  if (nslots <= 0) return cudaSuccess;
+  reduce_kernel<<<nslots * G.n[2], 256, 0, s>>>(U, meta, nslots, partials, 0, err, G);
+  return PH_CHECK_LAUNCH();
+}
+
+cudaError_t launch_rank_reduce(const double* partials, int n, double* out, cudaStream_t s) {
+  rank_reduce_kernel<<<1, 256, 0, s>>>(partials, n, out);
+  return PH_CHECK_LAUNCH();
+}
+
+cudaError_t launch_finalize(const double* all, int nranks, CycleState* st, double* hist, int hist_cap, double cfl,
+                            int mode, double* tot_out, cudaStream_t s) {
+  finalize_kernel<<<1, 1, 0, s>>>(all, nranks, st, hist, hist_cap, cfl, mode, tot_out);
+  return PH_CHECK_LAUNCH();
+}
+
+cudaError_t launch_cycle_begin(CycleState* st, double tlim, int set_tlim, cudaStream_t s) {
+  cycle_begin_kernel<<<1, 1, 0, s>>>(st, tlim, set_tlim);
+  return PH_CHECK_LAUNCH();
+}
+
+cudaError_t launch_interior_copy(double* U, double* buf, int slot0, int nslots, int to_pool, const Geom& G,
+                                 cudaStream_t s) {
+  if (nslots <= 0) return cudaSuccess;
+  interior_copy_kernel<<<nslots * NVAR * G.n[2] * G.n[1], 128, 0, s>>>(U, buf, slot0, to_pool, G);
+  return PH_CHECK_LAUNCH();
+}
+
+}  // namespace ph
