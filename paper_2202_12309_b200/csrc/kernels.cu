@@ -42,17 +42,44 @@ __device__ __forceinline__ void plm_face(double q0, double q1, double q2, double
   wr = fma(-0.5, s2, q2);
 }
 
+// MUFU-seeded Newton reciprocal: rcp.approx (~2^-23) + 2 iterations -> ~1 ulp.  The paper fixes no
+// rounding; parity with the oracle's IEEE division is at round-off ("fp64 budget").
+__device__ __forceinline__ double rcp_nr(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// MUFU-seeded Newton reciprocal square root (2 iterations)
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double h = 0.5 * x;
+  double e = fma(-h, y * y, 0.5);
+  y = fma(y, e, y);
+  e = fma(-h, y * y, 0.5);
+  return fma(y, e, y);
+}
+
+// sound speed c = sqrt(gamma p / rho) = (gamma p) * rsqrt(gamma p rho): one MUFU, no division
+__device__ __forceinline__ double sound_speed(double rho, double p, double gamma) {
+  double gp = gamma * p;
+  return gp * rsqrt_nr(gp * rho);
+}
+
 // HLLE, Davis speeds, clamped branch-free form (a4; A4, A5).  w = (rho, u_n, v_t1, v_t2, p).
 __device__ __forceinline__ void hlle(const double* wl, const double* wr, const Geom& G, double* F) {
-  double cl = sqrt(G.gamma * wl[4] / wl[0]);
-  double cr = sqrt(G.gamma * wr[4] / wr[0]);
+  double cl = sound_speed(wl[0], wl[4], G.gamma);
+  double cr = sound_speed(wr[0], wr[4], G.gamma);
   double sl = fmin(wl[1] - cl, wr[1] - cr);
   double sr = fmax(wl[1] + cl, wr[1] + cr);
   double bp = fmax(sr, 0.0);
   double bm = fmin(sl, 0.0);
-  double inv = 1.0 / (bp - bm);
+  double inv = rcp_nr(bp - bm);
   double bb = bp * bm;
-  // left state
   double mul = wl[0] * wl[1];
   double El = wl[4] * G.inv_gm1 + (0.5 * wl[0]) * (wl[1] * wl[1] + (wl[2] * wl[2] + wl[3] * wl[3]));
   double mur = wr[0] * wr[1];
@@ -77,23 +104,27 @@ __device__ __forceinline__ void set_error(ErrWord* err, int stage, long long gid
 }
 
 // ------------------------------------------------------------------------------ stage kernel
-// One CTA = a TX x TY tile of (i,j) columns of one block, marching over a k-range of KC planes.
-// Per plane: the plus-shaped halo plane is converted to primitives into smem (a2); x and y face
-// fluxes (a3+a4) go to smem; the z direction is carried in registers per column; each cell is
-// finished two planes later with the flux divergence and the RK stage combine (a5).  The final
-// stage also produces the CFL dt term and the conserved totals (a6, a10) per CTA.
+// One CTA = a TX x TY tile of (i,j) columns of one block, marching up a k-range of KC planes.
+// Plane q is converted to primitives (a2) into slot q%4 of a 4-plane smem ring (plus-shaped
+// x/y halo).  Iteration q then computes, as ONE flat work list balanced over all 256 threads,
+// the x and y faces of plane q-2 and the z faces between planes q-2 and q-1 (a3 PLM + a4 HLLE,
+// one shared code path per face), and finishes the cells of plane q-2: flux divergence and the
+// RK stage combine (a5).  The final stage also reduces the CFL term and the totals (a6, a10).
 constexpr int TX = TILE_X, TY = TILE_Y, NT = TX * TY;
 constexpr int SWX = TX + 4, SWY = TY + 4;
-
-
+constexpr int VS = SWY * SWX;           // var stride in a ring slot
+constexpr int SLOT = NVAR * VS;         // doubles per ring slot
+constexpr int FXS = TY * (TX + 1);      // var stride of sFx
+constexpr int FYS = (TY + 1) * TX;      // var stride of sFy
+constexpr int FZS = NT;                 // var stride of sFz
 
 template <int RECON, bool REDUCE, bool USE_U0>
 __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   extern __shared__ double smem[];
-  double* sW = smem;                          // [5][SWY][SWX]
-  double* sFx = sW + NVAR * SWY * SWX;        // [5][TY][TX+1]
-  double* sFy = sFx + NVAR * TY * (TX + 1);   // [5][TY+1][TX]
-  double* sS = sFy + NVAR * (TY + 1) * TX;    // [3][5][TY][TX]
+  double* sW = smem;                       // [4][5][SWY][SWX]
+  double* sFx = sW + 4 * SLOT;             // [5][TY][TX+1]
+  double* sFy = sFx + NVAR * FXS;          // [5][TY+1][TX]
+  double* sFz = sFy + NVAR * FYS;          // [2][5][TY][TX]
 
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
@@ -117,7 +148,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   const double idx1 = M.idx[0], idx2 = M.idx[1], idx3 = M.idx[2];
   const bool own = (tx < nxt) && (ty < nyt);
 
-  // ---- load-slot geometry (two cells per thread for interior planes) ----
+  // ---- load-slot geometry: the plus-shaped halo plane is 2 cells per thread ----
   int sl_i[2], sl_j[2];
   bool sl_ok[2];
 #pragma unroll
@@ -129,6 +160,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
       j = c / SWX;
       i = c % SWX - 2;
       ok = (j < nyt) && (i < nxt + 2);
+      if (j >= nyt && j < nyt + 2 && i >= 0 && i < nxt) ok = true;  // ragged tile: rows nyt, nyt+1
     } else {
       int c2 = c - SWX * TY;
       int r = c2 / TX;
@@ -136,8 +168,6 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
       j = (r < 2) ? r - 2 : TY + r - 2;
       ok = (c2 < 4 * TX) && (i < nxt) && ((r < 2) || (nyt == TY));
     }
-    // rows j in [nyt, nyt+2) of a ragged tile live in the first region
-    if (c < SWX * TY && j >= nyt && j < nyt + 2 && i >= 0 && i < nxt) ok = true;
     sl_i[s] = i;
     sl_j[s] = j;
     sl_ok[s] = ok;
@@ -145,7 +175,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
 
   double pf[2][NVAR];
   auto issue_load = [&](int q) {
-    bool halo = (q < k0) || (q >= k1);
+    const bool halo = (q < k0) || (q >= k1);
     const double* base = Ub + (int64_t)(q + g) * plane;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -159,186 +189,157 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
     }
   };
   auto store_prims = [&](int q) {
-    bool halo = (q < k0) || (q >= k1);
+    const bool halo = (q < k0) || (q >= k1);
+    double* W = sW + (q & 3) * SLOT;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       int i = halo ? tx : sl_i[s], j = halo ? ty : sl_j[s];
       bool ok = halo ? (s == 0 && own) : sl_ok[s];
       if (ok) {
         double rho = pf[s][0];
-        double ir = 1.0 / rho;
+        double ir = rcp_nr(rho);
         double v1 = pf[s][1] * ir, v2 = pf[s][2] * ir, v3 = pf[s][3] * ir;
         double ke = 0.5 * ((pf[s][1] * v1 + pf[s][2] * v2) + pf[s][3] * v3);
         double p = G.gm1 * (pf[s][4] - ke);
         if (!(rho > 0.0) || !(p > 0.0)) set_error(A.err, A.stage, M.gid, q, y0 + j, x0 + i);
         int o = (j + 2) * SWX + (i + 2);
-        sW[o] = rho;
-        sW[SWY * SWX + o] = v1;
-        sW[2 * SWY * SWX + o] = v2;
-        sW[3 * SWY * SWX + o] = v3;
-        sW[4 * SWY * SWX + o] = p;
+        W[o] = rho;
+        W[VS + o] = v1;
+        W[2 * VS + o] = v2;
+        W[3 * VS + o] = v3;
+        W[4 * VS + o] = p;
       }
     }
   };
 
-  // z-direction state of my column
-  double wprev[NVAR], dprev[NVAR], topprev[NVAR], fzprev[NVAR];
   double tmax = 0.0, tsum[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};
   const int qbeg = k0 - 2, qend = k1 + 2;
+  const int nfx = (nxt + 1) * nyt, nfy = nxt * (nyt + 1), nfz = nxt * nyt;
   issue_load(qbeg);
   for (int q = qbeg; q < qend; ++q) {
-    __syncthreads();
     store_prims(q);
     if (q + 1 < qend) issue_load(q + 1);
     __syncthreads();
-    const bool interior = (q >= k0) && (q < k1);
-    if (interior) {
-      // x faces: (nxt+1) per row
-      const int nfx = (nxt + 1) * nyt;
-      for (int f = tid; f < nfx; f += NT) {
-        int j = f / (nxt + 1), fi = f % (nxt + 1);
-        const double* w = sW + (j + 2) * SWX + fi;  // w[0..3] = cells fi-2 .. fi+1
-        double wl[NVAR], wr[NVAR], F[NVAR];
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) {
-          const double* c = w + v * SWY * SWX;
-          plm_face<RECON>(c[0], c[1], c[2], c[3], wl[v], wr[v]);
-        }
-        double a[NVAR] = {wl[0], wl[1], wl[2], wl[3], wl[4]};
-        double b[NVAR] = {wr[0], wr[1], wr[2], wr[3], wr[4]};
-        hlle(a, b, G, F);  // normal = x1: (rho, v1, v2, v3, p)
-        double* o = sFx + j * (TX + 1) + fi;
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) o[v * TY * (TX + 1)] = F[v];
-        int gi = x0 + fi;
-        int fs = (gi == 0) ? M.fslot[0] : ((gi == G.n[0]) ? M.fslot[1] : -1);
-        if (fs >= 0) {
-          double* fb = A.fbuf + (int64_t)fs * G.fstride + (int64_t)q * G.n[1] + (y0 + j);
-          int64_t fst = (int64_t)G.n[1] * G.n[2];
-#pragma unroll
-          for (int v = 0; v < NVAR; ++v) fb[v * fst] = F[v];
+    const int c = q - 2;                 // plane whose x/y faces and cells are done now
+    const int fz = q - 1;                // z face between planes q-2 and q-1
+    const bool xy = (c >= k0) && (c < k1);
+    const bool zf = (fz >= k0) && (fz <= k1);
+    const int nitems = (xy ? nfx + nfy : 0) + (zf ? nfz : 0);
+    const double* Wc = sW + (c & 3) * SLOT;
+    for (int t = tid; t < nitems; t += NT) {
+      // ---- gather: four stencil points along the face normal, components permuted so that
+      // w = (rho, u_normal, v_t1, v_t2, p) (O5 a4) ----
+      const double *p0, *p1, *p2, *p3;
+      int cn, c1, c2;        // variable index of normal / tangential components
+      double* dst;           // flux destination (natural component order), stride fst
+      int fst;
+      int ftype, fa, fb;     // face type, in-tile coordinates for the face-flux buffer
+      int it = t;
+      if (xy && it < nfx) {
+        int j = it / (nxt + 1), fi = it - j * (nxt + 1);
+        p0 = Wc + (j + 2) * SWX + fi;
+        p1 = p0 + 1; p2 = p0 + 2; p3 = p0 + 3;
+        cn = 1; c1 = 2; c2 = 3;
+        dst = sFx + j * (TX + 1) + fi;
+        fst = FXS;
+        ftype = 0; fa = fi; fb = j;
+      } else {
+        if (xy) it -= nfx;
+        if (xy && it < nfy) {
+          int jf = it / nxt, i = it - jf * nxt;
+          p0 = Wc + jf * SWX + (i + 2);
+          p1 = p0 + SWX; p2 = p0 + 2 * SWX; p3 = p0 + 3 * SWX;
+          cn = 2; c1 = 3; c2 = 1;
+          dst = sFy + jf * TX + i;
+          fst = FYS;
+          ftype = 1; fa = i; fb = jf;
+        } else {
+          if (xy) it -= nfy;
+          int j = it / nxt, i = it - j * nxt;
+          int o = (j + 2) * SWX + (i + 2);
+          p0 = sW + ((q - 3) & 3) * SLOT + o;
+          p1 = sW + ((q - 2) & 3) * SLOT + o;
+          p2 = sW + ((q - 1) & 3) * SLOT + o;
+          p3 = sW + (q & 3) * SLOT + o;
+          cn = 3; c1 = 1; c2 = 2;
+          dst = sFz + (fz & 1) * NVAR * FZS + j * TX + i;
+          fst = FZS;
+          ftype = 2; fa = i; fb = j;
         }
       }
-      // y faces: (nyt+1) rows of nxt
-      const int nfy = nxt * (nyt + 1);
-      for (int f = tid; f < nfy; f += NT) {
-        int jf = f / nxt, i = f % nxt;
-        const double* w = sW + jf * SWX + (i + 2);  // rows jf-2 .. jf+1
-        double wl[NVAR], wr[NVAR], Fn[NVAR];
+      const int cv[NVAR] = {0, cn, c1, c2, 4};
+      double wl[NVAR], wr[NVAR], F[NVAR];
 #pragma unroll
-        for (int v = 0; v < NVAR; ++v) {
-          const double* c = w + v * SWY * SWX;
-          plm_face<RECON>(c[0], c[SWX], c[2 * SWX], c[3 * SWX], wl[v], wr[v]);
+      for (int s = 0; s < NVAR; ++s) {
+        const int o = cv[s] * VS;
+        plm_face<RECON>(p0[o], p1[o], p2[o], p3[o], wl[s], wr[s]);
+      }
+      hlle(wl, wr, G, F);
+#pragma unroll
+      for (int s = 0; s < NVAR; ++s) dst[cv[s] * fst] = F[s];
+      // coarse-fine block faces keep their fluxes for flux correction (O8)
+      if (A.fbuf) {
+        int fs = -1;
+        int64_t off = 0, fstr = 0;
+        if (ftype == 0) {
+          int gi = x0 + fa;
+          fs = (gi == 0) ? M.fslot[0] : ((gi == G.n[0]) ? M.fslot[1] : -1);
+          off = (int64_t)c * G.n[1] + (y0 + fb);
+          fstr = (int64_t)G.n[1] * G.n[2];
+        } else if (ftype == 1) {
+          int gj = y0 + fb;
+          fs = (gj == 0) ? M.fslot[2] : ((gj == G.n[1]) ? M.fslot[3] : -1);
+          off = (int64_t)c * G.n[0] + (x0 + fa);
+          fstr = (int64_t)G.n[0] * G.n[2];
+        } else {
+          fs = (fz == 0) ? M.fslot[4] : ((fz == G.n[2]) ? M.fslot[5] : -1);
+          off = (int64_t)(y0 + fb) * G.n[0] + (x0 + fa);
+          fstr = (int64_t)G.n[0] * G.n[1];
         }
-        double a[NVAR] = {wl[0], wl[2], wl[3], wl[1], wl[4]};  // normal = x2: (v2, v3, v1)
-        double b[NVAR] = {wr[0], wr[2], wr[3], wr[1], wr[4]};
-        hlle(a, b, G, Fn);
-        double F[NVAR] = {Fn[0], Fn[3], Fn[1], Fn[2], Fn[4]};
-        double* o = sFy + jf * TX + i;
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) o[v * (TY + 1) * TX] = F[v];
-        int gj = y0 + jf;
-        int fs = (gj == 0) ? M.fslot[2] : ((gj == G.n[1]) ? M.fslot[3] : -1);
         if (fs >= 0) {
-          double* fb = A.fbuf + (int64_t)fs * G.fstride + (int64_t)q * G.n[0] + (x0 + i);
-          int64_t fst = (int64_t)G.n[0] * G.n[2];
+          double* fb_ = A.fbuf + (int64_t)fs * G.fstride + off;
 #pragma unroll
-          for (int v = 0; v < NVAR; ++v) fb[v * fst] = F[v];
+          for (int s = 0; s < NVAR; ++s) fb_[cv[s] * fstr] = F[s];
         }
       }
     }
-    // ---- z direction for my column ----
-    double wz[NVAR];
-    if (own) {
-      int o = (ty + 2) * SWX + (tx + 2);
+    __syncthreads();
+    // ---- finish the cells of plane c: L = -(((dF1 + dF2) + dF3)) and the RK combine ----
+    if (xy && own) {
+      const int64_t cell = (int64_t)slot * G.bstride + (int64_t)(c + g) * plane +
+                           (int64_t)(y0 + ty + g) * G.N[0] + (x0 + tx + g);
+      const double* fzl = sFz + (c & 1) * NVAR * FZS + tid;        // face c   (lower)
+      const double* fzu = sFz + ((c + 1) & 1) * NVAR * FZS + tid;  // face c+1 (upper)
+      double un[NVAR];
 #pragma unroll
-      for (int v = 0; v < NVAR; ++v) wz[v] = sW[v * SWY * SWX + o];
-    }
-    __syncthreads();  // sFx / sFy complete
-    if (own) {
-      if (interior) {
-        int r = ((q % 3) + 3) % 3;
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) {
-          double d1 = (sFx[v * TY * (TX + 1) + ty * (TX + 1) + tx + 1] - sFx[v * TY * (TX + 1) + ty * (TX + 1) + tx]) * idx1;
-          double d2 = (sFy[v * (TY + 1) * TX + (ty + 1) * TX + tx] - sFy[v * (TY + 1) * TX + ty * TX + tx]) * idx2;
-          sS[(r * NVAR + v) * NT + tid] = d1 + d2;
-        }
+      for (int v = 0; v < NVAR; ++v) {
+        double d1 = (sFx[v * FXS + ty * (TX + 1) + tx + 1] - sFx[v * FXS + ty * (TX + 1) + tx]) * idx1;
+        double d2 = (sFy[v * FYS + (ty + 1) * TX + tx] - sFy[v * FYS + ty * TX + tx]) * idx2;
+        double d3 = (fzu[v * FZS] - fzl[v * FZS]) * idx3;
+        double L = -((d1 + d2) + d3);
+        double uin = A.Uin[cell + v * G.vstride];
+        double out = fma(A.b1, uin, (A.cdt * dt) * L);
+        if (USE_U0) out = fma(A.a0, A.U0[cell + v * G.vstride], out);
+        un[v] = out;
+        A.Uout[cell + v * G.vstride] = out;
       }
-      if (q >= qbeg + 1) {
-        double d[NVAR];
+      if (REDUCE) {
+        double ir = rcp_nr(un[0]);
+        double v1 = un[1] * ir, v2 = un[2] * ir, v3 = un[3] * ir;
+        double ke = 0.5 * ((un[1] * v1 + un[2] * v2) + un[3] * v3);
+        double p = G.gm1 * (un[4] - ke);
+        double cs = sound_speed(un[0], p, G.gamma);
+        double s1 = (fabs(v1) + cs) * idx1, s2 = (fabs(v2) + cs) * idx2, s3 = (fabs(v3) + cs) * idx3;
+        tmax = fmax(tmax, fmax(s1, fmax(s2, s3)));
 #pragma unroll
-        for (int v = 0; v < NVAR; ++v) d[v] = wz[v] - wprev[v];
-        if (q >= qbeg + 2) {
-          // slope of cell q-1, its bottom / top states
-          double bot[NVAR], top[NVAR];
-#pragma unroll
-          for (int v = 0; v < NVAR; ++v) {
-            double s = slope<RECON>(dprev[v], d[v]);
-            bot[v] = fma(-0.5, s, wprev[v]);
-            top[v] = fma(0.5, s, wprev[v]);
-          }
-          if (q >= qbeg + 3) {
-            // face between q-2 and q-1 (global face index q-1)
-            double a[NVAR] = {topprev[0], topprev[3], topprev[1], topprev[2], topprev[4]};  // normal = x3
-            double b[NVAR] = {bot[0], bot[3], bot[1], bot[2], bot[4]};
-            double Fn[NVAR];
-            hlle(a, b, G, Fn);
-            double Fz[NVAR] = {Fn[0], Fn[2], Fn[3], Fn[1], Fn[4]};
-            int gk = q - 1;
-            int fs = (gk == 0) ? M.fslot[4] : ((gk == G.n[2]) ? M.fslot[5] : -1);
-            if (fs >= 0) {
-              double* fb = A.fbuf + (int64_t)fs * G.fstride + (int64_t)(y0 + ty) * G.n[0] + (x0 + tx);
-              int64_t fst = (int64_t)G.n[0] * G.n[1];
-#pragma unroll
-              for (int v = 0; v < NVAR; ++v) fb[v * fst] = Fz[v];
-            }
-            if (q >= qbeg + 4) {
-              // finish cell c = q-2
-              const int c = q - 2;
-              const int r = ((c % 3) + 3) % 3;
-              const int64_t cell = (int64_t)slot * G.bstride + (int64_t)(c + g) * plane +
-                                   (int64_t)(y0 + ty + g) * G.N[0] + (x0 + tx + g);
-              double un[NVAR];
-#pragma unroll
-              for (int v = 0; v < NVAR; ++v) {
-                double dz = (Fz[v] - fzprev[v]) * idx3;
-                double L = -(sS[(r * NVAR + v) * NT + tid] + dz);
-                double uin = A.Uin[cell + v * G.vstride];
-                double out = fma(A.b1, uin, (A.cdt * dt) * L);
-                if (USE_U0) out = fma(A.a0, A.U0[cell + v * G.vstride], out);
-                un[v] = out;
-                A.Uout[cell + v * G.vstride] = out;
-              }
-              if (REDUCE) {
-                double ir = 1.0 / un[0];
-                double v1 = un[1] * ir, v2 = un[2] * ir, v3 = un[3] * ir;
-                double ke = 0.5 * ((un[1] * v1 + un[2] * v2) + un[3] * v3);
-                double p = G.gm1 * (un[4] - ke);
-                double cs = sqrt(G.gamma * p * ir);
-                double s1 = (fabs(v1) + cs) * idx1, s2 = (fabs(v2) + cs) * idx2, s3 = (fabs(v3) + cs) * idx3;
-                tmax = fmax(tmax, fmax(s1, fmax(s2, s3)));
-#pragma unroll
-                for (int v = 0; v < NVAR; ++v) tsum[v] += un[v];
-              }
-            }
-#pragma unroll
-            for (int v = 0; v < NVAR; ++v) fzprev[v] = Fz[v];
-          }
-#pragma unroll
-          for (int v = 0; v < NVAR; ++v) topprev[v] = top[v];
-        }
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) dprev[v] = d[v];
+        for (int v = 0; v < NVAR; ++v) tsum[v] += un[v];
       }
-#pragma unroll
-      for (int v = 0; v < NVAR; ++v) wprev[v] = wz[v];
     }
   }
   if (REDUCE) {
-    // deterministic CTA reduction: warp shuffles then warp 0 in fixed order
+    // deterministic CTA reduction: warp shuffles then thread 0 in fixed warp order
     __syncthreads();
-    double* red = smem;  // reuse sW
+    double* red = smem;
     for (int off = 16; off > 0; off >>= 1) {
       tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
 #pragma unroll
@@ -364,9 +365,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   }
 }
 
-size_t stage_smem_bytes() {
-  return sizeof(double) * (NVAR * SWY * SWX + NVAR * TY * (TX + 1) + NVAR * (TY + 1) * TX + 3 * NVAR * NT);
-}
+size_t stage_smem_bytes() { return sizeof(double) * (4 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS); }
 
 // ------------------------------------------------------------------------------ exchange kernel
 // One CTA per chunk of <= XCHUNK cells of one task; all tasks of one phase in one launch
@@ -623,12 +622,12 @@ __global__ void reduce_kernel(const double* U, const BlockMeta* meta, int nslots
       double un[NVAR];
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) un[v] = u[v * G.vstride];
-      double ir = 1.0 / un[0];
+      double ir = rcp_nr(un[0]);
       double v1 = un[1] * ir, v2 = un[2] * ir, v3 = un[3] * ir;
       double ke = 0.5 * ((un[1] * v1 + un[2] * v2) + un[3] * v3);
       double p = G.gm1 * (un[4] - ke);
       if (!(un[0] > 0.0) || !(p > 0.0)) set_error(err, 0, M.gid, k, j, i);
-      double cs = sqrt(G.gamma * p * ir);
+      double cs = sound_speed(un[0], p, G.gamma);
       double s1 = (fabs(v1) + cs) * M.idx[0], s2 = (fabs(v2) + cs) * M.idx[1], s3 = (fabs(v3) + cs) * M.idx[2];
       tmax = fmax(tmax, fmax(s1, fmax(s2, s3)));
 #pragma unroll
