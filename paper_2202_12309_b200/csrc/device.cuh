@@ -125,7 +125,7 @@ struct PgenArgs {
   double xmin[3], L[3];
 };
 
-constexpr int XCHUNK = 512;  // cells per exchange chunk (one CTA)
+constexpr int XCHUNK = 256;  // cells per exchange chunk (one CTA, one cell per thread)
 
 // launchers (kernels.cu)
 cudaError_t launch_stage(int recon, bool reduce, bool use_u0, int nblk_cta, const StageArgs& a, const Geom& G,

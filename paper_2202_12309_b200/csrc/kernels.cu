@@ -13,12 +13,13 @@
 namespace ph {
 
 // ------------------------------------------------------------------------------ point math
-// textbook minmod on the integer pipe: same sign bit -> the smaller magnitude
+// textbook minmod: same strict sign -> the smaller magnitude, else 0.  The sign test
+// reads only the high words (integer pipe); one DSETP with |.| modifiers picks the magnitude.
+// (+-0 operands give +-0, whose use q +- 0.5*(+-0) == q matches the oracle's 0.)
 __device__ __forceinline__ double minmod_i(double a, double b) {
-  long long ia = __double_as_longlong(a), ib = __double_as_longlong(b);
-  long long ma = ia & 0x7fffffffffffffffLL, mb = ib & 0x7fffffffffffffffLL;
-  long long m = (ma < mb) ? ia : ib;
-  return ((ia ^ ib) >= 0) ? __longlong_as_double(m) : 0.0;
+  const int ha = __double2hiint(a), hb = __double2hiint(b);
+  const double m = (fabs(a) < fabs(b)) ? a : b;
+  return ((ha ^ hb) >= 0) ? m : 0.0;
 }
 
 template <int RECON>
@@ -113,6 +114,27 @@ __device__ __forceinline__ void set_error(ErrWord* err, int stage, long long gid
 constexpr int TX = TILE_X, TY = TILE_Y, NT = TX * TY;
 constexpr int SWX = TX + 4, SWY = TY + 4;
 constexpr int VS = SWY * SWX;           // var stride in a ring slot
+
+// One face: PLM states from the 4 stencil points p0..p3 (cells c-2 .. c+1 along the normal) of
+// the smem primitives, permuted so that w = (rho, u_normal, v_t1, v_t2, p), then HLLE.  F is
+// returned in natural component order.  CN/C1/C2: variable index of normal, t1, t2.
+template <int RECON, int CN, int C1, int C2>
+__device__ __forceinline__ void face_flux(const double* p0, const double* p1, const double* p2, const double* p3,
+                                          const Geom& G, double* F) {
+  constexpr int cv[NVAR] = {0, CN, C1, C2, 4};
+  double wl[NVAR], wr[NVAR], Fn[NVAR];
+#pragma unroll
+  for (int s = 0; s < NVAR; ++s) {
+    const int o = cv[s] * VS;
+    plm_face<RECON>(p0[o], p1[o], p2[o], p3[o], wl[s], wr[s]);
+  }
+  hlle(wl, wr, G, Fn);
+  F[0] = Fn[0];
+  F[CN] = Fn[1];
+  F[C1] = Fn[2];
+  F[C2] = Fn[3];
+  F[4] = Fn[4];
+}
 constexpr int SLOT = NVAR * VS;         // doubles per ring slot
 constexpr int FXS = TY * (TX + 1);      // var stride of sFx
 constexpr int FYS = (TY + 1) * TX;      // var stride of sFy
@@ -214,7 +236,6 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
 
   double tmax = 0.0, tsum[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};
   const int qbeg = k0 - 2, qend = k1 + 2;
-  const int nfx = (nxt + 1) * nyt, nfy = nxt * (nyt + 1), nfz = nxt * nyt;
   issue_load(qbeg);
   for (int q = qbeg; q < qend; ++q) {
     store_prims(q);
@@ -224,82 +245,70 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
     const int fz = q - 1;                // z face between planes q-2 and q-1
     const bool xy = (c >= k0) && (c < k1);
     const bool zf = (fz >= k0) && (fz <= k1);
-    const int nitems = (xy ? nfx + nfy : 0) + (zf ? nfz : 0);
     const double* Wc = sW + (c & 3) * SLOT;
-    for (int t = tid; t < nitems; t += NT) {
-      // ---- gather: four stencil points along the face normal, components permuted so that
-      // w = (rho, u_normal, v_t1, v_t2, p) (O5 a4) ----
-      const double *p0, *p1, *p2, *p3;
-      int cn, c1, c2;        // variable index of normal / tangential components
-      double* dst;           // flux destination (natural component order), stride fst
-      int fst;
-      int ftype, fa, fb;     // face type, in-tile coordinates for the face-flux buffer
-      int it = t;
-      if (xy && it < nfx) {
-        int j = it / (nxt + 1), fi = it - j * (nxt + 1);
-        p0 = Wc + (j + 2) * SWX + fi;
-        p1 = p0 + 1; p2 = p0 + 2; p3 = p0 + 3;
-        cn = 1; c1 = 2; c2 = 3;
-        dst = sFx + j * (TX + 1) + fi;
-        fst = FXS;
-        ftype = 0; fa = fi; fb = j;
-      } else {
-        if (xy) it -= nfx;
-        if (xy && it < nfy) {
-          int jf = it / nxt, i = it - jf * nxt;
-          p0 = Wc + jf * SWX + (i + 2);
-          p1 = p0 + SWX; p2 = p0 + 2 * SWX; p3 = p0 + 3 * SWX;
-          cn = 2; c1 = 3; c2 = 1;
-          dst = sFy + jf * TX + i;
-          fst = FYS;
-          ftype = 1; fa = i; fb = jf;
-        } else {
-          if (xy) it -= nfy;
-          int j = it / nxt, i = it - j * nxt;
-          int o = (j + 2) * SWX + (i + 2);
-          p0 = sW + ((q - 3) & 3) * SLOT + o;
-          p1 = sW + ((q - 2) & 3) * SLOT + o;
-          p2 = sW + ((q - 1) & 3) * SLOT + o;
-          p3 = sW + (q & 3) * SLOT + o;
-          cn = 3; c1 = 1; c2 = 2;
-          dst = sFz + (fz & 1) * NVAR * FZS + j * TX + i;
-          fst = FZS;
-          ftype = 2; fa = i; fb = j;
+    // x faces of plane c: 33 per row, item t -> (row t/33, face t%33); rounds 0,1 (warp 0 only)
+    if (xy) {
+#pragma unroll 1
+      for (int t = tid; t < (TX + 1) * TY; t += NT) {
+        const int j = t / (TX + 1), fi = t - j * (TX + 1);
+        if (j < nyt && fi <= nxt) {
+          const double* p = Wc + (j + 2) * SWX + fi;
+          double F[NVAR];
+          face_flux<RECON, 1, 2, 3>(p, p + 1, p + 2, p + 3, G, F);
+          double* d = sFx + j * (TX + 1) + fi;
+          d[0] = F[0]; d[FXS] = F[1]; d[2 * FXS] = F[2]; d[3 * FXS] = F[3]; d[4 * FXS] = F[4];
+          if (A.fbuf) {
+            const int gi = x0 + fi;
+            const int fs = (gi == 0) ? M.fslot[0] : ((gi == G.n[0]) ? M.fslot[1] : -1);
+            if (fs >= 0) {
+              const int64_t fstr = (int64_t)G.n[1] * G.n[2];
+              double* o = A.fbuf + (int64_t)fs * G.fstride + (int64_t)c * G.n[1] + (y0 + j);
+#pragma unroll
+              for (int v = 0; v < NVAR; ++v) o[v * fstr] = F[v];
+            }
+          }
         }
       }
-      const int cv[NVAR] = {0, cn, c1, c2, 4};
-      double wl[NVAR], wr[NVAR], F[NVAR];
+      // y faces: 9 rows of 32; items rotated by 128 so the 9th row lands on warps 4-7
+#pragma unroll 1
+      for (int r = 0; r < 2; ++r) {
+        const int t = ((tid + 128) & (NT - 1)) + r * NT;
+        if (t >= TX * (TY + 1)) break;
+        const int jf = t / TX, i = t - jf * TX;
+        if (jf <= nyt && i < nxt) {
+          const double* p = Wc + jf * SWX + (i + 2);
+          double F[NVAR];
+          face_flux<RECON, 2, 3, 1>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
+          double* d = sFy + jf * TX + i;
+          d[0] = F[0]; d[FYS] = F[1]; d[2 * FYS] = F[2]; d[3 * FYS] = F[3]; d[4 * FYS] = F[4];
+          if (A.fbuf) {
+            const int gj = y0 + jf;
+            const int fs = (gj == 0) ? M.fslot[2] : ((gj == G.n[1]) ? M.fslot[3] : -1);
+            if (fs >= 0) {
+              const int64_t fstr = (int64_t)G.n[0] * G.n[2];
+              double* o = A.fbuf + (int64_t)fs * G.fstride + (int64_t)c * G.n[0] + (x0 + i);
 #pragma unroll
-      for (int s = 0; s < NVAR; ++s) {
-        const int o = cv[s] * VS;
-        plm_face<RECON>(p0[o], p1[o], p2[o], p3[o], wl[s], wr[s]);
+              for (int v = 0; v < NVAR; ++v) o[v * fstr] = F[v];
+            }
+          }
+        }
       }
-      hlle(wl, wr, G, F);
-#pragma unroll
-      for (int s = 0; s < NVAR; ++s) dst[cv[s] * fst] = F[s];
-      // coarse-fine block faces keep their fluxes for flux correction (O8)
+    }
+    // z face between planes q-2 and q-1 of my column
+    if (zf && own) {
+      const int o = (ty + 2) * SWX + (tx + 2);
+      double F[NVAR];
+      face_flux<RECON, 3, 1, 2>(sW + ((q - 3) & 3) * SLOT + o, sW + ((q - 2) & 3) * SLOT + o,
+                                sW + ((q - 1) & 3) * SLOT + o, sW + (q & 3) * SLOT + o, G, F);
+      double* d = sFz + (fz & 1) * NVAR * FZS + tid;
+      d[0] = F[0]; d[FZS] = F[1]; d[2 * FZS] = F[2]; d[3 * FZS] = F[3]; d[4 * FZS] = F[4];
       if (A.fbuf) {
-        int fs = -1;
-        int64_t off = 0, fstr = 0;
-        if (ftype == 0) {
-          int gi = x0 + fa;
-          fs = (gi == 0) ? M.fslot[0] : ((gi == G.n[0]) ? M.fslot[1] : -1);
-          off = (int64_t)c * G.n[1] + (y0 + fb);
-          fstr = (int64_t)G.n[1] * G.n[2];
-        } else if (ftype == 1) {
-          int gj = y0 + fb;
-          fs = (gj == 0) ? M.fslot[2] : ((gj == G.n[1]) ? M.fslot[3] : -1);
-          off = (int64_t)c * G.n[0] + (x0 + fa);
-          fstr = (int64_t)G.n[0] * G.n[2];
-        } else {
-          fs = (fz == 0) ? M.fslot[4] : ((fz == G.n[2]) ? M.fslot[5] : -1);
-          off = (int64_t)(y0 + fb) * G.n[0] + (x0 + fa);
-          fstr = (int64_t)G.n[0] * G.n[1];
-        }
+        const int fs = (fz == 0) ? M.fslot[4] : ((fz == G.n[2]) ? M.fslot[5] : -1);
         if (fs >= 0) {
-          double* fb_ = A.fbuf + (int64_t)fs * G.fstride + off;
+          const int64_t fstr = (int64_t)G.n[0] * G.n[1];
+          double* ob = A.fbuf + (int64_t)fs * G.fstride + (int64_t)(y0 + ty) * G.n[0] + (x0 + tx);
 #pragma unroll
-          for (int s = 0; s < NVAR; ++s) fb_[cv[s] * fstr] = F[s];
+          for (int v = 0; v < NVAR; ++v) ob[v * fstr] = F[v];
         }
       }
     }
@@ -370,7 +379,7 @@ size_t stage_smem_bytes() { return sizeof(double) * (4 * SLOT + NVAR * FXS + NVA
 // ------------------------------------------------------------------------------ exchange kernel
 // One CTA per chunk of <= XCHUNK cells of one task; all tasks of one phase in one launch
 // ("fill-in-one").
-constexpr int XT = 128;
+constexpr int XT = 256;
 
 
 
