@@ -1,0 +1,81 @@
+"""Multi-GPU parity check, launched with torchrun (one process per GPU, NCCL):
+
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port P tools/multi_check.py [--case blast]
+
+Every rank runs its Morton range; rank 0 gathers all blocks and compares them with (a) the CPU
+oracle (1e-12, tests/parity.py) and (b) a single-GPU run of the same problem (bitwise)."""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+CASES = {
+    "blast": dict(kw=dict(mesh_nx=(64, 64, 64), block_nx=(16, 16, 16), xmin=(-.5,) * 3, xmax=(.5,) * 3),
+                  problem=2, params=[10.0, 0.1, 0.15], cycles=10),
+    "sod_walls": dict(kw=dict(mesh_nx=(128, 32, 32), block_nx=(16, 16, 16), gamma=1.4,
+                              bc_inner=(1, 2, 0), bc_outer=(1, 2, 0)),
+                      problem=1, params=[0.5], cycles=10),
+    "wave64": dict(kw=dict(mesh_nx=(128, 64, 64), block_nx=(32, 32, 32)), problem=0,
+                   params=[1e-6, 1, 1, 1], cycles=10),
+}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", default="blast")
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2202_12309_b200 as P
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    C = CASES[a.case]
+    m = P.Mesh(device=local, rank=rank, nranks=world, **C["kw"])
+    m.set_problem(C["problem"], C["params"])
+    m.step(C["cycles"])
+    mine = {b["gid"]: m.get_state(b["gid"]) for b in m.blocks() if b["rank"] == rank}
+    hist = m.history()
+    tm = m.time()
+    info = m.plan_info()
+    objs = [None] * world
+    dist.gather_object(mine, objs if rank == 0 else None, dst=0)
+    ok = True
+    if rank == 0:
+        import oracle as O
+        from parity import errors
+        allb = {}
+        for o in objs:
+            allb.update(o)
+        G = np.stack([allb[g] for g in range(len(allb))])
+        orc = O.Mesh(**C["kw"])
+        orc.set_problem(C["problem"], C["params"])
+        orc.step(C["cycles"])
+        Og = np.stack([orc.get_state(g) for g in range(orc.num_blocks())])
+        e = errors(G, Og)
+        single = P.Mesh(device=local, **C["kw"])
+        single.set_problem(C["problem"], C["params"])
+        single.step(C["cycles"])
+        S = np.stack([single.get_state(g) for g in range(single.num_blocks())])
+        bitwise = bool(np.array_equal(S, G))
+        to = orc.time()
+        ho = orc.history()
+        res = dict(case=a.case, world=world, parity=e, max_err=max(e.values()), bitwise_vs_1gpu=bitwise,
+                   t=tm, t_oracle=to, dt_rel=abs(tm[1] - to[1]) / to[1],
+                   mass_rel=float(abs(hist[-1, 2] - ho[-1, 2]) / ho[-1, 2]),
+                   send_doubles=info["send_doubles_to"])
+        ok = res["max_err"] <= 1e-12 and bitwise and res["dt_rel"] <= 1e-12 and tm[2] == to[2]
+        res["ok"] = ok
+        print("MULTI_CHECK " + json.dumps(res), flush=True)
+    m.close()
+    dist.destroy_process_group()
+    sys.exit(0 if ok else 1)
+
+
+if __name__ == "__main__":
+    main()
