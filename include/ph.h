@@ -79,6 +79,9 @@ typedef struct {
   int32_t rank, nranks;             /* this process' rank and the number of GPUs */
   int32_t device;                   /* CUDA device ordinal */
   int32_t host_only;                /* 1: build the mesh/partition/exchange plan only (no GPU) */
+  int32_t no_direct_halo;           /* 1: materialise every ghost each exchange (the paper's scheme);
+                                       0 (default): on uniform meshes the stage kernel reads local
+                                       same-level face neighbours' interiors directly */
   void* stream;                     /* cudaStream_t to enqueue on (borrowed); NULL = legacy default */
   const void* nccl_id;              /* 128-byte ncclUniqueId (nranks > 1), else NULL */
   void* (*dev_alloc)(size_t bytes, void* ctx); /* optional device allocator (torch caching allocator) */
@@ -119,6 +122,13 @@ typedef struct {
   int64_t recv_doubles_from[64];
   uint64_t send_hash_to[64];    /* order-sensitive hash of the (dst gid, entry) sequence */
   uint64_t recv_hash_from[64];
+  /* the per-cycle exchange (direct halo: only remote faces and physical BCs on uniform meshes) */
+  int64_t cyc_send_doubles_to[64];
+  int64_t cyc_recv_doubles_from[64];
+  uint64_t cyc_send_hash_to[64];
+  uint64_t cyc_recv_hash_from[64];
+  int32_t direct_halo;          /* 1 if stage kernels read local same-level face neighbours directly */
+  int64_t n_cyc_local_tasks;
 } ph_plan_info;
 
 /* ---- lifecycle ---------------------------------------------------------------------------- */

@@ -52,6 +52,17 @@ struct Phase {
   int nchunks() const { return (int)chunks.size(); }
 };
 
+// One exchange plan: the fill-in-one phases of SURVEY O7 (A: pack / local / unpack, B1, B2, C, D)
+// plus the per-peer buffer layout.  plan[0] = full exchange (all 26 directions), plan[1] = the
+// per-cycle exchange (== full unless the direct-halo path makes some of it unnecessary).
+struct Plan {
+  Phase pack, local, unpack, b1, b2, pro, bcf;
+  std::vector<int64_t> send_off, send_cnt, recv_off, recv_cnt;  // per peer, doubles
+  std::vector<uint64_t> send_hash, recv_hash;
+  int64_t sbuf_n = 0, rbuf_n = 0;
+  std::vector<Phase*> phases() { return {&pack, &local, &unpack, &b1, &b2, &pro, &bcf}; }
+};
+
 struct ph_mesh {
   ph_config cfg;
   std::vector<double> regions;
@@ -81,10 +92,11 @@ struct ph_mesh {
   int hist_cap = 1 << 16;
   int n_cslots = 0, n_fslots = 0;
   std::vector<BlockMeta> meta;
-  // plan
-  Phase pack, local, unpack, b1, b2, pro, bcf;
-  std::vector<int64_t> send_off, send_cnt, recv_off, recv_cnt;  // per peer, doubles
-  std::vector<uint64_t> send_hash, recv_hash;
+  // plans: [0] full exchange, [1] per-cycle exchange
+  Plan plan[2];
+  bool no_direct_halo = false;  // config: force materialised ghosts every exchange
+  bool ghosts_stale = false;  // a direct-halo cycle ran since the last full exchange
+  bool direct_halo = false;  // uniform mesh: stage kernels read local same-level face neighbours directly
   std::vector<RefluxTask> reflux[3];
   RefluxTask* d_reflux[3] = {nullptr, nullptr, nullptr};
   // stage launch geometry
@@ -203,19 +215,172 @@ static bool region_physical(const BlockInfo& b, const int o[3]) {
   return false;
 }
 
-/* Build the per-exchange plan of this rank (fill-in-one phases A-D, remote first). */
-static ph_status build_plan(ph_mesh* m) {
+/* One exchange plan of this rank (fill-in-one phases A-D, remote first).  cyc: per-cycle plan of
+ * the direct-halo path -- drops the face copies between local same-level blocks (the stage kernel
+ * reads those neighbours' interiors directly) and, on uniform meshes, all edge / corner regions
+ * (the stage stencil is a plus shape: it never reads them). */
+static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>& cslot) {
   const int R = m->nranks, me = m->rank;
-  for (Phase* P : {&m->pack, &m->local, &m->unpack, &m->b1, &m->b2, &m->pro, &m->bcf}) {
-    P->tasks.clear();
-    P->chunks.clear();
+  for (Phase* ph : P.phases()) {
+    ph->tasks.clear();
+    ph->chunks.clear();
   }
-  m->send_off.assign(R, 0);
-  m->send_cnt.assign(R, 0);
-  m->recv_off.assign(R, 0);
-  m->recv_cnt.assign(R, 0);
-  m->send_hash.assign(R, 0);
-  m->recv_hash.assign(R, 0);
+  P.send_off.assign(R, 0);
+  P.send_cnt.assign(R, 0);
+  P.recv_off.assign(R, 0);
+  P.recv_cnt.assign(R, 0);
+  P.send_hash.assign(R, 0);
+  P.recv_hash.assign(R, 0);
+  // ---- phase A: per destination block (gid order), entries in canonical order
+  std::vector<int64_t> soff(R, 0), roff(R, 0);
+  std::vector<int> pack_peer, unpack_peer;
+  for (auto& b : m->blocks) {
+    for (auto& e : b.nbrs) {
+      const BlockInfo& s = m->blocks[e.gid];
+      bool dst_here = (b.rank == me), src_here = (s.rank == me);
+      if (!dst_here && !src_here) continue;
+      if (cyc) {
+        int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
+        if (nz > 1) continue;                               // edges / corners: never read
+        if (dst_here && src_here && e.dlevel == 0) continue;  // read directly by the stage kernel
+      }
+      XTask t = entry_task(m, b, e);
+      int cs = (t.kind == T_CCOPY) ? cslot[b.gid] : (int)b.local;
+      if (dst_here && src_here) {
+        t.dst_slot = cs;
+        t.src_slot = (int)s.local;
+        add_chunks(P.local, t);
+      } else if (src_here) {  // pack for b.rank
+        int peer = b.rank;
+        t.dst_slot = -1;
+        t.src_slot = (int)s.local;
+        t.buf = soff[peer];
+        soff[peer] += (int64_t)NVAR * t.ncell;
+        P.send_hash[peer] = mix(P.send_hash[peer], (uint64_t)b.gid * 64 + (uint64_t)(&e - &b.nbrs[0]));
+        pack_peer.push_back(peer);
+        add_chunks(P.pack, t);
+      } else {  // unpack from s.rank
+        int peer = s.rank;
+        t.kind = (t.kind == T_CCOPY) ? T_UNPACK_C : T_UNPACK_U;
+        t.dst_slot = cs;
+        t.src_slot = -1;
+        t.buf = roff[peer];
+        roff[peer] += (int64_t)NVAR * t.ncell;
+        P.recv_hash[peer] = mix(P.recv_hash[peer], (uint64_t)b.gid * 64 + (uint64_t)(&e - &b.nbrs[0]));
+        unpack_peer.push_back(peer);
+        add_chunks(P.unpack, t);
+      }
+    }
+  }
+  // per-peer buffer offsets (peer-major)
+  int64_t so = 0, ro = 0;
+  for (int p = 0; p < R; ++p) {
+    P.send_off[p] = so;
+    P.send_cnt[p] = soff[p];
+    so += soff[p];
+    P.recv_off[p] = ro;
+    P.recv_cnt[p] = roff[p];
+    ro += roff[p];
+  }
+  for (size_t i = 0; i < P.pack.tasks.size(); ++i) P.pack.tasks[i].buf += P.send_off[pack_peer[i]];
+  for (size_t i = 0; i < P.unpack.tasks.size(); ++i) P.unpack.tasks[i].buf += P.recv_off[unpack_peer[i]];
+  P.sbuf_n = so;
+  P.rbuf_n = ro;
+  // ---- phases B, C, D per local block
+  const int* n = m->G.n;
+  const int g = m->G.g, cg = m->G.cg;
+  for (int64_t gid : m->local_gids) {
+    const BlockInfo& b = m->blocks[gid];
+    int kind[27];
+    for (int q = 0; q < 27; ++q) kind[q] = -2;
+    for (auto& e : b.nbrs) kind[(e.off[2] + 1) * 9 + (e.off[1] + 1) * 3 + (e.off[0] + 1)] = e.dlevel;
+    bool anyphys = false;
+    for (int d = 0; d < 3; ++d) anyphys = anyphys || b.phys_lo[d] || b.phys_hi[d];
+    int bits = bc_bits(m, b);
+    if (b.has_coarser) {
+      int cs = cslot[gid];
+      XTask t{};
+      t.kind = T_CRESTRICT;
+      t.dst_slot = cs;
+      t.src_slot = (int)b.local;
+      for (int d = 0; d < 3; ++d) { t.lo[d] = 0; t.ext[d] = m->G.nc[d]; t.so[d] = 0; }
+      t.ncell = t.ext[0] * t.ext[1] * t.ext[2];
+      add_chunks(P.b1, t);
+      for (int q = 0; q < 27; ++q) {
+        if (q == 13 || kind[q] == -2 || kind[q] == -1) continue;
+        int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
+        XTask r{};
+        r.kind = T_CRESTRICT;
+        r.dst_slot = cs;
+        r.src_slot = (int)b.local;
+        for (int d = 0; d < 3; ++d) {
+          if (o[d] < 0) { r.lo[d] = -1; r.ext[d] = 1; }
+          else if (o[d] > 0) { r.lo[d] = m->G.nc[d]; r.ext[d] = 1; }
+          else { r.lo[d] = 0; r.ext[d] = m->G.nc[d]; }
+          r.so[d] = 0;
+        }
+        r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
+        add_chunks(P.b1, r);
+      }
+      for (int q = 0; q < 27 && anyphys; ++q) {
+        if (q == 13) continue;
+        int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
+        if (!region_physical(b, o)) continue;
+        XTask r{};
+        r.kind = T_BC_COARSE;
+        r.dst_slot = cs;
+        r.src_slot = cs;
+        r.bc = bits;
+        for (int d = 0; d < 3; ++d) {
+          if (o[d] < 0) { r.lo[d] = -cg; r.ext[d] = cg; }
+          else if (o[d] > 0) { r.lo[d] = m->G.nc[d]; r.ext[d] = cg; }
+          else { r.lo[d] = 0; r.ext[d] = m->G.nc[d]; }
+        }
+        r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
+        add_chunks(P.b2, r);
+      }
+      for (int q = 0; q < 27; ++q) {
+        if (q == 13 || kind[q] != -1) continue;
+        int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
+        XTask r{};
+        r.kind = T_PROLONG;
+        r.dst_slot = (int)b.local;
+        r.src_slot = cs;
+        for (int d = 0; d < 3; ++d) {
+          if (o[d] < 0) { r.lo[d] = -1; r.ext[d] = 1; }
+          else if (o[d] > 0) { r.lo[d] = m->G.nc[d]; r.ext[d] = 1; }
+          else { r.lo[d] = 0; r.ext[d] = m->G.nc[d]; }
+        }
+        r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
+        add_chunks(P.pro, r);
+      }
+    }
+    if (anyphys) {
+      for (int q = 0; q < 27; ++q) {
+        if (q == 13) continue;
+        int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
+        if (!region_physical(b, o)) continue;
+        if (cyc && ((o[0] != 0) + (o[1] != 0) + (o[2] != 0)) > 1) continue;
+        XTask r{};
+        r.kind = T_BC_FINE;
+        r.dst_slot = (int)b.local;
+        r.src_slot = (int)b.local;
+        r.bc = bits;
+        for (int d = 0; d < 3; ++d) {
+          if (o[d] < 0) { r.lo[d] = -g; r.ext[d] = g; }
+          else if (o[d] > 0) { r.lo[d] = n[d]; r.ext[d] = g; }
+          else { r.lo[d] = 0; r.ext[d] = n[d]; }
+        }
+        r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
+        add_chunks(P.bcf, r);
+      }
+    }
+  }
+}
+
+/* Slots, staging / face-flux slots, block metadata, reflux tasks and both exchange plans. */
+static ph_status build_plan(ph_mesh* m) {
+  const int me = m->rank;
   for (int d = 0; d < 3; ++d) m->reflux[d].clear();
   m->cross_rank_reflux = false;
   // slots
@@ -245,145 +410,13 @@ static ph_status build_plan(ph_mesh* m) {
       if (fslot[b.gid][face] < 0) fslot[b.gid][face] = m->n_fslots++;
     }
   }
-  // ---- phase A: per destination block (gid order), entries in canonical order
-  std::vector<int64_t> soff(R, 0), roff(R, 0);
-  std::vector<int> pack_peer, unpack_peer;
-  for (auto& b : m->blocks) {
-    for (auto& e : b.nbrs) {
-      const BlockInfo& s = m->blocks[e.gid];
-      bool dst_here = (b.rank == me), src_here = (s.rank == me);
-      if (!dst_here && !src_here) continue;
-      XTask t = entry_task(m, b, e);
-      int cs = (t.kind == T_CCOPY) ? cslot[b.gid] : (int)b.local;
-      if (dst_here && src_here) {
-        t.dst_slot = cs;
-        t.src_slot = (int)s.local;
-        add_chunks(m->local, t);
-      } else if (src_here) {  // pack for b.rank
-        int peer = b.rank;
-        t.dst_slot = -1;
-        t.src_slot = (int)s.local;
-        t.buf = soff[peer];
-        soff[peer] += (int64_t)NVAR * t.ncell;
-        m->send_hash[peer] = mix(m->send_hash[peer], (uint64_t)b.gid * 64 + (uint64_t)(&e - &b.nbrs[0]));
-        pack_peer.push_back(peer);
-        add_chunks(m->pack, t);
-      } else {  // unpack from s.rank
-        int peer = s.rank;
-        t.kind = (t.kind == T_CCOPY) ? T_UNPACK_C : T_UNPACK_U;
-        t.dst_slot = cs;
-        t.src_slot = -1;
-        t.buf = roff[peer];
-        roff[peer] += (int64_t)NVAR * t.ncell;
-        m->recv_hash[peer] = mix(m->recv_hash[peer], (uint64_t)b.gid * 64 + (uint64_t)(&e - &b.nbrs[0]));
-        unpack_peer.push_back(peer);
-        add_chunks(m->unpack, t);
-      }
-    }
-  }
-  // per-peer buffer offsets (peer-major)
-  int64_t so = 0, ro = 0;
-  for (int p = 0; p < R; ++p) {
-    m->send_off[p] = so;
-    m->send_cnt[p] = soff[p];
-    so += soff[p];
-    m->recv_off[p] = ro;
-    m->recv_cnt[p] = roff[p];
-    ro += roff[p];
-  }
-  for (size_t i = 0; i < m->pack.tasks.size(); ++i) m->pack.tasks[i].buf += m->send_off[pack_peer[i]];
-  for (size_t i = 0; i < m->unpack.tasks.size(); ++i) m->unpack.tasks[i].buf += m->recv_off[unpack_peer[i]];
-  m->sbuf_n = so;
-  m->rbuf_n = ro;
-  // ---- phases B, C, D per local block
+  m->direct_halo = !m->multilevel && !m->no_direct_halo;
+  build_exchange(m, m->plan[0], false, cslot);
+  build_exchange(m, m->plan[1], m->direct_halo, cslot);
+  // reflux tasks (coarse side)
   const int* n = m->G.n;
-  const int g = m->G.g, cg = m->G.cg;
   for (int64_t gid : m->local_gids) {
     const BlockInfo& b = m->blocks[gid];
-    int kind[27];
-    for (int q = 0; q < 27; ++q) kind[q] = -2;
-    for (auto& e : b.nbrs) kind[(e.off[2] + 1) * 9 + (e.off[1] + 1) * 3 + (e.off[0] + 1)] = e.dlevel;
-    bool anyphys = false;
-    for (int d = 0; d < 3; ++d) anyphys = anyphys || b.phys_lo[d] || b.phys_hi[d];
-    int bits = bc_bits(m, b);
-    if (b.has_coarser) {
-      int cs = cslot[gid];
-      XTask t{};
-      t.kind = T_CRESTRICT;
-      t.dst_slot = cs;
-      t.src_slot = (int)b.local;
-      for (int d = 0; d < 3; ++d) { t.lo[d] = 0; t.ext[d] = m->G.nc[d]; t.so[d] = 0; }
-      t.ncell = t.ext[0] * t.ext[1] * t.ext[2];
-      add_chunks(m->b1, t);
-      for (int q = 0; q < 27; ++q) {
-        if (q == 13 || kind[q] == -2 || kind[q] == -1) continue;
-        int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
-        XTask r{};
-        r.kind = T_CRESTRICT;
-        r.dst_slot = cs;
-        r.src_slot = (int)b.local;
-        for (int d = 0; d < 3; ++d) {
-          if (o[d] < 0) { r.lo[d] = -1; r.ext[d] = 1; }
-          else if (o[d] > 0) { r.lo[d] = m->G.nc[d]; r.ext[d] = 1; }
-          else { r.lo[d] = 0; r.ext[d] = m->G.nc[d]; }
-          r.so[d] = 0;
-        }
-        r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
-        add_chunks(m->b1, r);
-      }
-      for (int q = 0; q < 27 && anyphys; ++q) {
-        if (q == 13) continue;
-        int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
-        if (!region_physical(b, o)) continue;
-        XTask r{};
-        r.kind = T_BC_COARSE;
-        r.dst_slot = cs;
-        r.src_slot = cs;
-        r.bc = bits;
-        for (int d = 0; d < 3; ++d) {
-          if (o[d] < 0) { r.lo[d] = -cg; r.ext[d] = cg; }
-          else if (o[d] > 0) { r.lo[d] = m->G.nc[d]; r.ext[d] = cg; }
-          else { r.lo[d] = 0; r.ext[d] = m->G.nc[d]; }
-        }
-        r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
-        add_chunks(m->b2, r);
-      }
-      for (int q = 0; q < 27; ++q) {
-        if (q == 13 || kind[q] != -1) continue;
-        int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
-        XTask r{};
-        r.kind = T_PROLONG;
-        r.dst_slot = (int)b.local;
-        r.src_slot = cs;
-        for (int d = 0; d < 3; ++d) {
-          if (o[d] < 0) { r.lo[d] = -1; r.ext[d] = 1; }
-          else if (o[d] > 0) { r.lo[d] = m->G.nc[d]; r.ext[d] = 1; }
-          else { r.lo[d] = 0; r.ext[d] = m->G.nc[d]; }
-        }
-        r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
-        add_chunks(m->pro, r);
-      }
-    }
-    if (anyphys) {
-      for (int q = 0; q < 27; ++q) {
-        if (q == 13) continue;
-        int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
-        if (!region_physical(b, o)) continue;
-        XTask r{};
-        r.kind = T_BC_FINE;
-        r.dst_slot = (int)b.local;
-        r.src_slot = (int)b.local;
-        r.bc = bits;
-        for (int d = 0; d < 3; ++d) {
-          if (o[d] < 0) { r.lo[d] = -g; r.ext[d] = g; }
-          else if (o[d] > 0) { r.lo[d] = n[d]; r.ext[d] = g; }
-          else { r.lo[d] = 0; r.ext[d] = n[d]; }
-        }
-        r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
-        add_chunks(m->bcf, r);
-      }
-    }
-    // reflux tasks (coarse side)
     for (auto& e : b.nbrs) {
       int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
       if (nz != 1 || e.dlevel != 1) continue;
@@ -419,7 +452,18 @@ static ph_status build_plan(ph_mesh* m) {
     M.gid = b.gid;
     M.level = b.loc.level;
     M.cslot = cslot[b.gid];
-    for (int f = 0; f < 6; ++f) M.fslot[f] = fslot[b.gid][f];
+    for (int f = 0; f < 6; ++f) {
+      M.fslot[f] = fslot[b.gid][f];
+      M.nb[f] = -1;
+    }
+    if (m->direct_halo) {
+      for (auto& e : b.nbrs) {
+        int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
+        if (nz != 1 || e.dlevel != 0 || m->blocks[e.gid].rank != me) continue;
+        int d = e.off[0] ? 0 : (e.off[1] ? 1 : 2);
+        M.nb[2 * d + (e.off[d] > 0 ? 1 : 0)] = (int)m->blocks[e.gid].local;
+      }
+    }
   }
   return PH_OK;
 }
@@ -444,7 +488,10 @@ static ph_status setup_device(ph_mesh* m) {
   std::vector<int> slots(nloc);
   for (int64_t s = 0; s < nloc; ++s) slots[s] = (int)s;
   TRY(upload(m, &m->d_slots, slots));
-  for (Phase* P : {&m->pack, &m->local, &m->unpack, &m->b1, &m->b2, &m->pro, &m->bcf}) TRY(upload_phase(m, *P));
+  for (Plan& pl : m->plan)
+    for (Phase* P : pl.phases()) TRY(upload_phase(m, *P));
+  m->sbuf_n = std::max(m->plan[0].sbuf_n, m->plan[1].sbuf_n);
+  m->rbuf_n = std::max(m->plan[0].rbuf_n, m->plan[1].rbuf_n);
   for (int d = 0; d < 3; ++d) TRY(upload(m, &m->d_reflux[d], m->reflux[d]));
   if (m->sbuf_n) TRY(dalloc(m, (void**)&m->sbuf, m->sbuf_n * sizeof(double)));
   if (m->rbuf_n) TRY(dalloc(m, (void**)&m->rbuf, m->rbuf_n * sizeof(double)));
@@ -499,7 +546,8 @@ static cudaEvent_t pool_event(ph_mesh* m) {
   return e;
 }
 
-static ph_status exchange(ph_mesh* m, double* U) {
+static ph_status exchange(ph_mesh* m, double* U, int which) {
+  Plan& PL = m->plan[which];
   const Geom& G = m->G;
   XArgs a{};
   a.U = U;
@@ -520,30 +568,30 @@ static ph_status exchange(ph_mesh* m, double* U) {
     m->launches++;
     return PH_OK;
   };
-  const bool remote = (m->nranks > 1) && (m->sbuf_n > 0 || m->rbuf_n > 0);
+  const bool remote = (m->nranks > 1) && (PL.sbuf_n > 0 || PL.rbuf_n > 0);
   if (remote) {
     // remote buffers first, then the local copies overlap the NCCL transfer
-    TRY(run(m->pack, m->stream));
+    TRY(run(PL.pack, m->stream));
     CU(cudaEventRecord(m->ev_pack, m->stream));
     CU(cudaStreamWaitEvent(m->comm_stream, m->ev_pack, 0));
     NC(ncclGroupStart());
     for (int p = 0; p < m->nranks; ++p) {
       if (p == m->rank) continue;
-      if (m->send_cnt[p]) NC(ncclSend(m->sbuf + m->send_off[p], m->send_cnt[p], ncclDouble, p, m->comm, m->comm_stream));
-      if (m->recv_cnt[p]) NC(ncclRecv(m->rbuf + m->recv_off[p], m->recv_cnt[p], ncclDouble, p, m->comm, m->comm_stream));
+      if (PL.send_cnt[p]) NC(ncclSend(m->sbuf + PL.send_off[p], PL.send_cnt[p], ncclDouble, p, m->comm, m->comm_stream));
+      if (PL.recv_cnt[p]) NC(ncclRecv(m->rbuf + PL.recv_off[p], PL.recv_cnt[p], ncclDouble, p, m->comm, m->comm_stream));
     }
     NC(ncclGroupEnd());
     CU(cudaEventRecord(m->ev_comm, m->comm_stream));
   }
-  TRY(run(m->local, m->stream));
+  TRY(run(PL.local, m->stream));
   if (remote) {
     CU(cudaStreamWaitEvent(m->stream, m->ev_comm, 0));
-    TRY(run(m->unpack, m->stream));
+    TRY(run(PL.unpack, m->stream));
   }
-  TRY(run(m->b1, m->stream));
-  TRY(run(m->b2, m->stream));
-  TRY(run(m->pro, m->stream));
-  TRY(run(m->bcf, m->stream));
+  TRY(run(PL.b1, m->stream));
+  TRY(run(PL.b2, m->stream));
+  TRY(run(PL.pro, m->stream));
+  TRY(run(PL.bcf, m->stream));
   if (m->timing) {
     CU(cudaEventRecord(t1, m->stream));
     m->t_exch.push_back({t0, t1});
@@ -627,14 +675,14 @@ static ph_status one_cycle(ph_mesh* m) {
   const int nloc = (int)m->local_gids.size();
   if (m->cfg.integrator == PH_INT_VL2) {
     TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, 0.5, false, 1));
-    TRY(exchange(m, m->U1));
+    TRY(exchange(m, m->U1, 1));
     TRY(run_stage(m, m->U1, m->U0, 1.0, 0.0, 1.0, fuse_reduce, 2));
   } else {
     TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, 1.0, false, 1));
-    TRY(exchange(m, m->U1));
+    TRY(exchange(m, m->U1, 1));
     TRY(run_stage(m, m->U1, m->U0, 0.5, 0.5, 0.5, fuse_reduce, 2));
   }
-  TRY(exchange(m, m->U0));
+  TRY(exchange(m, m->U0, 1));
   if (fuse_reduce) TRY(reduce_finalize(m, nloc > 0 ? m->stage_ctas : 0, 1));
   else TRY(standalone_reduce(m, m->U0, 1));
   return PH_OK;
@@ -693,6 +741,7 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
   m->rank = cfg->rank;
   m->nranks = cfg->nranks;
   m->host_only = cfg->host_only != 0;
+  m->no_direct_halo = cfg->no_direct_halo != 0;
   Geom& G = m->G;
   G.g = cfg->nghost;
   G.cg = (G.g + 1) / 2 + 1;
@@ -793,13 +842,13 @@ static ph_status need_device(const ph_mesh* m) {
 
 ph_status ph_exchange(ph_mesh* m) {
   TRY(need_device(m));
-  TRY(exchange(m, m->U0));
+  TRY(exchange(m, m->U0, 0));
   return check_err(m);
 }
 
 ph_status ph_refresh(ph_mesh* m) {
   TRY(need_device(m));
-  TRY(exchange(m, m->U0));
+  TRY(exchange(m, m->U0, 0));
   TRY(standalone_reduce(m, m->U0, 0));
   m->have_state = true;
   return check_err(m);
@@ -831,7 +880,7 @@ ph_status ph_set_problem(ph_mesh* m, int32_t problem, const double* p, int32_t n
   CU(launch_pgen(m->U0, m->d_meta, (int)m->local_gids.size(), P, m->G, m->stream));
   m->launches++;
   CU(cudaMemsetAsync(m->d_st, 0, sizeof(CycleState), m->stream));
-  TRY(exchange(m, m->U0));
+  TRY(exchange(m, m->U0, 0));
   TRY(standalone_reduce(m, m->U0, 0));
   m->have_state = true;
   return check_err(m);
@@ -884,6 +933,10 @@ ph_status ph_get_state_full(const ph_mesh* mc, int64_t gid, double* out, int64_t
   if (nelem != m->G.bstride) return fail(PH_ERR_INVALID_ARG, "bad nelem");
   TRY(check_err(m));
   if (s < 0) return PH_OK;
+  if (m->ghosts_stale && m->nranks == 1) {  // direct-halo cycles leave local face ghosts stale
+    TRY(exchange(m, m->U0, 0));
+    m->ghosts_stale = false;
+  }
   CU(cudaMemcpyAsync(out, m->U0 + s * m->G.bstride, nelem * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
   return PH_OK;
@@ -910,6 +963,7 @@ ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) 
   CU(launch_cycle_begin(m->d_st, tlim, 1, m->stream));
   m->launches++;
   for (int c = 0; c < ncycles; ++c) TRY(one_cycle(m));
+  if (ncycles > 0 && m->direct_halo) m->ghosts_stale = true;
   if (info) {
     TRY(check_err(m));
     CycleState st;
@@ -936,7 +990,7 @@ ph_status ph_step_host(ph_mesh* m, const double* host_in, double* host_out, int6
     m->launches++;
   }
   m->have_state = true;
-  TRY(exchange(m, m->U0));
+  TRY(exchange(m, m->U0, 0));
   TRY(standalone_reduce(m, m->U0, 0));
   TRY(ph_step(m, ncycles, tlim, nullptr));
   if (nloc) {
@@ -1045,15 +1099,22 @@ ph_status ph_totals(ph_mesh* m, double out[5]) {
 ph_status ph_get_plan_info(const ph_mesh* m, ph_plan_info* out) {
   if (!m || !out) return fail(PH_ERR_INVALID_ARG, "null argument");
   memset(out, 0, sizeof *out);
-  out->n_local_tasks = (int64_t)m->local.tasks.size();
-  out->n_send_tasks = (int64_t)m->pack.tasks.size();
-  out->n_recv_tasks = (int64_t)m->unpack.tasks.size();
+  const Plan& PL = m->plan[0];
+  out->n_local_tasks = (int64_t)PL.local.tasks.size();
+  out->n_send_tasks = (int64_t)PL.pack.tasks.size();
+  out->n_recv_tasks = (int64_t)PL.unpack.tasks.size();
   for (int p = 0; p < m->nranks && p < 64; ++p) {
-    out->send_doubles_to[p] = m->send_cnt[p];
-    out->recv_doubles_from[p] = m->recv_cnt[p];
-    out->send_hash_to[p] = m->send_hash[p];
-    out->recv_hash_from[p] = m->recv_hash[p];
+    out->send_doubles_to[p] = PL.send_cnt[p];
+    out->recv_doubles_from[p] = PL.recv_cnt[p];
+    out->send_hash_to[p] = PL.send_hash[p];
+    out->recv_hash_from[p] = PL.recv_hash[p];
+    out->cyc_send_doubles_to[p] = m->plan[1].send_cnt[p];
+    out->cyc_recv_doubles_from[p] = m->plan[1].recv_cnt[p];
+    out->cyc_send_hash_to[p] = m->plan[1].send_hash[p];
+    out->cyc_recv_hash_from[p] = m->plan[1].recv_hash[p];
   }
+  out->direct_halo = m->direct_halo ? 1 : 0;
+  out->n_cyc_local_tasks = (int64_t)m->plan[1].local.tasks.size();
   return PH_OK;
 }
 

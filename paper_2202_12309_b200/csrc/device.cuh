@@ -35,6 +35,7 @@ struct BlockMeta {
   int level;
   int cslot;         // coarse staging slot, -1 if none
   int fslot[6];      // face-flux slot for faces -x,+x,-y,+y,-z,+z (coarse-fine faces), else -1
+  int nb[6];         // direct halo: slot of the local same-level face neighbour, else -1 (use ghosts)
 };
 
 // Ghost-exchange task (fill-in-one).  One task fills one destination box.

@@ -195,16 +195,32 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
     sl_ok[s] = ok;
   }
 
+  // ---- per-slot source pointers (without the plane offset).  Direct halo: a halo cell outside
+  // the block in x or y is read from the local same-level face neighbour's interior (M.nb).
+  const double* sbase[2];
+#pragma unroll
+  for (int s = 0; s < 2; ++s) {
+    int gi = x0 + sl_i[s], gj = y0 + sl_j[s], bs = slot;
+    if (gi < 0 && M.nb[0] >= 0) { bs = M.nb[0]; gi += G.n[0]; }
+    else if (gi >= G.n[0] && M.nb[1] >= 0) { bs = M.nb[1]; gi -= G.n[0]; }
+    if (gj < 0 && M.nb[2] >= 0) { bs = M.nb[2]; gj += G.n[1]; }
+    else if (gj >= G.n[1] && M.nb[3] >= 0) { bs = M.nb[3]; gj -= G.n[1]; }
+    sbase[s] = A.Uin + (int64_t)bs * G.bstride + (int64_t)(gj + g) * G.N[0] + (gi + g);
+  }
+  const int64_t colo = (int64_t)(y0 + ty + g) * G.N[0] + (x0 + tx + g);
+  const double* obase = Ub + colo;
+  const double* zlo = M.nb[4] >= 0 ? A.Uin + (int64_t)M.nb[4] * G.bstride + colo + (int64_t)G.n[2] * plane : obase;
+  const double* zhi = M.nb[5] >= 0 ? A.Uin + (int64_t)M.nb[5] * G.bstride + colo - (int64_t)G.n[2] * plane : obase;
+
   double pf[2][NVAR];
   auto issue_load = [&](int q) {
     const bool halo = (q < k0) || (q >= k1);
-    const double* base = Ub + (int64_t)(q + g) * plane;
+    const int64_t qo = (int64_t)(q + g) * plane;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      int i = halo ? tx : sl_i[s], j = halo ? ty : sl_j[s];
       bool ok = halo ? (s == 0 && own) : sl_ok[s];
       if (ok) {
-        const double* p = base + (int64_t)(y0 + j + g) * G.N[0] + (x0 + i + g);
+        const double* p = halo ? ((q < 0 ? zlo : (q >= G.n[2] ? zhi : obase)) + qo) : (sbase[s] + qo);
 #pragma unroll
         for (int v = 0; v < NVAR; ++v) pf[s][v] = __ldg(p + v * G.vstride);
       }
@@ -246,6 +262,17 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
     const bool xy = (c >= k0) && (c < k1);
     const bool zf = (fz >= k0) && (fz <= k1);
     const double* Wc = sW + (c & 3) * SLOT;
+    // prefetch the finish-phase operands of my cell so their latency hides behind the faces
+    double uin[NVAR], u0v[NVAR];
+    const int64_t cell = (int64_t)slot * G.bstride + (int64_t)(c + g) * plane +
+                         (int64_t)(y0 + ty + g) * G.N[0] + (x0 + tx + g);
+    if (xy && own) {
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) {
+        uin[v] = __ldg(A.Uin + cell + v * G.vstride);
+        if (USE_U0) u0v[v] = A.U0[cell + v * G.vstride];
+      }
+    }
     // x faces of plane c: 33 per row, item t -> (row t/33, face t%33); rounds 0,1 (warp 0 only)
     if (xy) {
 #pragma unroll 1
@@ -315,8 +342,6 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
     __syncthreads();
     // ---- finish the cells of plane c: L = -(((dF1 + dF2) + dF3)) and the RK combine ----
     if (xy && own) {
-      const int64_t cell = (int64_t)slot * G.bstride + (int64_t)(c + g) * plane +
-                           (int64_t)(y0 + ty + g) * G.N[0] + (x0 + tx + g);
       const double* fzl = sFz + (c & 1) * NVAR * FZS + tid;        // face c   (lower)
       const double* fzu = sFz + ((c + 1) & 1) * NVAR * FZS + tid;  // face c+1 (upper)
       double un[NVAR];
@@ -326,9 +351,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
         double d2 = (sFy[v * FYS + (ty + 1) * TX + tx] - sFy[v * FYS + ty * TX + tx]) * idx2;
         double d3 = (fzu[v * FZS] - fzl[v * FZS]) * idx3;
         double L = -((d1 + d2) + d3);
-        double uin = A.Uin[cell + v * G.vstride];
-        double out = fma(A.b1, uin, (A.cdt * dt) * L);
-        if (USE_U0) out = fma(A.a0, A.U0[cell + v * G.vstride], out);
+        double out = fma(A.b1, uin[v], (A.cdt * dt) * L);
+        if (USE_U0) out = fma(A.a0, u0v[v], out);
         un[v] = out;
         A.Uout[cell + v * G.vstride] = out;
       }

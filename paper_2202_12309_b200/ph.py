@@ -38,6 +38,7 @@ class _Cfg(C.Structure):
         ("nregions", C.c_int32), ("regions", C.POINTER(C.c_double)),
         ("pack_size", C.c_int32),
         ("rank", C.c_int32), ("nranks", C.c_int32), ("device", C.c_int32), ("host_only", C.c_int32),
+        ("no_direct_halo", C.c_int32),
         ("stream", C.c_void_p), ("nccl_id", C.c_void_p),
         ("dev_alloc", _ALLOC), ("dev_free", _FREE), ("alloc_ctx", C.c_void_p),
     ]
@@ -60,7 +61,10 @@ class PhStepInfo(C.Structure):
 class PhPlanInfo(C.Structure):
     _fields_ = [("n_local_tasks", C.c_int64), ("n_send_tasks", C.c_int64), ("n_recv_tasks", C.c_int64),
                 ("send_doubles_to", C.c_int64 * 64), ("recv_doubles_from", C.c_int64 * 64),
-                ("send_hash_to", C.c_uint64 * 64), ("recv_hash_from", C.c_uint64 * 64)]
+                ("send_hash_to", C.c_uint64 * 64), ("recv_hash_from", C.c_uint64 * 64),
+                ("cyc_send_doubles_to", C.c_int64 * 64), ("cyc_recv_doubles_from", C.c_int64 * 64),
+                ("cyc_send_hash_to", C.c_uint64 * 64), ("cyc_recv_hash_from", C.c_uint64 * 64),
+                ("direct_halo", C.c_int32), ("n_cyc_local_tasks", C.c_int64)]
 
 
 EXPORTS = ["ph_nccl_unique_id", "ph_mesh_create", "ph_mesh_destroy", "ph_set_problem", "ph_set_state",
@@ -128,6 +132,7 @@ DEFAULTS = dict(
     bc_inner=(PERIODIC,) * 3, bc_outer=(PERIODIC,) * 3,
     gamma=5.0 / 3.0, cfl=0.3, recon=MINMOD, integrator=RK2,
     refine_tol=0.1, derefine_tol=0.025, derefine_interval=8, regions=(), pack_size=0,
+    direct_halo=True,
 )
 
 
@@ -167,6 +172,7 @@ class Mesh:
         cfg.pack_size = c["pack_size"]
         cfg.rank, cfg.nranks, cfg.device = rank, nranks, device
         cfg.host_only = 1 if host_only else 0
+        cfg.no_direct_halo = 0 if c["direct_halo"] else 1
         self._keep = []
         if not host_only:
             import torch
@@ -330,7 +336,11 @@ class Mesh:
         R = self.nranks
         return dict(n_local_tasks=p.n_local_tasks, n_send_tasks=p.n_send_tasks, n_recv_tasks=p.n_recv_tasks,
                     send_doubles_to=list(p.send_doubles_to[:R]), recv_doubles_from=list(p.recv_doubles_from[:R]),
-                    send_hash_to=list(p.send_hash_to[:R]), recv_hash_from=list(p.recv_hash_from[:R]))
+                    send_hash_to=list(p.send_hash_to[:R]), recv_hash_from=list(p.recv_hash_from[:R]),
+                    cyc_send_doubles_to=list(p.cyc_send_doubles_to[:R]),
+                    cyc_recv_doubles_from=list(p.cyc_recv_doubles_from[:R]),
+                    cyc_send_hash_to=list(p.cyc_send_hash_to[:R]), cyc_recv_hash_from=list(p.cyc_recv_hash_from[:R]),
+                    direct_halo=bool(p.direct_halo), n_cyc_local_tasks=p.n_cyc_local_tasks)
 
     def launch_count(self):
         n = C.c_int64()

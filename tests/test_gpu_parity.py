@@ -186,3 +186,20 @@ def test_config2a_full_size_parity(oracle_mod, P):
     kw = dict(mesh_nx=(256,) * 3, block_nx=(64,) * 3, xmin=(-.5,) * 3, xmax=(.5,) * 3)
     o, g = _run_both(oracle_mod, P, P.BLAST, [10.0, 0.1, 0.1], 10, **kw)
     _check_run(o, g)
+
+
+@pytest.mark.parametrize("bc", [0, 1])
+def test_direct_halo_equals_materialised_ghosts(P, bc):
+    """The direct-halo path (stage kernel reads local neighbour interiors) is bitwise identical to
+    the paper's scheme of exchanging every ghost each stage."""
+    kw = dict(mesh_nx=(64, 32, 48), block_nx=(16, 16, 16), xmin=(-.5,) * 3, xmax=(.5,) * 3,
+              bc_inner=(bc,) * 3, bc_outer=(bc,) * 3)
+    outs = []
+    for dh in (True, False):
+        g = P.Mesh(direct_halo=dh, **kw)
+        assert g.plan_info()["direct_halo"] == dh
+        g.set_problem(P.BLAST, [10.0, 0.1, 0.2, 0.05, -0.1, 0.0])
+        g.step(6)
+        outs.append((gather(g), g.history()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1][:, :2], outs[1][1][:, :2])

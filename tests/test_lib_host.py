@@ -120,3 +120,23 @@ def test_weak_8rank_plan_has_7_peers(P):
         info = P.Mesh(host_only=True, rank=r, nranks=8, mesh_nx=(512,) * 3, block_nx=(64,) * 3).plan_info()
         peers = [p for p in range(8) if info["send_doubles_to"][p] > 0]
         assert len(peers) == 7
+
+
+def test_direct_halo_cycle_plan(P):
+    # uniform periodic single rank: the per-cycle exchange is empty (all faces read directly)
+    info = P.Mesh(host_only=True, mesh_nx=(64, 64, 64), block_nx=(16, 16, 16)).plan_info()
+    assert info["direct_halo"] and info["n_cyc_local_tasks"] == 0
+    # outflow: only physical-boundary tasks remain; multilevel: direct halo is off
+    info = P.Mesh(host_only=True, mesh_nx=(64, 64, 64), block_nx=(16, 16, 16), max_level=1, refinement=1,
+                  regions=[(1, 0.1, 0.3, 0.1, 0.3, 0.1, 0.3)]).plan_info()
+    assert not info["direct_halo"]
+    # multi-rank uniform: the cycle plan keeps only remote faces, symmetric across ranks
+    R = 4
+    kw = dict(mesh_nx=(128, 64, 64), block_nx=(16, 16, 16))
+    infos = [P.Mesh(host_only=True, rank=r, nranks=R, **kw).plan_info() for r in range(R)]
+    for s in range(R):
+        for d in range(R):
+            assert infos[s]["cyc_send_doubles_to"][d] == infos[d]["cyc_recv_doubles_from"][s]
+            assert infos[s]["cyc_send_hash_to"][d] == infos[d]["cyc_recv_hash_from"][s]
+            assert infos[s]["cyc_send_doubles_to"][d] <= infos[s]["send_doubles_to"][d]
+    assert all(i["n_cyc_local_tasks"] == 0 for i in infos)
