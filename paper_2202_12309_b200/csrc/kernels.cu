@@ -780,7 +780,9 @@ cudaError_t launch_stage(int recon, bool reduce, bool use_u0, int nblk_cta, cons
   if (recon == R && reduce == RD && use_u0 == U0) {                                                 \
     static bool attr = false;                                                                       \
     if (!attr) {                                                                                    \
-      cudaFuncSetAttribute(stage_kernel<R, RD, U0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm); \
+      cudaError_t e_ = cudaFuncSetAttribute(stage_kernel<R, RD, U0>,                                \
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
+      if (e_ != cudaSuccess) return e_;                                                             \
       attr = true;                                                                                  \
     }                                                                                               \
     stage_kernel<R, RD, U0><<<grid, block, sm, s>>>(a, G);                                          \
