@@ -140,7 +140,7 @@ constexpr int FXS = TY * (TX + 1);      // var stride of sFx
 constexpr int FYS = (TY + 1) * TX;      // var stride of sFy
 constexpr int FZS = NT;                 // var stride of sFz
 
-template <int RECON, bool REDUCE, bool USE_U0>
+template <int RECON, bool REDUCE, bool USE_U0, bool ML>
 __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   extern __shared__ double smem[];
   double* sW = smem;                       // [4][5][SWY][SWX]
@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   };
 
   double tmax = 0.0, tsum[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  double topz[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};  // z top state of plane q-2 (my column)
   const int qbeg = k0 - 2, qend = k1 + 2;
   issue_load(qbeg);
   for (int q = qbeg; q < qend; ++q) {
@@ -284,7 +285,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
           face_flux<RECON, 1, 2, 3>(p, p + 1, p + 2, p + 3, G, F);
           double* d = sFx + j * (TX + 1) + fi;
           d[0] = F[0]; d[FXS] = F[1]; d[2 * FXS] = F[2]; d[3 * FXS] = F[3]; d[4 * FXS] = F[4];
-          if (A.fbuf) {
+          if (ML) {
             const int gi = x0 + fi;
             const int fs = (gi == 0) ? M.fslot[0] : ((gi == G.n[0]) ? M.fslot[1] : -1);
             if (fs >= 0) {
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
           face_flux<RECON, 2, 3, 1>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
           double* d = sFy + jf * TX + i;
           d[0] = F[0]; d[FYS] = F[1]; d[2 * FYS] = F[2]; d[3 * FYS] = F[3]; d[4 * FYS] = F[4];
-          if (A.fbuf) {
+          if (ML) {
             const int gj = y0 + jf;
             const int fs = (gj == 0) ? M.fslot[2] : ((gj == G.n[1]) ? M.fslot[3] : -1);
             if (fs >= 0) {
@@ -321,23 +322,41 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
         }
       }
     }
-    // z face between planes q-2 and q-1 of my column
-    if (zf && own) {
+    // z direction of my column: the slope of plane q-1 gives its bottom state (right state of the
+    // face between q-2 and q-1) and its top state, carried in registers to the next face.
+    if (own && q >= qbeg + 2) {
       const int o = (ty + 2) * SWX + (tx + 2);
-      double F[NVAR];
-      face_flux<RECON, 3, 1, 2>(sW + ((q - 3) & 3) * SLOT + o, sW + ((q - 2) & 3) * SLOT + o,
-                                sW + ((q - 1) & 3) * SLOT + o, sW + (q & 3) * SLOT + o, G, F);
-      double* d = sFz + (fz & 1) * NVAR * FZS + tid;
-      d[0] = F[0]; d[FZS] = F[1]; d[2 * FZS] = F[2]; d[3 * FZS] = F[3]; d[4 * FZS] = F[4];
-      if (A.fbuf) {
-        const int fs = (fz == 0) ? M.fslot[4] : ((fz == G.n[2]) ? M.fslot[5] : -1);
-        if (fs >= 0) {
-          const int64_t fstr = (int64_t)G.n[0] * G.n[1];
-          double* ob = A.fbuf + (int64_t)fs * G.fstride + (int64_t)(y0 + ty) * G.n[0] + (x0 + tx);
+      const double* pm = sW + ((q - 2) & 3) * SLOT + o;
+      const double* p0 = sW + ((q - 1) & 3) * SLOT + o;
+      const double* pp = sW + (q & 3) * SLOT + o;
+      double bot[NVAR], top[NVAR];
 #pragma unroll
-          for (int v = 0; v < NVAR; ++v) ob[v * fstr] = F[v];
+      for (int v = 0; v < NVAR; ++v) {
+        const double a = p0[v * VS];
+        const double s = slope<RECON>(a - pm[v * VS], pp[v * VS] - a);
+        bot[v] = fma(-0.5, s, a);
+        top[v] = fma(0.5, s, a);
+      }
+      if (zf) {
+        const double wl[NVAR] = {topz[0], topz[3], topz[1], topz[2], topz[4]};  // normal = x3
+        const double wr[NVAR] = {bot[0], bot[3], bot[1], bot[2], bot[4]};
+        double Fn[NVAR];
+        hlle(wl, wr, G, Fn);
+        const double F[NVAR] = {Fn[0], Fn[2], Fn[3], Fn[1], Fn[4]};
+        double* d = sFz + (fz & 1) * NVAR * FZS + tid;
+        d[0] = F[0]; d[FZS] = F[1]; d[2 * FZS] = F[2]; d[3 * FZS] = F[3]; d[4 * FZS] = F[4];
+        if (ML) {
+          const int fs = (fz == 0) ? M.fslot[4] : ((fz == G.n[2]) ? M.fslot[5] : -1);
+          if (fs >= 0) {
+            const int64_t fstr = (int64_t)G.n[0] * G.n[1];
+            double* ob = A.fbuf + (int64_t)fs * G.fstride + (int64_t)(y0 + ty) * G.n[0] + (x0 + tx);
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) ob[v * fstr] = F[v];
+          }
         }
       }
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) topz[v] = top[v];
     }
     __syncthreads();
     // ---- finish the cells of plane c: L = -(((dF1 + dF2) + dF3)) and the RK combine ----
@@ -772,35 +791,37 @@ __global__ void interior_copy_kernel(double* U, double* buf, int slot0, int to_p
 // ------------------------------------------------------------------------------ launchers
 #define PH_CHECK_LAUNCH() cudaGetLastError()
 
+template <int R, bool RD, bool U0, bool ML>
+static cudaError_t launch_stage_t(int nblk_cta, const StageArgs& a, const Geom& G, cudaStream_t s) {
+  const size_t sm = stage_smem_bytes();
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  stage_kernel<R, RD, U0, ML><<<nblk_cta, NT, sm, s>>>(a, G);
+  return cudaGetLastError();
+}
+
+template <int R, bool RD, bool U0>
+static cudaError_t launch_stage_ml(bool ml, int n, const StageArgs& a, const Geom& G, cudaStream_t s) {
+  return ml ? launch_stage_t<R, RD, U0, true>(n, a, G, s) : launch_stage_t<R, RD, U0, false>(n, a, G, s);
+}
+
+template <int R>
+static cudaError_t launch_stage_r(bool reduce, bool use_u0, bool ml, int n, const StageArgs& a, const Geom& G,
+                                  cudaStream_t s) {
+  if (reduce) return use_u0 ? launch_stage_ml<R, true, true>(ml, n, a, G, s) : launch_stage_ml<R, true, false>(ml, n, a, G, s);
+  return use_u0 ? launch_stage_ml<R, false, true>(ml, n, a, G, s) : launch_stage_ml<R, false, false>(ml, n, a, G, s);
+}
+
 cudaError_t launch_stage(int recon, bool reduce, bool use_u0, int nblk_cta, const StageArgs& a, const Geom& G,
                          cudaStream_t s) {
-  size_t sm = stage_smem_bytes();
-  dim3 grid(nblk_cta), block(NT);
-#define PH_STAGE_CASE(R, RD, U0)                                                                    \
-  if (recon == R && reduce == RD && use_u0 == U0) {                                                 \
-    static bool attr = false;                                                                       \
-    if (!attr) {                                                                                    \
-      cudaError_t e_ = cudaFuncSetAttribute(stage_kernel<R, RD, U0>,                                \
-                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);  \
-      if (e_ != cudaSuccess) return e_;                                                             \
-      attr = true;                                                                                  \
-    }                                                                                               \
-    stage_kernel<R, RD, U0><<<grid, block, sm, s>>>(a, G);                                          \
-    return PH_CHECK_LAUNCH();                                                                       \
-  }
-  PH_STAGE_CASE(0, false, false)
-  PH_STAGE_CASE(0, false, true)
-  PH_STAGE_CASE(0, true, false)
-  PH_STAGE_CASE(0, true, true)
-  PH_STAGE_CASE(1, false, false)
-  PH_STAGE_CASE(1, false, true)
-  PH_STAGE_CASE(1, true, false)
-  PH_STAGE_CASE(1, true, true)
-  PH_STAGE_CASE(2, false, false)
-  PH_STAGE_CASE(2, false, true)
-  PH_STAGE_CASE(2, true, false)
-  PH_STAGE_CASE(2, true, true)
-#undef PH_STAGE_CASE
+  const bool ml = a.fbuf != nullptr;
+  if (recon == 0) return launch_stage_r<0>(reduce, use_u0, ml, nblk_cta, a, G, s);
+  if (recon == 1) return launch_stage_r<1>(reduce, use_u0, ml, nblk_cta, a, G, s);
+  if (recon == 2) return launch_stage_r<2>(reduce, use_u0, ml, nblk_cta, a, G, s);
   return cudaErrorInvalidValue;
 }
 
