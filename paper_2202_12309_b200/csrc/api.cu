@@ -80,7 +80,9 @@ struct ph_mesh {
   cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
   ncclComm_t comm = nullptr;
   // device memory
-  std::vector<void*> allocs;
+  std::vector<void*> allocs;   // mesh-dependent (replaced on every remesh)
+  std::vector<void*> pallocs;  // persistent (cycle state, history, reductions)
+  unsigned long long* d_eps = nullptr;  // AMR indicator per local slot (double bits)
   double *U0 = nullptr, *U1 = nullptr, *C = nullptr, *fbuf = nullptr;
   double *partials = nullptr, *my6 = nullptr, *all6 = nullptr, *tot5 = nullptr, *hist = nullptr, *stage_buf = nullptr;
   BlockMeta* d_meta = nullptr;
@@ -114,7 +116,7 @@ struct ph_mesh {
 };
 
 /* ------------------------------------------------------------------------------- helpers */
-static ph_status dalloc(ph_mesh* m, void** p, size_t bytes) {
+static ph_status dalloc(ph_mesh* m, void** p, size_t bytes, bool persistent = false) {
   *p = nullptr;
   if (bytes == 0) return PH_OK;
   if (m->cfg.dev_alloc) {
@@ -124,7 +126,7 @@ static ph_status dalloc(ph_mesh* m, void** p, size_t bytes) {
     cudaError_t e = cudaMalloc(p, bytes);
     if (e != cudaSuccess) return fail(PH_ERR_OOM, std::string("cudaMalloc: ") + cudaGetErrorString(e));
   }
-  m->allocs.push_back(*p);
+  (persistent ? m->pallocs : m->allocs).push_back(*p);
   return PH_OK;
 }
 
@@ -137,14 +139,19 @@ static ph_status upload(ph_mesh* m, T** d, const std::vector<T>& h) {
   return PH_OK;
 }
 
-static void free_all(ph_mesh* m) {
-  if (m->host_only) return;
-  cudaStreamSynchronize(m->stream);
-  for (void* p : m->allocs) {
+static void free_list(ph_mesh* m, std::vector<void*>& l) {
+  for (void* p : l) {
     if (m->cfg.dev_free) m->cfg.dev_free(p, m->cfg.alloc_ctx);
     else cudaFree(p);
   }
-  m->allocs.clear();
+  l.clear();
+}
+
+static void free_all(ph_mesh* m) {
+  if (m->host_only) return;
+  cudaStreamSynchronize(m->stream);
+  free_list(m, m->allocs);
+  free_list(m, m->pallocs);
 }
 
 static uint64_t mix(uint64_t h, uint64_t x) {
@@ -410,7 +417,7 @@ static ph_status build_plan(ph_mesh* m) {
       if (fslot[b.gid][face] < 0) fslot[b.gid][face] = m->n_fslots++;
     }
   }
-  m->direct_halo = !m->multilevel && !m->no_direct_halo;
+  m->direct_halo = !m->multilevel && !m->no_direct_halo && m->cfg.refinement != PH_REF_ADAPTIVE;
   build_exchange(m, m->plan[0], false, cslot);
   build_exchange(m, m->plan[1], m->direct_halo, cslot);
   // reflux tasks (coarse side)
@@ -508,17 +515,18 @@ static ph_status setup_device(ph_mesh* m) {
   m->partials_n = std::max<int64_t>({(int64_t)m->stage_ctas, nloc * G.n[2], 1});
   TRY(dalloc(m, (void**)&m->partials, m->partials_n * 6 * sizeof(double)));
   CU(cudaMemsetAsync(m->partials, 0, m->partials_n * 6 * sizeof(double), m->stream));
+  TRY(dalloc(m, (void**)&m->d_eps, (size_t)std::max<int64_t>(nloc, 1) * sizeof(unsigned long long)));
   TRY(dalloc(m, (void**)&m->stage_buf, (size_t)std::max<int64_t>(nloc, 1) * NVAR * G.n[0] * G.n[1] * G.n[2] * sizeof(double)));
   return PH_OK;
 }
 
 static ph_status setup_persistent(ph_mesh* m) {
-  TRY(dalloc(m, (void**)&m->my6, 8 * sizeof(double)));
-  TRY(dalloc(m, (void**)&m->all6, (size_t)6 * m->nranks * sizeof(double)));
-  TRY(dalloc(m, (void**)&m->tot5, 8 * sizeof(double)));
-  TRY(dalloc(m, (void**)&m->hist, (size_t)m->hist_cap * 7 * sizeof(double)));
-  TRY(dalloc(m, (void**)&m->d_st, sizeof(CycleState)));
-  TRY(dalloc(m, (void**)&m->d_err, sizeof(ErrWord)));
+  TRY(dalloc(m, (void**)&m->my6, 8 * sizeof(double), true));
+  TRY(dalloc(m, (void**)&m->all6, (size_t)6 * m->nranks * sizeof(double), true));
+  TRY(dalloc(m, (void**)&m->tot5, 8 * sizeof(double), true));
+  TRY(dalloc(m, (void**)&m->hist, (size_t)m->hist_cap * 7 * sizeof(double), true));
+  TRY(dalloc(m, (void**)&m->d_st, sizeof(CycleState), true));
+  TRY(dalloc(m, (void**)&m->d_err, sizeof(ErrWord), true));
   CU(cudaMemsetAsync(m->d_st, 0, sizeof(CycleState), m->stream));
   CU(cudaMemsetAsync(m->d_err, 0, sizeof(ErrWord), m->stream));
   return PH_OK;
@@ -668,10 +676,13 @@ static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a
   return PH_OK;
 }
 
+static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, bool move, bool* changed);
+
 static ph_status one_cycle(ph_mesh* m) {
   CU(launch_cycle_begin(m->d_st, 0.0, 0, m->stream));
   m->launches++;
-  const bool fuse_reduce = !m->multilevel;
+  const bool adaptive = m->cfg.refinement == PH_REF_ADAPTIVE;
+  const bool fuse_reduce = !m->multilevel && !adaptive;
   const int nloc = (int)m->local_gids.size();
   if (m->cfg.integrator == PH_INT_VL2) {
     TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, 0.5, false, 1));
@@ -683,8 +694,109 @@ static ph_status one_cycle(ph_mesh* m) {
     TRY(run_stage(m, m->U1, m->U0, 0.5, 0.5, 0.5, fuse_reduce, 2));
   }
   TRY(exchange(m, m->U0, 1));
+  if (adaptive) {
+    // O5 step 6: tag after the cycle, remesh, exchange; dt and totals on the new mesh
+    CycleState st;
+    CU(cudaMemcpyAsync(&st, m->d_st, sizeof st, cudaMemcpyDeviceToHost, m->stream));
+    CU(cudaStreamSynchronize(m->stream));
+    if (st.active) {
+      const int iv = m->cfg.derefine_interval > 0 ? m->cfg.derefine_interval : 1;
+      const bool gate = ((st.cycle + 1) % iv) == 0;  // P:580, A16 (cycle after increment)
+      bool changed = false;
+      TRY(tag_and_remesh(m, false, gate, true, &changed));
+      if (changed) TRY(exchange(m, m->U0, 0));
+    }
+  }
   if (fuse_reduce) TRY(reduce_finalize(m, nloc > 0 ? m->stage_ctas : 0, 1));
   else TRY(standalone_reduce(m, m->U0, 1));
+  return PH_OK;
+}
+
+/* ------------------------------------------------------------------------------- AMR (O9) */
+/* Install a new leaf set: rebuild blocks / partition / plan / device pools (P:214, P:583-592:
+ * the tree is rebuilt first, then populated) and, when move, fill the new pool from the old one:
+ * same-level blocks are moved, refined parents prolongated into 8 children, derefined siblings
+ * restricted into their parent. */
+static ph_status remesh(ph_mesh* m, const std::unordered_set<LocKey>& leaves, bool move) {
+  if (m->nranks > 1) return fail(PH_ERR_UNSUPPORTED, "AMR block migration across ranks is not implemented yet");
+  std::unordered_map<LocKey, int> old_slot;
+  for (int64_t gid : m->local_gids) old_slot[pack(m->blocks[gid].loc)] = (int)m->blocks[gid].local;
+  double* oldU0 = m->U0;
+  std::vector<void*> old_allocs;
+  old_allocs.swap(m->allocs);
+  m->tree->set_leaves(leaves);
+  try {
+    build_blocks(*m->tree, m->nranks, m->rank, m->blocks, m->gid_of);
+  } catch (const std::exception& e) {
+    return fail(PH_ERR_STATE, e.what());
+  }
+  TRY(build_plan(m));
+  TRY(setup_device(m));
+  if (move) {
+    std::vector<RemeshTask> tasks;
+    for (int64_t gid : m->local_gids) {
+      const BlockInfo& b = m->blocks[gid];
+      RemeshTask t{};
+      t.dst = (int)b.local;
+      auto it = old_slot.find(pack(b.loc));
+      if (it != old_slot.end()) {
+        t.kind = R_MOVE;
+        t.src[0] = it->second;
+      } else if (b.loc.level > 0 && old_slot.count(pack(parent(b.loc)))) {
+        t.kind = R_REFINE;
+        t.src[0] = old_slot[pack(parent(b.loc))];
+        for (int d = 0; d < 3; ++d) t.ch[d] = (int)(b.loc.x[d] & 1);
+      } else {
+        t.kind = R_DEREFINE;
+        for (int c = 0; c < 8; ++c) {
+          auto ic = old_slot.find(pack(child(b.loc, c)));
+          if (ic == old_slot.end()) return fail(PH_ERR_STATE, "remesh: block has no source");
+          t.src[c] = ic->second;
+        }
+      }
+      tasks.push_back(t);
+    }
+    RemeshTask* d_tasks = nullptr;
+    TRY(upload(m, &d_tasks, tasks));
+    CU(launch_remesh(d_tasks, (int)tasks.size(), oldU0, m->U0, m->G, m->stream));
+    m->launches++;
+  }
+  CU(cudaStreamSynchronize(m->stream));
+  free_list(m, old_allocs);
+  return PH_OK;
+}
+
+/* Tag every local block (eps_B, A14) and normalise the flags (O9).  Returns true in *changed if
+ * the leaf set changed (and was installed). */
+static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, bool move, bool* changed) {
+  *changed = false;
+  const int nloc = (int)m->local_gids.size();
+  CU(launch_tag(m->U0, nloc, m->d_eps, m->G, m->stream));
+  m->launches++;
+  std::vector<unsigned long long> bits(nloc);
+  CU(cudaMemcpyAsync(bits.data(), m->d_eps, nloc * sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  std::vector<Loc> locs;
+  std::vector<int8_t> flags;
+  for (int s = 0; s < nloc; ++s) {
+    const BlockInfo& b = m->blocks[m->local_gids[s]];
+    double eps;
+    memcpy(&eps, &bits[s], sizeof eps);
+    int8_t f = 0;
+    if (eps > m->cfg.refine_tol && b.loc.level < m->cfg.max_level) f = 1;
+    else if (eps < m->cfg.derefine_tol && b.loc.level > 0) f = -1;
+    if (refine_only && f < 0) f = 0;
+    locs.push_back(b.loc);
+    flags.push_back(f);
+  }
+  if (!refine_only) m->last_flags = flags;
+  bool any = false;
+  for (int8_t f : flags) any = any || f != 0;
+  if (!any) return PH_OK;
+  std::unordered_set<LocKey> nl = normalize_flags(*m->tree, locs, flags, allow_deref && !refine_only);
+  if (nl == m->tree->leaves()) return PH_OK;
+  TRY(remesh(m, nl, move));
+  *changed = true;
   return PH_OK;
 }
 
@@ -876,7 +988,17 @@ ph_status ph_set_problem(ph_mesh* m, int32_t problem, const double* p, int32_t n
   } else {
     return fail(PH_ERR_INVALID_ARG, "unknown problem");
   }
-  if (m->cfg.refinement == PH_REF_ADAPTIVE) return fail(PH_ERR_UNSUPPORTED, "adaptive refinement not yet on the GPU path");
+  if (m->cfg.refinement == PH_REF_ADAPTIVE) {
+    // O9: AMR pre-refinement at t = 0 (generate, exchange, tag refine-only, refine + 2:1)
+    for (int it = 0; it < m->cfg.max_level; ++it) {
+      CU(launch_pgen(m->U0, m->d_meta, (int)m->local_gids.size(), P, m->G, m->stream));
+      m->launches++;
+      TRY(exchange(m, m->U0, 0));
+      bool changed = false;
+      TRY(tag_and_remesh(m, true, false, false, &changed));
+      if (!changed) break;
+    }
+  }
   CU(launch_pgen(m->U0, m->d_meta, (int)m->local_gids.size(), P, m->G, m->stream));
   m->launches++;
   CU(cudaMemsetAsync(m->d_st, 0, sizeof(CycleState), m->stream));
@@ -957,7 +1079,8 @@ ph_status ph_set_state_full(ph_mesh* m, int64_t gid, const double* in, int64_t n
 ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) {
   TRY(need_device(m));
   if (!m->have_state) return fail(PH_ERR_STATE, "no state: call ph_set_problem or ph_set_state + ph_refresh");
-  if (m->cfg.refinement == PH_REF_ADAPTIVE) return fail(PH_ERR_UNSUPPORTED, "adaptive refinement not yet on the GPU path");
+  if (m->cfg.refinement == PH_REF_ADAPTIVE && m->nranks > 1)
+    return fail(PH_ERR_UNSUPPORTED, "adaptive refinement across ranks is not implemented yet");
   if (m->cross_rank_reflux)
     return fail(PH_ERR_UNSUPPORTED, "flux correction across ranks is not implemented yet (multilevel + nranks > 1)");
   CU(launch_cycle_begin(m->d_st, tlim, 1, m->stream));

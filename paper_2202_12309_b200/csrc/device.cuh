@@ -126,6 +126,15 @@ struct PgenArgs {
   double xmin[3], L[3];
 };
 
+// Remesh data movement (O9): new block slot <- old pool.
+enum RemeshKind : int { R_MOVE = 0, R_REFINE = 1, R_DEREFINE = 2 };
+struct RemeshTask {
+  int kind;
+  int dst;       // new slot
+  int src[8];    // MOVE: src[0]; REFINE: src[0] = old parent slot; DEREFINE: old children, (k,j,i) order
+  int ch[3];     // REFINE: which child of the parent
+};
+
 constexpr int XCHUNK = 256;  // cells per exchange chunk (one CTA, one cell per thread)
 
 // launchers (kernels.cu)
@@ -144,6 +153,9 @@ cudaError_t launch_finalize(const double* all, int nranks, CycleState* st, doubl
 cudaError_t launch_cycle_begin(CycleState* st, double tlim, int set_tlim, cudaStream_t s);
 cudaError_t launch_interior_copy(double* U, double* buf, int slot0, int nslots, int to_pool, const Geom& G,
                                  cudaStream_t s);
+cudaError_t launch_tag(const double* U, int nslots, unsigned long long* eps_bits, const Geom& G, cudaStream_t s);
+cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, double* Unew, const Geom& G,
+                          cudaStream_t s);
 size_t stage_smem_bytes();
 
 }  // namespace ph

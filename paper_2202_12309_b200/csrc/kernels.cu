@@ -788,6 +788,77 @@ __global__ void interior_copy_kernel(double* U, double* buf, int slot0, int to_p
   }
 }
 
+// ------------------------------------------------------------------------------ AMR (O9)
+// Refinement indicator eps_B = max over interior cells of |grad p| / p with central differences
+// (A14).  Written with explicitly rounded ops in the oracle's order so that the flags match it.
+__device__ __forceinline__ double pressure_rn(const double* u, int64_t vs, double gm1) {
+  double rho = u[0];
+  double ir = __ddiv_rn(1.0, rho);
+  double m1 = u[vs], m2 = u[2 * vs], m3 = u[3 * vs];
+  double v1 = __dmul_rn(m1, ir), v2 = __dmul_rn(m2, ir), v3 = __dmul_rn(m3, ir);
+  double ke = __dmul_rn(0.5, __dadd_rn(__dadd_rn(__dmul_rn(m1, v1), __dmul_rn(m2, v2)), __dmul_rn(m3, v3)));
+  return __dmul_rn(gm1, __dsub_rn(u[4 * vs], ke));
+}
+
+__global__ void tag_kernel(const double* U, unsigned long long* eps_bits, Geom G) {
+  const int k = blockIdx.x % G.n[2];
+  const int slot = blockIdx.x / G.n[2];
+  const double* ub = U + (int64_t)slot * G.bstride;
+  const int64_t sj = G.N[0], sk = (int64_t)G.N[0] * G.N[1];
+  double mx = 0.0;
+  for (int c = threadIdx.x; c < G.n[0] * G.n[1]; c += blockDim.x) {
+    const int j = c / G.n[0], i = c % G.n[0];
+    const double* u = ub + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+    const int64_t vs = G.vstride;
+    double g1 = __dmul_rn(0.5, __dsub_rn(pressure_rn(u + 1, vs, G.gm1), pressure_rn(u - 1, vs, G.gm1)));
+    double g2 = __dmul_rn(0.5, __dsub_rn(pressure_rn(u + sj, vs, G.gm1), pressure_rn(u - sj, vs, G.gm1)));
+    double g3 = __dmul_rn(0.5, __dsub_rn(pressure_rn(u + sk, vs, G.gm1), pressure_rn(u - sk, vs, G.gm1)));
+    double s = __dadd_rn(__dadd_rn(__dmul_rn(g1, g1), __dmul_rn(g2, g2)), __dmul_rn(g3, g3));
+    double e = __ddiv_rn(__dsqrt_rn(s), pressure_rn(u, vs, G.gm1));
+    mx = fmax(mx, e);
+  }
+  for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if ((threadIdx.x & 31) == 0) atomicMax(eps_bits + slot, (unsigned long long)__double_as_longlong(mx));
+}
+
+// new pool <- old pool: same-level move, 8-child prolongation of a refined parent (using the
+// parent's valid ghosts for the slopes, A11), pairwise restriction of 8 derefined siblings (A10)
+__global__ void remesh_kernel(const RemeshTask* tasks, const double* Uold, double* Unew, Geom G) {
+  const RemeshTask t = tasks[blockIdx.y];
+  const int k = blockIdx.x;
+  const int64_t sj = G.N[0], sk = (int64_t)G.N[0] * G.N[1];
+  for (int c = threadIdx.x; c < G.n[0] * G.n[1]; c += blockDim.x) {
+    const int j = c / G.n[0], i = c % G.n[0];
+    const int64_t dq = ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+    double* d = Unew + (int64_t)t.dst * G.bstride + dq;
+    if (t.kind == R_MOVE) {
+      const double* s = Uold + (int64_t)t.src[0] * G.bstride + dq;
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) d[v * G.vstride] = s[v * G.vstride];
+    } else if (t.kind == R_REFINE) {
+      const int I = t.ch[0] * G.nc[0] + i / 2, J = t.ch[1] * G.nc[1] + j / 2, K = t.ch[2] * G.nc[2] + k / 2;
+      const double* p = Uold + (int64_t)t.src[0] * G.bstride + ((int64_t)(K + G.g) * G.N[1] + (J + G.g)) * G.N[0] + (I + G.g);
+      const double s1 = (i & 1) ? 0.25 : -0.25, s2 = (j & 1) ? 0.25 : -0.25, s3 = (k & 1) ? 0.25 : -0.25;
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) {
+        const double* q = p + v * G.vstride;
+        const double c0 = q[0];
+        const double a1 = minmod_i(c0 - q[-1], q[1] - c0);
+        const double a2 = minmod_i(c0 - q[-sj], q[sj] - c0);
+        const double a3 = minmod_i(c0 - q[-sk], q[sk] - c0);
+        d[v * G.vstride] = __dadd_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(s1, a1)), __dmul_rn(s2, a2)), __dmul_rn(s3, a3));
+      }
+    } else {
+      const int ci = i / G.nc[0], cj = j / G.nc[1], ck = k / G.nc[2];
+      const int fi = 2 * (i - ci * G.nc[0]), fj = 2 * (j - cj * G.nc[1]), fk = 2 * (k - ck * G.nc[2]);
+      const double* p = Uold + (int64_t)t.src[ck * 4 + cj * 2 + ci] * G.bstride +
+                        ((int64_t)(fk + G.g) * G.N[1] + (fj + G.g)) * G.N[0] + (fi + G.g);
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) d[v * G.vstride] = mean8(p + v * G.vstride, sj, sk);
+    }
+  }
+}
+
 // ------------------------------------------------------------------------------ launchers
 #define PH_CHECK_LAUNCH() cudaGetLastError()
 
@@ -878,6 +949,22 @@ cudaError_t launch_interior_copy(double* U, double* buf, int slot0, int nslots, 
   if (nslots <= 0) return cudaSuccess;
   interior_copy_kernel<<<nslots * NVAR * G.n[2] * G.n[1], 128, 0, s>>>(U, buf, slot0, to_pool, G);
   return PH_CHECK_LAUNCH();
+}
+
+cudaError_t launch_tag(const double* U, int nslots, unsigned long long* eps_bits, const Geom& G, cudaStream_t s) {
+  if (nslots <= 0) return cudaSuccess;
+  cudaError_t e = cudaMemsetAsync(eps_bits, 0, sizeof(unsigned long long) * nslots, s);
+  if (e != cudaSuccess) return e;
+  tag_kernel<<<nslots * G.n[2], 128, 0, s>>>(U, eps_bits, G);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, double* Unew, const Geom& G,
+                          cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  dim3 grid(G.n[2], ntasks);
+  remesh_kernel<<<grid, 128, 0, s>>>(t, Uold, Unew, G);
+  return cudaGetLastError();
 }
 
 }  // namespace ph

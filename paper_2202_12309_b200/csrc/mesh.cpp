@@ -237,4 +237,44 @@ void build_blocks(const Tree& t, int nranks, int rank, std::vector<BlockInfo>& o
     for (auto& e : b.nbrs) e.rank = out[e.gid].rank;
 }
 
+std::unordered_set<LocKey> normalize_flags(const Tree& t, const std::vector<Loc>& locs,
+                                           const std::vector<int8_t>& flags, bool allow_deref) {
+  Tree nt = t;
+  for (size_t i = 0; i < locs.size(); ++i)
+    if (flags[i] == 1 && nt.is_leaf(locs[i]) && locs[i].level < nt.cfg().max_level) nt.refine_leaf(locs[i]);
+  nt.balance();
+  if (!allow_deref) return nt.leaves();
+  std::unordered_map<LocKey, int> cnt;
+  for (size_t i = 0; i < locs.size(); ++i)
+    if (flags[i] == -1 && locs[i].level > 0 && nt.is_leaf(locs[i])) cnt[pack(parent(locs[i]))]++;
+  std::vector<Loc> accept;
+  for (auto& kv : cnt) {
+    if (kv.second != 8) continue;
+    const Loc P = unpack(kv.first);
+    bool ok = true;
+    // every leaf touching P must be at most one level finer than P: a refined same-level
+    // neighbour region may not have refined children on the side facing P
+    for (int o = 0; o < 27 && ok; ++o) {
+      if (o == 13) continue;
+      const int od[3] = {o % 3 - 1, (o / 3) % 3 - 1, o / 9 - 1};
+      Loc q{P.level, {P.x[0] + od[0], P.x[1] + od[1], P.x[2] + od[2]}};
+      if (!nt.wrap(q) || !nt.is_internal(q)) continue;
+      for (int ch = 0; ch < 8 && ok; ++ch) {
+        const int cd[3] = {ch & 1, (ch >> 1) & 1, (ch >> 2) & 1};
+        bool adj = true;
+        for (int d = 0; d < 3; ++d)
+          if ((od[d] == 1 && cd[d] != 0) || (od[d] == -1 && cd[d] != 1)) adj = false;
+        if (adj && nt.is_internal(child(q, ch))) ok = false;
+      }
+    }
+    if (ok) accept.push_back(P);
+  }
+  std::unordered_set<LocKey> leaves = nt.leaves();
+  for (const Loc& P : accept) {
+    for (int ch = 0; ch < 8; ++ch) leaves.erase(pack(child(P, ch)));
+    leaves.insert(pack(P));
+  }
+  return leaves;
+}
+
 }  // namespace ph

@@ -96,4 +96,11 @@ void build_blocks(const Tree& t, int nranks, int rank, std::vector<BlockInfo>& o
 
 void partition_range(int64_t nb, int R, int r, int64_t* lo, int64_t* hi);
 
+// AMR flag normalisation: refine flagged leaves, restore 2:1
+// (refine-only closure), then accept a derefinement of 8 siblings only if the gate is open, all
+// 8 are leaves flagged -1 and the parent keeps 2:1 against the post-refinement tree.
+// flags: +1 refine, -1 derefine, 0 keep, per entry of `locs`.  Returns the new leaf set.
+std::unordered_set<LocKey> normalize_flags(const Tree& t, const std::vector<Loc>& locs,
+                                           const std::vector<int8_t>& flags, bool allow_deref);
+
 }  // namespace ph
