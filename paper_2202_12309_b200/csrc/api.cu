@@ -101,6 +101,12 @@ struct ph_mesh {
   bool direct_halo = false;  // uniform mesh: stage kernels read local same-level face neighbours directly
   std::vector<RefluxTask> reflux[3];
   RefluxTask* d_reflux[3] = {nullptr, nullptr, nullptr};
+  // cross-rank flux correction: fine-side packs and per-peer layout
+  std::vector<FluxPackTask> fpack;
+  FluxPackTask* d_fpack = nullptr;
+  std::vector<int64_t> fsend_off, fsend_cnt, frecv_off, frecv_cnt;
+  int64_t fsbuf_n = 0, frbuf_n = 0;
+  double *fsbuf = nullptr, *frbuf = nullptr;
   // stage launch geometry
   int ntx = 1, nty = 1, nkc = 1, KC = 1;
   int stage_ctas = 0;
@@ -420,31 +426,75 @@ static ph_status build_plan(ph_mesh* m) {
   m->direct_halo = !m->multilevel && !m->no_direct_halo && m->cfg.refinement != PH_REF_ADAPTIVE;
   build_exchange(m, m->plan[0], false, cslot);
   build_exchange(m, m->plan[1], m->direct_halo, cslot);
-  // reflux tasks (coarse side)
+  // reflux tasks (coarse side) and, across ranks, the fine-side flux packs (O8).
+  // Per (sender, receiver) pair both ranks enumerate coarse blocks in gid order and their finer
+  // face entries in canonical order, so buffer offsets agree without any handshake.
   const int* n = m->G.n;
-  for (int64_t gid : m->local_gids) {
-    const BlockInfo& b = m->blocks[gid];
+  const int R = m->nranks;
+  m->fpack.clear();
+  std::vector<int64_t> fso(R, 0), fro(R, 0);
+  std::vector<int> fpack_peer;
+  std::vector<std::pair<int, size_t>> rflux_peer;  // (peer, index into reflux[d]) for rebasing
+  for (auto& b : m->blocks) {
     for (auto& e : b.nbrs) {
       int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
       if (nz != 1 || e.dlevel != 1) continue;
       int d = e.off[0] ? 0 : (e.off[1] ? 1 : 2);
       const BlockInfo& f = m->blocks[e.gid];
-      if (f.rank != me) {  // needs a per-stage flux message between ranks (not built yet)
-        m->cross_rank_reflux = true;
-        continue;
-      }
       int ta = (d == 0) ? 1 : 0, tb = (d == 2) ? 1 : 2;
-      RefluxTask rt{};
-      rt.cslot = (int)b.local;
-      rt.dir = d;
-      rt.side = e.off[d];
-      rt.cfs = fslot[gid][2 * d + (e.off[d] > 0 ? 1 : 0)];
-      rt.ffs = fslot[e.gid][2 * d + (e.off[d] > 0 ? 0 : 1)];
-      rt.t0lo = e.fine[0] * n[ta] / 2;
-      rt.t1lo = e.fine[1] * n[tb] / 2;
-      m->reflux[d].push_back(rt);
+      int64_t qsize = (int64_t)NVAR * (n[ta] / 2) * (n[tb] / 2);
+      int ffs_face = 2 * d + (e.off[d] > 0 ? 0 : 1);
+      if (b.rank == me) {
+        RefluxTask rt{};
+        rt.cslot = (int)b.local;
+        rt.dir = d;
+        rt.side = e.off[d];
+        rt.cfs = fslot[b.gid][2 * d + (e.off[d] > 0 ? 1 : 0)];
+        rt.t0lo = e.fine[0] * n[ta] / 2;
+        rt.t1lo = e.fine[1] * n[tb] / 2;
+        if (f.rank == me) {
+          rt.ffs = fslot[e.gid][ffs_face];
+          rt.roff = -1;
+        } else {
+          rt.ffs = -1;
+          rt.roff = fro[f.rank];
+          fro[f.rank] += qsize;
+          rflux_peer.push_back({f.rank, 0});
+          rflux_peer.back().second = ((size_t)d << 32) | m->reflux[d].size();
+        }
+        m->reflux[d].push_back(rt);
+      } else if (f.rank == me) {
+        FluxPackTask ft{};
+        ft.ffs = fslot[e.gid][ffs_face];
+        ft.dir = d;
+        ft.off = fso[b.rank];
+        fso[b.rank] += qsize;
+        fpack_peer.push_back(b.rank);
+        m->fpack.push_back(ft);
+      }
     }
   }
+  m->fsend_off.assign(R, 0);
+  m->fsend_cnt.assign(R, 0);
+  m->frecv_off.assign(R, 0);
+  m->frecv_cnt.assign(R, 0);
+  int64_t fs_acc = 0, fr_acc = 0;
+  for (int p = 0; p < R; ++p) {
+    m->fsend_off[p] = fs_acc;
+    m->fsend_cnt[p] = fso[p];
+    fs_acc += fso[p];
+    m->frecv_off[p] = fr_acc;
+    m->frecv_cnt[p] = fro[p];
+    fr_acc += fro[p];
+  }
+  for (size_t i = 0; i < m->fpack.size(); ++i) m->fpack[i].off += m->fsend_off[fpack_peer[i]];
+  for (auto& pr : rflux_peer) {
+    int d = (int)(pr.second >> 32);
+    size_t idx = pr.second & 0xffffffffu;
+    m->reflux[d][idx].roff += m->frecv_off[pr.first];
+  }
+  m->fsbuf_n = fs_acc;
+  m->frbuf_n = fr_acc;
   // block metadata
   m->meta.assign(nloc, BlockMeta{});
   for (int64_t s = 0; s < nloc; ++s) {
@@ -500,6 +550,9 @@ static ph_status setup_device(ph_mesh* m) {
   m->sbuf_n = std::max(m->plan[0].sbuf_n, m->plan[1].sbuf_n);
   m->rbuf_n = std::max(m->plan[0].rbuf_n, m->plan[1].rbuf_n);
   for (int d = 0; d < 3; ++d) TRY(upload(m, &m->d_reflux[d], m->reflux[d]));
+  TRY(upload(m, &m->d_fpack, m->fpack));
+  if (m->fsbuf_n) TRY(dalloc(m, (void**)&m->fsbuf, m->fsbuf_n * sizeof(double)));
+  if (m->frbuf_n) TRY(dalloc(m, (void**)&m->frbuf, m->frbuf_n * sizeof(double)));
   if (m->sbuf_n) TRY(dalloc(m, (void**)&m->sbuf, m->sbuf_n * sizeof(double)));
   if (m->rbuf_n) TRY(dalloc(m, (void**)&m->rbuf, m->rbuf_n * sizeof(double)));
   // stage launch geometry
@@ -666,10 +719,24 @@ static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a
     }
   }
   if (m->multilevel) {
+    if (m->nranks > 1 && (m->fsbuf_n > 0 || m->frbuf_n > 0)) {
+      // fine ranks restrict and send their coarse-fine face fluxes to the coarse blocks' ranks
+      if (!m->fpack.empty()) {
+        CU(launch_flux_pack((int)m->fpack.size(), m->d_fpack, m->fbuf, m->fsbuf, m->G, m->stream));
+        m->launches++;
+      }
+      NC(ncclGroupStart());
+      for (int p = 0; p < m->nranks; ++p) {
+        if (p == m->rank) continue;
+        if (m->fsend_cnt[p]) NC(ncclSend(m->fsbuf + m->fsend_off[p], m->fsend_cnt[p], ncclDouble, p, m->comm, m->stream));
+        if (m->frecv_cnt[p]) NC(ncclRecv(m->frbuf + m->frecv_off[p], m->frecv_cnt[p], ncclDouble, p, m->comm, m->stream));
+      }
+      NC(ncclGroupEnd());
+    }
     for (int d = 0; d < 3; ++d) {
       if (m->reflux[d].empty()) continue;
-      CU(launch_reflux((int)m->reflux[d].size(), m->d_reflux[d], Uout, m->d_meta, m->fbuf, m->d_st, cdt, m->G,
-                       m->stream));
+      CU(launch_reflux((int)m->reflux[d].size(), m->d_reflux[d], Uout, m->d_meta, m->fbuf, m->frbuf, m->d_st, cdt,
+                       m->G, m->stream));
       m->launches++;
     }
   }
@@ -1081,8 +1148,6 @@ ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) 
   if (!m->have_state) return fail(PH_ERR_STATE, "no state: call ph_set_problem or ph_set_state + ph_refresh");
   if (m->cfg.refinement == PH_REF_ADAPTIVE && m->nranks > 1)
     return fail(PH_ERR_UNSUPPORTED, "adaptive refinement across ranks is not implemented yet");
-  if (m->cross_rank_reflux)
-    return fail(PH_ERR_UNSUPPORTED, "flux correction across ranks is not implemented yet (multilevel + nranks > 1)");
   CU(launch_cycle_begin(m->d_st, tlim, 1, m->stream));
   m->launches++;
   for (int c = 0; c < ncycles; ++c) TRY(one_cycle(m));

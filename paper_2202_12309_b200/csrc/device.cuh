@@ -75,6 +75,16 @@ struct RefluxTask {
   int cfs;           // coarse face-flux slot
   int ffs;           // fine face-flux slot
   int t0lo, t1lo;    // coarse tangential start of this fine block's quarter
+  int64_t roff;      // >= 0: the fine block lives on another rank; its restricted fluxes are at
+                     // recv-buffer offset roff ([v][B0][A0] over the quarter)
+};
+
+// Fine side of a cross-rank flux correction: restrict (mean of 4) this fine block's face fluxes
+// and pack them for the coarse block's rank (flux correction is communicated).
+struct FluxPackTask {
+  int ffs;           // fine face-flux slot
+  int dir;
+  int64_t off;       // send-buffer offset
 };
 
 struct ErrWord {
@@ -142,7 +152,9 @@ cudaError_t launch_stage(int recon, bool reduce, bool use_u0, int nblk_cta, cons
                          cudaStream_t s);
 cudaError_t launch_xfill(int nchunks, const XArgs& a, const Geom& G, cudaStream_t s);
 cudaError_t launch_reflux(int ntasks, const RefluxTask* t, double* U, const BlockMeta* meta, const double* fbuf,
-                          const CycleState* st, double w, const Geom& G, cudaStream_t s);
+                          const double* rbuf, const CycleState* st, double w, const Geom& G, cudaStream_t s);
+cudaError_t launch_flux_pack(int ntasks, const FluxPackTask* t, const double* fbuf, double* sbuf, const Geom& G,
+                             cudaStream_t s);
 cudaError_t launch_pgen(double* U, const BlockMeta* meta, int nslots, const PgenArgs& P, const Geom& G,
                         cudaStream_t s);
 cudaError_t launch_reduce(const double* U, const BlockMeta* meta, int nslots, double* partials, ErrWord* err,

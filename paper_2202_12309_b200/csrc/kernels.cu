@@ -573,7 +573,7 @@ __global__ void __launch_bounds__(XT) xfill_kernel(XArgs A, Geom G) {
 // ------------------------------------------------------------------------------ reflux (O8 / a8)
 // U_c(adjacent cell) += w dt s (F_own - F_corr) / dx, F_corr = pairwise mean of 4 fine fluxes.
 __global__ void reflux_kernel(const RefluxTask* tasks, double* U, const BlockMeta* meta, const double* fbuf,
-                              const CycleState* st, double w, Geom G) {
+                              const double* rbuf, const CycleState* st, double w, Geom G) {
   const RefluxTask t = tasks[blockIdx.y];
   const int d = t.dir;
   const int ta = (d == 0) ? 1 : 0, tb = (d == 2) ? 1 : 2;  // tangential dims, increasing
@@ -596,12 +596,38 @@ __global__ void reflux_kernel(const RefluxTask* tasks, double* U, const BlockMet
   const int a0 = 2 * A0, b0 = 2 * B0;
 #pragma unroll
   for (int v = 0; v < NVAR; ++v) {
+    double corr;
+    if (t.roff >= 0) {
+      corr = rbuf[t.roff + (int64_t)v * qa * qb + (int64_t)B0 * qa + A0];
+    } else {
+      const double* f = ff + v * fst;
+      double f00 = f[(int64_t)b0 * na + a0], f10 = f[(int64_t)b0 * na + a0 + 1];
+      double f01 = f[(int64_t)(b0 + 1) * na + a0], f11 = f[(int64_t)(b0 + 1) * na + a0 + 1];
+      corr = ((f00 + f10) + (f01 + f11)) * 0.25;
+    }
+    double own = cf[v * fst + (int64_t)Bc * na + Ac];
+    u[v * G.vstride] += fac * (own - corr);
+  }
+}
+
+__global__ void flux_pack_kernel(const FluxPackTask* tasks, const double* fbuf, double* sbuf, Geom G) {
+  const FluxPackTask t = tasks[blockIdx.y];
+  const int d = t.dir;
+  const int ta = (d == 0) ? 1 : 0, tb = (d == 2) ? 1 : 2;
+  const int na = G.n[ta], nb = G.n[tb];
+  const int qa = na / 2, qb = nb / 2;
+  const int idxc = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idxc >= qa * qb) return;
+  const int A0 = idxc % qa, B0 = idxc / qa;
+  const int a0 = 2 * A0, b0 = 2 * B0;
+  const int64_t fst = (int64_t)na * nb;
+  const double* ff = fbuf + (int64_t)t.ffs * G.fstride;
+#pragma unroll
+  for (int v = 0; v < NVAR; ++v) {
     const double* f = ff + v * fst;
     double f00 = f[(int64_t)b0 * na + a0], f10 = f[(int64_t)b0 * na + a0 + 1];
     double f01 = f[(int64_t)(b0 + 1) * na + a0], f11 = f[(int64_t)(b0 + 1) * na + a0 + 1];
-    double corr = ((f00 + f10) + (f01 + f11)) * 0.25;
-    double own = cf[v * fst + (int64_t)Bc * na + Ac];
-    u[v * G.vstride] += fac * (own - corr);
+    sbuf[t.off + (int64_t)v * qa * qb + (int64_t)B0 * qa + A0] = ((f00 + f10) + (f01 + f11)) * 0.25;
   }
 }
 
@@ -902,15 +928,26 @@ cudaError_t launch_xfill(int nchunks, const XArgs& a, const Geom& G, cudaStream_
   return PH_CHECK_LAUNCH();
 }
 
-cudaError_t launch_reflux(int ntasks, const RefluxTask* t, double* U, const BlockMeta* meta, const double* fbuf,
-                          const CycleState* st, double w, const Geom& G, cudaStream_t s) {
-  if (ntasks <= 0) return cudaSuccess;
+static int max_quarter(const Geom& G) {
   int qa = G.n[1] / 2 * G.n[2] / 2;  // upper bound of face quarter cells over dirs
   int q2 = G.n[0] / 2 * G.n[2] / 2, q3 = G.n[0] / 2 * G.n[1] / 2;
   int q = qa > q2 ? qa : q2;
-  q = q > q3 ? q : q3;
-  dim3 grid((q + 127) / 128, ntasks);
-  reflux_kernel<<<grid, 128, 0, s>>>(t, U, meta, fbuf, st, w, G);
+  return q > q3 ? q : q3;
+}
+
+cudaError_t launch_reflux(int ntasks, const RefluxTask* t, double* U, const BlockMeta* meta, const double* fbuf,
+                          const double* rbuf, const CycleState* st, double w, const Geom& G, cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  dim3 grid((max_quarter(G) + 127) / 128, ntasks);
+  reflux_kernel<<<grid, 128, 0, s>>>(t, U, meta, fbuf, rbuf, st, w, G);
+  return PH_CHECK_LAUNCH();
+}
+
+cudaError_t launch_flux_pack(int ntasks, const FluxPackTask* t, const double* fbuf, double* sbuf, const Geom& G,
+                             cudaStream_t s) {
+  if (ntasks <= 0) return cudaSuccess;
+  dim3 grid((max_quarter(G) + 127) / 128, ntasks);
+  flux_pack_kernel<<<grid, 128, 0, s>>>(t, fbuf, sbuf, G);
   return PH_CHECK_LAUNCH();
 }
 

@@ -21,6 +21,13 @@ CASES = {
                       problem=1, params=[0.5], cycles=10),
     "wave64": dict(kw=dict(mesh_nx=(128, 64, 64), block_nx=(32, 32, 32)), problem=0,
                    params=[1e-6, 1, 1, 1], cycles=10),
+    # static multilevel: coarse-fine faces (flux correction) and level-jump ghosts cross ranks
+    "smr2": dict(kw=dict(mesh_nx=(32, 32, 32), block_nx=(8, 8, 8), xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=1,
+                         refinement=1, regions=[(1, -0.15, 0.15, -0.15, 0.15, -0.15, 0.15)]),
+                 problem=2, params=[10.0, 0.1, 0.12], cycles=10),
+    "smr3_walls": dict(kw=dict(mesh_nx=(32, 16, 16), block_nx=(8, 8, 8), max_level=2, refinement=1, gamma=1.4,
+                               regions=[(2, 0.45, 0.55, 0.2, 0.6, 0.3, 0.7)], bc_inner=(1, 1, 2), bc_outer=(1, 2, 1)),
+                       problem=1, params=[0.5], cycles=10),
 }
 
 
