@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <array>
@@ -82,7 +83,8 @@ struct ph_mesh {
   // device memory
   std::vector<void*> allocs;   // mesh-dependent (replaced on every remesh)
   std::vector<void*> pallocs;  // persistent (cycle state, history, reductions)
-  unsigned long long* d_eps = nullptr;  // AMR indicator per local slot (double bits)
+  unsigned long long* d_eps = nullptr;      // AMR indicator per local slot (double bits), padded
+  unsigned long long* d_eps_all = nullptr;  // all ranks' indicators (allgather)
   double *U0 = nullptr, *U1 = nullptr, *C = nullptr, *fbuf = nullptr;
   double *partials = nullptr, *my6 = nullptr, *all6 = nullptr, *tot5 = nullptr, *hist = nullptr, *stage_buf = nullptr;
   BlockMeta* d_meta = nullptr;
@@ -568,7 +570,14 @@ static ph_status setup_device(ph_mesh* m) {
   m->partials_n = std::max<int64_t>({(int64_t)m->stage_ctas, nloc * G.n[2], 1});
   TRY(dalloc(m, (void**)&m->partials, m->partials_n * 6 * sizeof(double)));
   CU(cudaMemsetAsync(m->partials, 0, m->partials_n * 6 * sizeof(double), m->stream));
-  TRY(dalloc(m, (void**)&m->d_eps, (size_t)std::max<int64_t>(nloc, 1) * sizeof(unsigned long long)));
+  {
+    const int64_t nglob = (int64_t)m->blocks.size();
+    const int64_t maxloc = std::max<int64_t>((nglob + m->nranks - 1) / m->nranks, 1);
+    TRY(dalloc(m, (void**)&m->d_eps, (size_t)maxloc * sizeof(unsigned long long)));
+    CU(cudaMemsetAsync(m->d_eps, 0, (size_t)maxloc * sizeof(unsigned long long), m->stream));
+    if (m->nranks > 1)
+      TRY(dalloc(m, (void**)&m->d_eps_all, (size_t)maxloc * m->nranks * sizeof(unsigned long long)));
+  }
   TRY(dalloc(m, (void**)&m->stage_buf, (size_t)std::max<int64_t>(nloc, 1) * NVAR * G.n[0] * G.n[1] * G.n[2] * sizeof(double)));
   return PH_OK;
 }
@@ -781,51 +790,177 @@ static ph_status one_cycle(ph_mesh* m) {
 
 /* ------------------------------------------------------------------------------- AMR (O9) */
 /* Install a new leaf set: rebuild blocks / partition / plan / device pools (P:214, P:583-592:
- * the tree is rebuilt first, then populated) and, when move, fill the new pool from the old one:
- * same-level blocks are moved, refined parents prolongated into 8 children, derefined siblings
- * restricted into their parent. */
+ * the tree is rebuilt first and the new distribution computed from it, then populated) and, when
+ * move, fill the new pool: same-level blocks are moved (sent if their owner changes), refined
+ * parents are sent whole and prolongated on the receiving rank, derefined siblings are restricted
+ * on their sending rank and sent as octants.  Per (sender, receiver) pair both ranks enumerate
+ * the new blocks in gid order, so buffer offsets agree without a handshake. */
 static ph_status remesh(ph_mesh* m, const std::unordered_set<LocKey>& leaves, bool move) {
-  if (m->nranks > 1) return fail(PH_ERR_UNSUPPORTED, "AMR block migration across ranks is not implemented yet");
-  std::unordered_map<LocKey, int> old_slot;
-  for (int64_t gid : m->local_gids) old_slot[pack(m->blocks[gid].loc)] = (int)m->blocks[gid].local;
+  const int R = m->nranks, me = m->rank;
+  struct Old { int rank; int slot; };
+  std::unordered_map<LocKey, Old> old;
+  for (auto& b : m->blocks) old[pack(b.loc)] = Old{b.rank, (int)b.local};
   double* oldU0 = m->U0;
   std::vector<void*> old_allocs;
   old_allocs.swap(m->allocs);
   m->tree->set_leaves(leaves);
   try {
     build_blocks(*m->tree, m->nranks, m->rank, m->blocks, m->gid_of);
-  } catch (const std::exception& e) {
-    return fail(PH_ERR_STATE, e.what());
+  } catch (const std::exception& ex) {
+    return fail(PH_ERR_STATE, ex.what());
   }
   TRY(build_plan(m));
   TRY(setup_device(m));
   if (move) {
-    std::vector<RemeshTask> tasks;
-    for (int64_t gid : m->local_gids) {
-      const BlockInfo& b = m->blocks[gid];
-      RemeshTask t{};
-      t.dst = (int)b.local;
-      auto it = old_slot.find(pack(b.loc));
-      if (it != old_slot.end()) {
+    const Geom& G = m->G;
+    const int64_t nint = (int64_t)NVAR * G.n[0] * G.n[1] * G.n[2];
+    const int64_t noct = (int64_t)NVAR * G.nc[0] * G.nc[1] * G.nc[2];
+    std::vector<RemeshTask> send_t, work_t;      // send: pack kernels; work: local + from recv buffer
+    std::vector<std::pair<int, int64_t>> send_full;  // (old slot, offset) whole-block sends
+    std::vector<int> send_peer, work_peer, full_peer;
+    std::vector<int64_t> so(R, 0), ro(R, 0);
+    std::map<std::pair<LocKey, int>, bool> parent_sent;
+    std::map<LocKey, int64_t> parent_recv;  // parent -> recv offset (relative, peer in parent_recv_peer)
+    std::map<LocKey, int> parent_recv_peer;
+    for (auto& b : m->blocks) {
+      const int Rn = b.rank;
+      const LocKey key = pack(b.loc);
+      auto it = old.find(key);
+      if (it != old.end()) {  // same-level move
+        const int Ro = it->second.rank;
+        RemeshTask t{};
         t.kind = R_MOVE;
-        t.src[0] = it->second;
-      } else if (b.loc.level > 0 && old_slot.count(pack(parent(b.loc)))) {
-        t.kind = R_REFINE;
-        t.src[0] = old_slot[pack(parent(b.loc))];
-        for (int d = 0; d < 3; ++d) t.ch[d] = (int)(b.loc.x[d] & 1);
-      } else {
-        t.kind = R_DEREFINE;
-        for (int c = 0; c < 8; ++c) {
-          auto ic = old_slot.find(pack(child(b.loc, c)));
-          if (ic == old_slot.end()) return fail(PH_ERR_STATE, "remesh: block has no source");
-          t.src[c] = ic->second;
+        if (Ro == me && Rn == me) {
+          t.src = it->second.slot;
+          t.dst = (int)b.local;
+          work_t.push_back(t);
+          work_peer.push_back(-1);
+        } else if (Ro == me) {
+          t.src = it->second.slot;
+          t.dst = -1;
+          t.dst_off = so[Rn];
+          so[Rn] += nint;
+          send_t.push_back(t);
+          send_peer.push_back(Rn);
+        } else if (Rn == me) {
+          t.src = -1;
+          t.src_off = ro[Ro];
+          ro[Ro] += nint;
+          t.dst = (int)b.local;
+          work_t.push_back(t);
+          work_peer.push_back(Ro);
+        }
+        continue;
+      }
+      const LocKey pk = b.loc.level > 0 ? pack(parent(b.loc)) : 0;
+      auto ip = b.loc.level > 0 ? old.find(pk) : old.end();
+      if (ip != old.end()) {  // refined: prolongate the parent on the child's new rank
+        const int Ro = ip->second.rank;
+        if (Ro == me && Rn != me && !parent_sent[{pk, Rn}]) {
+          parent_sent[{pk, Rn}] = true;
+          send_full.push_back({ip->second.slot, so[Rn]});
+          full_peer.push_back(Rn);
+          so[Rn] += G.bstride;
+        }
+        if (Rn == me) {
+          RemeshTask t{};
+          t.kind = R_REFINE;
+          t.dst = (int)b.local;
+          for (int d = 0; d < 3; ++d) t.ch[d] = (int)(b.loc.x[d] & 1);
+          if (Ro == me) {
+            t.src = ip->second.slot;
+            work_peer.push_back(-1);
+          } else {
+            if (!parent_recv.count(pk)) {
+              parent_recv[pk] = ro[Ro];
+              parent_recv_peer[pk] = Ro;
+              ro[Ro] += G.bstride;
+            }
+            t.src = -1;
+            t.src_off = parent_recv[pk];
+            work_peer.push_back(Ro);
+          }
+          work_t.push_back(t);
+        }
+        continue;
+      }
+      // derefined: 8 old children -> octants of this block
+      for (int c = 0; c < 8; ++c) {
+        auto ic = old.find(pack(child(b.loc, c)));
+        if (ic == old.end()) return fail(PH_ERR_STATE, "remesh: block has no source");
+        const int Ro = ic->second.rank;
+        RemeshTask t{};
+        t.ch[0] = c & 1;
+        t.ch[1] = (c >> 1) & 1;
+        t.ch[2] = (c >> 2) & 1;
+        if (Ro == me && Rn == me) {
+          t.kind = R_OCT;
+          t.src = ic->second.slot;
+          t.dst = (int)b.local;
+          work_t.push_back(t);
+          work_peer.push_back(-1);
+        } else if (Ro == me) {
+          t.kind = R_OCT;
+          t.src = ic->second.slot;
+          t.dst = -1;
+          t.dst_off = so[Rn];
+          so[Rn] += noct;
+          send_t.push_back(t);
+          send_peer.push_back(Rn);
+        } else if (Rn == me) {
+          t.kind = R_OCTCOPY;
+          t.src = -1;
+          t.src_off = ro[Ro];
+          ro[Ro] += noct;
+          t.dst = (int)b.local;
+          work_t.push_back(t);
+          work_peer.push_back(Ro);
         }
       }
-      tasks.push_back(t);
     }
-    RemeshTask* d_tasks = nullptr;
-    TRY(upload(m, &d_tasks, tasks));
-    CU(launch_remesh(d_tasks, (int)tasks.size(), oldU0, m->U0, m->G, m->stream));
+    // concatenate per-peer regions
+    std::vector<int64_t> soff(R, 0), roff(R, 0);
+    int64_t stot = 0, rtot = 0;
+    for (int q = 0; q < R; ++q) {
+      soff[q] = stot;
+      stot += so[q];
+      roff[q] = rtot;
+      rtot += ro[q];
+    }
+    for (size_t i = 0; i < send_t.size(); ++i) send_t[i].dst_off += soff[send_peer[i]];
+    for (size_t i = 0; i < send_full.size(); ++i) send_full[i].second += soff[full_peer[i]];
+    for (size_t i = 0; i < work_t.size(); ++i)
+      if (work_peer[i] >= 0) work_t[i].src_off += roff[work_peer[i]];
+    double *msb = nullptr, *mrb = nullptr;
+    std::vector<void*> keep;
+    keep.swap(m->allocs);  // migration buffers and task arrays go to a temporary list
+    if (stot) TRY(dalloc(m, (void**)&msb, stot * sizeof(double)));
+    if (rtot) TRY(dalloc(m, (void**)&mrb, rtot * sizeof(double)));
+    RemeshTask *d_send = nullptr, *d_work = nullptr;
+    TRY(upload(m, &d_send, send_t));
+    TRY(upload(m, &d_work, work_t));
+    std::vector<void*> tmp;
+    tmp.swap(m->allocs);
+    m->allocs.swap(keep);
+    for (void* q : tmp) old_allocs.push_back(q);
+    // 1. sender side: pack moved interiors / restricted octants, copy whole parents
+    CU(launch_remesh(d_send, (int)send_t.size(), oldU0, m->U0, mrb, msb, G, m->stream));
+    m->launches++;
+    for (auto& sf : send_full)
+      CU(cudaMemcpyAsync(msb + sf.second, oldU0 + (int64_t)sf.first * G.bstride, G.bstride * sizeof(double),
+                         cudaMemcpyDeviceToDevice, m->stream));
+    // 2. exchange the migration buffers
+    if (R > 1 && (stot || rtot)) {
+      NC(ncclGroupStart());
+      for (int q = 0; q < R; ++q) {
+        if (q == me) continue;
+        if (so[q]) NC(ncclSend(msb + soff[q], so[q], ncclDouble, q, m->comm, m->stream));
+        if (ro[q]) NC(ncclRecv(mrb + roff[q], ro[q], ncclDouble, q, m->comm, m->stream));
+      }
+      NC(ncclGroupEnd());
+    }
+    // 3. local moves / prolongations / restrictions and the received data
+    CU(launch_remesh(d_work, (int)work_t.size(), oldU0, m->U0, mrb, msb, G, m->stream));
     m->launches++;
   }
   CU(cudaStreamSynchronize(m->stream));
@@ -833,28 +968,41 @@ static ph_status remesh(ph_mesh* m, const std::unordered_set<LocKey>& leaves, bo
   return PH_OK;
 }
 
-/* Tag every local block (eps_B, A14) and normalise the flags (O9).  Returns true in *changed if
- * the leaf set changed (and was installed). */
+/* Tag every local block (eps_B, A14), gather the indicators of all ranks, normalise the flags
+ * (O9) identically on every rank and install the new mesh if it changed. */
 static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, bool move, bool* changed) {
   *changed = false;
   const int nloc = (int)m->local_gids.size();
+  const int R = m->nranks;
+  const int64_t nglob = (int64_t)m->blocks.size();
+  const int64_t maxloc = (nglob + R - 1) / R;
   CU(launch_tag(m->U0, nloc, m->d_eps, m->G, m->stream));
   m->launches++;
-  std::vector<unsigned long long> bits(nloc);
-  CU(cudaMemcpyAsync(bits.data(), m->d_eps, nloc * sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
+  std::vector<unsigned long long> bits((size_t)maxloc * R, 0ull);
+  if (R > 1) {
+    NC(ncclAllGather(m->d_eps, m->d_eps_all, maxloc, ncclUint64, m->comm, m->stream));
+    CU(cudaMemcpyAsync(bits.data(), m->d_eps_all, bits.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                       m->stream));
+  } else if (nloc) {
+    CU(cudaMemcpyAsync(bits.data(), m->d_eps, nloc * sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
+  }
   CU(cudaStreamSynchronize(m->stream));
   std::vector<Loc> locs;
   std::vector<int8_t> flags;
-  for (int s = 0; s < nloc; ++s) {
-    const BlockInfo& b = m->blocks[m->local_gids[s]];
-    double eps;
-    memcpy(&eps, &bits[s], sizeof eps);
-    int8_t f = 0;
-    if (eps > m->cfg.refine_tol && b.loc.level < m->cfg.max_level) f = 1;
-    else if (eps < m->cfg.derefine_tol && b.loc.level > 0) f = -1;
-    if (refine_only && f < 0) f = 0;
-    locs.push_back(b.loc);
-    flags.push_back(f);
+  for (int r = 0; r < R; ++r) {
+    int64_t lo, hi;
+    partition_range(nglob, R, r, &lo, &hi);
+    for (int64_t g = lo; g < hi; ++g) {
+      const BlockInfo& b = m->blocks[g];
+      double eps;
+      memcpy(&eps, &bits[(size_t)r * maxloc + (g - lo)], sizeof eps);
+      int8_t f = 0;
+      if (eps > m->cfg.refine_tol && b.loc.level < m->cfg.max_level) f = 1;
+      else if (eps < m->cfg.derefine_tol && b.loc.level > 0) f = -1;
+      if (refine_only && f < 0) f = 0;
+      locs.push_back(b.loc);
+      flags.push_back(f);
+    }
   }
   if (!refine_only) m->last_flags = flags;
   bool any = false;
@@ -1146,8 +1294,6 @@ ph_status ph_set_state_full(ph_mesh* m, int64_t gid, const double* in, int64_t n
 ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) {
   TRY(need_device(m));
   if (!m->have_state) return fail(PH_ERR_STATE, "no state: call ph_set_problem or ph_set_state + ph_refresh");
-  if (m->cfg.refinement == PH_REF_ADAPTIVE && m->nranks > 1)
-    return fail(PH_ERR_UNSUPPORTED, "adaptive refinement across ranks is not implemented yet");
   CU(launch_cycle_begin(m->d_st, tlim, 1, m->stream));
   m->launches++;
   for (int c = 0; c < ncycles; ++c) TRY(one_cycle(m));

@@ -136,13 +136,17 @@ struct PgenArgs {
   double xmin[3], L[3];
 };
 
-// Remesh data movement (O9): new block slot <- old pool.
-enum RemeshKind : int { R_MOVE = 0, R_REFINE = 1, R_DEREFINE = 2 };
+// Remesh data movement (O9): new pool <- old pool, possibly through the migration
+// send / recv buffers.  MOVE: interior copy; REFINE: prolongate a parent (full block incl. ghosts)
+// into child ch; OCT: restrict a child into octant ch of its parent; OCTCOPY: packed octant ->
+// octant ch.  dst < 0: packed into the send buffer at dst_off; src < 0: from the recv buffer at
+// src_off (packed interior / packed octant / a full block laid out like a pool slot for REFINE).
+enum RemeshKind : int { R_MOVE = 0, R_REFINE = 1, R_OCT = 2, R_OCTCOPY = 3 };
 struct RemeshTask {
   int kind;
-  int dst;       // new slot
-  int src[8];    // MOVE: src[0]; REFINE: src[0] = old parent slot; DEREFINE: old children, (k,j,i) order
-  int ch[3];     // REFINE: which child of the parent
+  int dst, src;
+  int64_t dst_off, src_off;
+  int ch[3];
 };
 
 constexpr int XCHUNK = 256;  // cells per exchange chunk (one CTA, one cell per thread)
@@ -166,8 +170,8 @@ cudaError_t launch_cycle_begin(CycleState* st, double tlim, int set_tlim, cudaSt
 cudaError_t launch_interior_copy(double* U, double* buf, int slot0, int nslots, int to_pool, const Geom& G,
                                  cudaStream_t s);
 cudaError_t launch_tag(const double* U, int nslots, unsigned long long* eps_bits, const Geom& G, cudaStream_t s);
-cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, double* Unew, const Geom& G,
-                          cudaStream_t s);
+cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, double* Unew, const double* rbuf,
+                          double* sbuf, const Geom& G, cudaStream_t s);
 size_t stage_smem_bytes();
 
 }  // namespace ph

@@ -847,23 +847,48 @@ __global__ void tag_kernel(const double* U, unsigned long long* eps_bits, Geom G
   if ((threadIdx.x & 31) == 0) atomicMax(eps_bits + slot, (unsigned long long)__double_as_longlong(mx));
 }
 
-// new pool <- old pool: same-level move, 8-child prolongation of a refined parent (using the
-// parent's valid ghosts for the slopes, A11), pairwise restriction of 8 derefined siblings (A10)
-__global__ void remesh_kernel(const RemeshTask* tasks, const double* Uold, double* Unew, Geom G) {
+// new pool <- old pool (see RemeshTask): same-level move, 8-child prolongation of a refined parent
+// using the parent's valid ghosts for the slopes (A11), pairwise restriction of derefined
+// siblings (A10) -- optionally through the migration buffers
+__global__ void remesh_kernel(const RemeshTask* tasks, const double* Uold, double* Unew, const double* rbuf,
+                              double* sbuf, Geom G) {
   const RemeshTask t = tasks[blockIdx.y];
   const int k = blockIdx.x;
+  const bool oct = (t.kind == R_OCT || t.kind == R_OCTCOPY);
+  const int e0 = oct ? G.nc[0] : G.n[0], e1 = oct ? G.nc[1] : G.n[1], e2 = oct ? G.nc[2] : G.n[2];
+  if (k >= e2) return;
   const int64_t sj = G.N[0], sk = (int64_t)G.N[0] * G.N[1];
-  for (int c = threadIdx.x; c < G.n[0] * G.n[1]; c += blockDim.x) {
-    const int j = c / G.n[0], i = c % G.n[0];
-    const int64_t dq = ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
-    double* d = Unew + (int64_t)t.dst * G.bstride + dq;
-    if (t.kind == R_MOVE) {
-      const double* s = Uold + (int64_t)t.src[0] * G.bstride + dq;
+  const int64_t pstride = (int64_t)e0 * e1 * e2;  // packed var stride
+  for (int c = threadIdx.x; c < e0 * e1; c += blockDim.x) {
+    const int j = c / e0, i = c % e0;
+    const int64_t pk = ((int64_t)k * e1 + j) * e0 + i;  // packed index
+    // destination pointer (per var stride dvs)
+    double* d;
+    int64_t dvs;
+    if (t.dst < 0) {
+      d = sbuf + t.dst_off + pk;
+      dvs = pstride;
+    } else {
+      const int oi = oct ? t.ch[0] * G.nc[0] : 0, oj = oct ? t.ch[1] * G.nc[1] : 0, ok = oct ? t.ch[2] * G.nc[2] : 0;
+      d = Unew + (int64_t)t.dst * G.bstride + ((int64_t)(k + ok + G.g) * G.N[1] + (j + oj + G.g)) * G.N[0] + (i + oi + G.g);
+      dvs = G.vstride;
+    }
+    if (t.kind == R_MOVE || t.kind == R_OCTCOPY) {
+      const double* s;
+      int64_t svs;
+      if (t.src < 0) {
+        s = rbuf + t.src_off + pk;
+        svs = pstride;
+      } else {
+        s = Uold + (int64_t)t.src * G.bstride + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+        svs = G.vstride;
+      }
 #pragma unroll
-      for (int v = 0; v < NVAR; ++v) d[v * G.vstride] = s[v * G.vstride];
+      for (int v = 0; v < NVAR; ++v) d[v * dvs] = s[v * svs];
     } else if (t.kind == R_REFINE) {
+      const double* base = (t.src < 0) ? rbuf + t.src_off : Uold + (int64_t)t.src * G.bstride;
       const int I = t.ch[0] * G.nc[0] + i / 2, J = t.ch[1] * G.nc[1] + j / 2, K = t.ch[2] * G.nc[2] + k / 2;
-      const double* p = Uold + (int64_t)t.src[0] * G.bstride + ((int64_t)(K + G.g) * G.N[1] + (J + G.g)) * G.N[0] + (I + G.g);
+      const double* p = base + ((int64_t)(K + G.g) * G.N[1] + (J + G.g)) * G.N[0] + (I + G.g);
       const double s1 = (i & 1) ? 0.25 : -0.25, s2 = (j & 1) ? 0.25 : -0.25, s3 = (k & 1) ? 0.25 : -0.25;
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
@@ -872,15 +897,12 @@ __global__ void remesh_kernel(const RemeshTask* tasks, const double* Uold, doubl
         const double a1 = minmod_i(c0 - q[-1], q[1] - c0);
         const double a2 = minmod_i(c0 - q[-sj], q[sj] - c0);
         const double a3 = minmod_i(c0 - q[-sk], q[sk] - c0);
-        d[v * G.vstride] = __dadd_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(s1, a1)), __dmul_rn(s2, a2)), __dmul_rn(s3, a3));
+        d[v * dvs] = __dadd_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(s1, a1)), __dmul_rn(s2, a2)), __dmul_rn(s3, a3));
       }
-    } else {
-      const int ci = i / G.nc[0], cj = j / G.nc[1], ck = k / G.nc[2];
-      const int fi = 2 * (i - ci * G.nc[0]), fj = 2 * (j - cj * G.nc[1]), fk = 2 * (k - ck * G.nc[2]);
-      const double* p = Uold + (int64_t)t.src[ck * 4 + cj * 2 + ci] * G.bstride +
-                        ((int64_t)(fk + G.g) * G.N[1] + (fj + G.g)) * G.N[0] + (fi + G.g);
+    } else {  // R_OCT: restrict the child's fine cells 2i..2i+1
+      const double* p = Uold + (int64_t)t.src * G.bstride + ((int64_t)(2 * k + G.g) * G.N[1] + (2 * j + G.g)) * G.N[0] + (2 * i + G.g);
 #pragma unroll
-      for (int v = 0; v < NVAR; ++v) d[v * G.vstride] = mean8(p + v * G.vstride, sj, sk);
+      for (int v = 0; v < NVAR; ++v) d[v * dvs] = mean8(p + v * G.vstride, sj, sk);
     }
   }
 }
@@ -996,11 +1018,11 @@ cudaError_t launch_tag(const double* U, int nslots, unsigned long long* eps_bits
   return cudaGetLastError();
 }
 
-cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, double* Unew, const Geom& G,
-                          cudaStream_t s) {
+cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, double* Unew, const double* rbuf,
+                          double* sbuf, const Geom& G, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
   dim3 grid(G.n[2], ntasks);
-  remesh_kernel<<<grid, 128, 0, s>>>(t, Uold, Unew, G);
+  remesh_kernel<<<grid, 128, 0, s>>>(t, Uold, Unew, rbuf, sbuf, G);
   return cudaGetLastError();
 }
 

@@ -28,6 +28,10 @@ CASES = {
     "smr3_walls": dict(kw=dict(mesh_nx=(32, 16, 16), block_nx=(8, 8, 8), max_level=2, refinement=1, gamma=1.4,
                                regions=[(2, 0.45, 0.55, 0.2, 0.6, 0.3, 0.7)], bc_inner=(1, 1, 2), bc_outer=(1, 2, 1)),
                        problem=1, params=[0.5], cycles=10),
+    # AMR: tagging gathered across ranks, remesh with block migration between GPUs
+    "amr2": dict(kw=dict(mesh_nx=(32, 32, 32), block_nx=(8, 8, 8), xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=2,
+                         refinement=2, refine_tol=0.1, derefine_tol=0.025, derefine_interval=2),
+                 problem=2, params=[10.0, 0.1, 0.1], cycles=10),
 }
 
 
@@ -59,7 +63,7 @@ def main():
         allb = {}
         for o in objs:
             allb.update(o)
-        G = np.stack([allb[g] for g in range(len(allb))])
+        G = np.stack([allb[g] for g in sorted(allb)])
         orc = O.Mesh(**C["kw"])
         orc.set_problem(C["problem"], C["params"])
         orc.step(C["cycles"])
@@ -69,14 +73,17 @@ def main():
         single.set_problem(C["problem"], C["params"])
         single.step(C["cycles"])
         S = np.stack([single.get_state(g) for g in range(single.num_blocks())])
-        bitwise = bool(np.array_equal(S, G))
+        bitwise = bool(S.shape == G.shape and np.array_equal(S, G))
+        same_mesh = [(b["gid"], b["level"], b["lx"]) for b in orc.blocks()] == \
+            [(b["gid"], b["level"], b["lx"]) for b in m.blocks()]
         to = orc.time()
         ho = orc.history()
         res = dict(case=a.case, world=world, parity=e, max_err=max(e.values()), bitwise_vs_1gpu=bitwise,
+                   same_mesh=same_mesh, nblocks=len(allb),
                    t=tm, t_oracle=to, dt_rel=abs(tm[1] - to[1]) / to[1],
                    mass_rel=float(abs(hist[-1, 2] - ho[-1, 2]) / ho[-1, 2]),
                    send_doubles=info["send_doubles_to"])
-        ok = res["max_err"] <= 1e-12 and bitwise and res["dt_rel"] <= 1e-12 and tm[2] == to[2]
+        ok = res["max_err"] <= 1e-12 and bitwise and same_mesh and res["dt_rel"] <= 1e-12 and tm[2] == to[2]
         res["ok"] = ok
         print("MULTI_CHECK " + json.dumps(res), flush=True)
     m.close()
