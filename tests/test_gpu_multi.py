@@ -31,10 +31,13 @@ def _port():
 def test_multi_gpu_matches_oracle_and_single_gpu(case, world):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-           os.path.join(ROOT, "tools", "multi_check.py"), "--case", case]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    for attempt in range(4):  # the free-port probe can race with another rendezvous: retry
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr", "127.0.0.1", "--master-port", str(_port()),
+               os.path.join(ROOT, "tools", "multi_check.py"), "--case", case]
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+        if "EADDRINUSE" not in r.stderr:
+            break
     line = [l for l in r.stdout.splitlines() if l.startswith("MULTI_CHECK")]
     assert r.returncode == 0 and line, r.stdout[-3000:] + r.stderr[-3000:]
     assert '"ok": true' in line[0], line[0]
