@@ -43,26 +43,23 @@ __device__ __forceinline__ void plm_face(double q0, double q1, double q2, double
   wr = fma(-0.5, s2, q2);
 }
 
-// MUFU-seeded Newton reciprocal: rcp.approx (~2^-23) + 2 iterations -> ~1 ulp.  The paper fixes no
-// rounding; parity with the oracle's IEEE division is at round-off ("fp64 budget").
+// MUFU-seeded reciprocal with one third-order correction: r (1 + e + e^2), e = 1 - x r.  The
+// rcp.approx seed (~2^-23) becomes ~1 ulp in 3 fp64 ops.  The paper fixes no rounding; parity
+// with the oracle's IEEE division is at round-off (A31).
 __device__ __forceinline__ double rcp_nr(double x) {
   double r;
   asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  double e = fma(-x, r, 1.0);
-  r = fma(r, e, r);
-  e = fma(-x, r, 1.0);
-  return fma(r, e, r);
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
 }
 
-// MUFU-seeded Newton reciprocal square root (2 iterations)
+// MUFU-seeded reciprocal square root with one third-order correction:
+// y (1 + e/2 + 3e^2/8), e = 1 - x y^2 (5 fp64 ops)
 __device__ __forceinline__ double rsqrt_nr(double x) {
   double y;
   asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  double h = 0.5 * x;
-  double e = fma(-h, y * y, 0.5);
-  y = fma(y, e, y);
-  e = fma(-h, y * y, 0.5);
-  return fma(y, e, y);
+  const double e = fma(-x, y * y, 1.0);
+  return fma(y, e * fma(0.375, e, 0.5), y);
 }
 
 // sound speed c = sqrt(gamma p / rho) = (gamma p) * rsqrt(gamma p rho): one MUFU, no division

@@ -74,6 +74,18 @@ EXPORTS = ["ph_nccl_unique_id", "ph_mesh_create", "ph_mesh_destroy", "ph_set_pro
            "ph_kernel_timing", "ph_last_error"]
 
 _lib = None
+_LIVE = __import__("weakref").WeakSet()
+
+
+def _close_all():
+    for m in list(_LIVE):
+        try:
+            m.close()
+        except Exception:
+            pass
+
+
+__import__("atexit").register(_close_all)
 
 
 def lib():
@@ -183,15 +195,20 @@ class Mesh:
             cfg.stream = C.c_void_p(stream.cuda_stream)
             if torch_alloc:
                 dev = device
+                _calloc = torch.cuda.caching_allocator_alloc
+                _cfree = torch.cuda.caching_allocator_delete
 
                 def _alloc(nbytes, ctx, _s=stream):
                     try:
-                        return torch.cuda.caching_allocator_alloc(int(nbytes), dev, _s)
+                        return _calloc(int(nbytes), dev, _s)
                     except Exception:
                         return None
 
                 def _free(ptr, ctx):
-                    torch.cuda.caching_allocator_delete(ptr)
+                    try:
+                        _cfree(ptr)
+                    except Exception:
+                        pass  # interpreter shutdown: the process is exiting anyway
 
                 a, f = _ALLOC(_alloc), _FREE(_free)
                 self._keep += [a, f]
@@ -206,6 +223,7 @@ class Mesh:
         h = C.c_void_p()
         _check(lib().ph_mesh_create(C.byref(cfg), C.byref(h)))
         self._h = h
+        _LIVE.add(self)
         self.n = tuple(int(x) for x in c["block_nx"])
         self.g = int(c["nghost"])
         self.rank, self.nranks = rank, nranks
