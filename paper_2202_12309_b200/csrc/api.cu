@@ -7,6 +7,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -99,7 +100,12 @@ struct ph_mesh {
   // plans: [0] full exchange, [1] per-cycle exchange
   Plan plan[2];
   bool no_direct_halo = false;  // config: force materialised ghosts every exchange
-  bool ghosts_stale = false;  // a direct-halo cycle ran since the last full exchange
+  bool ghosts_stale = false;
+  bool use_graph = true;                 // PH_NO_GRAPH=1 disables
+  cudaGraphExec_t graph_exec = nullptr;  // one captured cycle
+  cudaStream_t gstream = nullptr;        // private capture / replay stream
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int64_t graph_launches = 0;  // a direct-halo cycle ran since the last full exchange
   bool direct_halo = false;  // uniform mesh: stage kernels read local same-level face neighbours directly
   std::vector<RefluxTask> reflux[3];
   RefluxTask* d_reflux[3] = {nullptr, nullptr, nullptr};
@@ -797,6 +803,10 @@ static ph_status one_cycle(ph_mesh* m) {
  * the new blocks in gid order, so buffer offsets agree without a handshake. */
 static ph_status remesh(ph_mesh* m, const std::unordered_set<LocKey>& leaves, bool move) {
   const int R = m->nranks, me = m->rank;
+  if (m->graph_exec) {
+    cudaGraphExecDestroy(m->graph_exec);
+    m->graph_exec = nullptr;
+  }
   struct Old { int rank; int slot; };
   std::unordered_map<LocKey, Old> old;
   for (auto& b : m->blocks) old[pack(b.loc)] = Old{b.rank, (int)b.local};
@@ -1069,6 +1079,7 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
   m->nranks = cfg->nranks;
   m->host_only = cfg->host_only != 0;
   m->no_direct_halo = cfg->no_direct_halo != 0;
+  m->use_graph = !(getenv("PH_NO_GRAPH") && atoi(getenv("PH_NO_GRAPH")) != 0);
   Geom& G = m->G;
   G.g = cfg->nghost;
   G.cg = (G.g + 1) / 2 + 1;
@@ -1149,12 +1160,16 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
 
 ph_status ph_mesh_destroy(ph_mesh* m) {
   if (!m) return PH_OK;
+  if (m->graph_exec) cudaGraphExecDestroy(m->graph_exec);
+  if (m->ev_fork) cudaEventDestroy(m->ev_fork);
+  if (m->ev_join) cudaEventDestroy(m->ev_join);
   free_all(m);
   for (auto& p : m->t_stage) (void)p;
   for (cudaEvent_t e : m->ev_pool) cudaEventDestroy(e);
   if (m->ev_pack) cudaEventDestroy(m->ev_pack);
   if (m->ev_comm) cudaEventDestroy(m->ev_comm);
   if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
+  if (m->gstream) cudaStreamDestroy(m->gstream);
   if (m->comm) ncclCommDestroy(m->comm);
   delete m->tree;
   delete m;
@@ -1296,7 +1311,53 @@ ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) 
   if (!m->have_state) return fail(PH_ERR_STATE, "no state: call ph_set_problem or ph_set_state + ph_refresh");
   CU(launch_cycle_begin(m->d_st, tlim, 1, m->stream));
   m->launches++;
-  for (int c = 0; c < ncycles; ++c) TRY(one_cycle(m));
+  // Steady state: one CUDA graph per cycle (captured once, replayed; pointers are stable until a
+  // remesh), on a private stream forked from / joined to the caller's stream (the legacy default
+  // stream cannot be captured).  Adaptive meshes (host-side remesh decisions) and kernel-timing
+  // runs stay eager on the caller's stream.
+  const bool graph_ok = m->use_graph && !m->timing && m->cfg.refinement != PH_REF_ADAPTIVE && ncycles > 0;
+  if (graph_ok) {
+    if (!m->gstream) {
+      CU(cudaStreamCreateWithFlags(&m->gstream, cudaStreamNonBlocking));
+      CU(cudaEventCreateWithFlags(&m->ev_fork, cudaEventDisableTiming));
+      CU(cudaEventCreateWithFlags(&m->ev_join, cudaEventDisableTiming));
+    }
+    CU(cudaEventRecord(m->ev_fork, m->stream));
+    CU(cudaStreamWaitEvent(m->gstream, m->ev_fork, 0));
+    cudaStream_t caller = m->stream;
+    m->stream = m->gstream;
+    ph_status st = PH_OK;
+    if (!m->graph_exec) {
+      const int64_t l0 = m->launches;
+      cudaGraph_t gr = nullptr;
+      cudaError_t eb = cudaStreamBeginCapture(m->stream, cudaStreamCaptureModeThreadLocal);
+      if (eb == cudaSuccess) {
+        st = one_cycle(m);
+        cudaError_t ec = cudaStreamEndCapture(m->stream, &gr);
+        if (st == PH_OK && ec != cudaSuccess) st = fail(PH_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ec));
+        if (st == PH_OK) {
+          cudaError_t ei = cudaGraphInstantiate(&m->graph_exec, gr, 0);
+          if (ei != cudaSuccess) st = fail(PH_ERR_CUDA, std::string("instantiate: ") + cudaGetErrorString(ei));
+        }
+        if (gr) cudaGraphDestroy(gr);
+      } else {
+        st = fail(PH_ERR_CUDA, std::string("begin capture: ") + cudaGetErrorString(eb));
+      }
+      m->graph_launches = m->launches - l0;
+      m->launches = l0;
+    }
+    for (int c = 0; c < ncycles && st == PH_OK; ++c) {
+      cudaError_t e = cudaGraphLaunch(m->graph_exec, m->stream);
+      if (e != cudaSuccess) st = fail(PH_ERR_CUDA, std::string("graph launch: ") + cudaGetErrorString(e));
+      m->launches += m->graph_launches;
+    }
+    m->stream = caller;
+    CU(cudaEventRecord(m->ev_join, m->gstream));
+    CU(cudaStreamWaitEvent(m->stream, m->ev_join, 0));
+    TRY(st);
+  } else {
+    for (int c = 0; c < ncycles; ++c) TRY(one_cycle(m));
+  }
   if (ncycles > 0 && m->direct_halo) m->ghosts_stale = true;
   if (info) {
     TRY(check_err(m));

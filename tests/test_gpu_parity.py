@@ -203,3 +203,20 @@ def test_direct_halo_equals_materialised_ghosts(P, bc):
         outs.append((gather(g), g.history()))
     assert np.array_equal(outs[0][0], outs[1][0])
     assert np.array_equal(outs[0][1][:, :2], outs[1][1][:, :2])
+
+
+def test_graph_replay_equals_eager(P, monkeypatch):
+    """one captured cycle replayed N times == N eager cycles (bitwise)"""
+    kw = dict(mesh_nx=(32, 32, 32), block_nx=(16, 16, 16), xmin=(-.5,) * 3, xmax=(.5,) * 3,
+              bc_inner=(1, 0, 2), bc_outer=(2, 0, 1))
+    outs = []
+    for nog in ("0", "1"):
+        monkeypatch.setenv("PH_NO_GRAPH", nog)
+        g = P.Mesh(**kw)
+        g.set_problem(P.BLAST, [10.0, 0.1, 0.2])
+        g.step(3)
+        g.step(2, 0.0)
+        outs.append((gather(g), g.history(), g.launch_count()))
+    assert np.array_equal(outs[0][0], outs[1][0])
+    assert np.array_equal(outs[0][1], outs[1][1])
+    assert outs[0][2] == outs[1][2]
