@@ -137,11 +137,11 @@ constexpr int FXS = TY * (TX + 1);      // var stride of sFx
 constexpr int FYS = (TY + 1) * TX;      // var stride of sFy
 constexpr int FZS = NT;                 // var stride of sFz
 
-template <int RECON, bool REDUCE, bool USE_U0, bool ML>
+template <int RECON, bool REDUCE, bool USE_U0, bool ML, bool FULL>
 __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   extern __shared__ double smem[];
-  double* sW = smem;                       // [4][5][SWY][SWX]
-  double* sFx = sW + 4 * SLOT;             // [5][TY][TX+1]
+  double* sW = smem;                       // [3][5][SWY][SWX]: planes q-2, q-1, q
+  double* sFx = sW + 3 * SLOT;             // [5][TY][TX+1]
   double* sFy = sFx + NVAR * FXS;          // [5][TY+1][TX]
   double* sFz = sFy + NVAR * FYS;          // [2][5][TY][TX]
 
@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   const int slot = A.slots[pb];
   const BlockMeta& M = A.meta[slot];
   const int x0 = txi * TX, y0 = tyi * TY;
-  const int nxt = min(TX, G.n[0] - x0), nyt = min(TY, G.n[1] - y0);
+  const int nxt = FULL ? TX : min(TX, G.n[0] - x0), nyt = FULL ? TY : min(TY, G.n[1] - y0);
   const int k0 = kc * A.KC;
   const int k1 = min(k0 + A.KC, G.n[2]);
   const int g = G.g;
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   const double* Ub = A.Uin + (int64_t)slot * G.bstride;
   const double dt = A.st->dt_used;
   const double idx1 = M.idx[0], idx2 = M.idx[1], idx3 = M.idx[2];
-  const bool own = (tx < nxt) && (ty < nyt);
+  const bool own = FULL || ((tx < nxt) && (ty < nyt));
 
   // ---- load-slot geometry: the plus-shaped halo plane is 2 cells per thread ----
   int sl_i[2], sl_j[2];
@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   };
   auto store_prims = [&](int q) {
     const bool halo = (q < k0) || (q >= k1);
-    double* W = sW + (q & 3) * SLOT;
+    double* W = sW + ((q + 3) % 3) * SLOT;
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
       int i = halo ? tx : sl_i[s], j = halo ? ty : sl_j[s];
@@ -259,7 +259,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
     const int fz = q - 1;                // z face between planes q-2 and q-1
     const bool xy = (c >= k0) && (c < k1);
     const bool zf = (fz >= k0) && (fz <= k1);
-    const double* Wc = sW + (c & 3) * SLOT;
+    const double* Wc = sW + ((c + 3) % 3) * SLOT;
     // prefetch the finish-phase operands of my cell so their latency hides behind the faces
     double uin[NVAR], u0v[NVAR];
     const int64_t cell = (int64_t)slot * G.bstride + (int64_t)(c + g) * plane +
@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
 #pragma unroll 1
       for (int t = tid; t < (TX + 1) * TY; t += NT) {
         const int j = t / (TX + 1), fi = t - j * (TX + 1);
-        if (j < nyt && fi <= nxt) {
+        if (FULL || (j < nyt && fi <= nxt)) {
           const double* p = Wc + (j + 2) * SWX + fi;
           double F[NVAR];
           face_flux<RECON, 1, 2, 3>(p, p + 1, p + 2, p + 3, G, F);
@@ -300,7 +300,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
         const int t = ((tid + 128) & (NT - 1)) + r * NT;
         if (t >= TX * (TY + 1)) break;
         const int jf = t / TX, i = t - jf * TX;
-        if (jf <= nyt && i < nxt) {
+        if (FULL || (jf <= nyt && i < nxt)) {
           const double* p = Wc + jf * SWX + (i + 2);
           double F[NVAR];
           face_flux<RECON, 2, 3, 1>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
@@ -323,9 +323,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
     // face between q-2 and q-1) and its top state, carried in registers to the next face.
     if (own && q >= qbeg + 2) {
       const int o = (ty + 2) * SWX + (tx + 2);
-      const double* pm = sW + ((q - 2) & 3) * SLOT + o;
-      const double* p0 = sW + ((q - 1) & 3) * SLOT + o;
-      const double* pp = sW + (q & 3) * SLOT + o;
+      const double* pm = sW + ((q + 1) % 3) * SLOT + o;
+      const double* p0 = sW + ((q + 2) % 3) * SLOT + o;
+      const double* pp = sW + ((q + 3) % 3) * SLOT + o;
       double bot[NVAR], top[NVAR];
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   }
 }
 
-size_t stage_smem_bytes() { return sizeof(double) * (4 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS); }
+size_t stage_smem_bytes() { return sizeof(double) * (3 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS); }
 
 // ------------------------------------------------------------------------------ exchange kernel
 // One CTA per chunk of <= XCHUNK cells of one task; all tasks of one phase in one launch
@@ -907,22 +907,26 @@ __global__ void remesh_kernel(const RemeshTask* tasks, const double* Uold, doubl
 // ------------------------------------------------------------------------------ launchers
 #define PH_CHECK_LAUNCH() cudaGetLastError()
 
-template <int R, bool RD, bool U0, bool ML>
+template <int R, bool RD, bool U0, bool ML, bool FULL>
 static cudaError_t launch_stage_t(int nblk_cta, const StageArgs& a, const Geom& G, cudaStream_t s) {
   const size_t sm = stage_smem_bytes();
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  stage_kernel<R, RD, U0, ML><<<nblk_cta, NT, sm, s>>>(a, G);
+  stage_kernel<R, RD, U0, ML, FULL><<<nblk_cta, NT, sm, s>>>(a, G);
   return cudaGetLastError();
 }
 
 template <int R, bool RD, bool U0>
 static cudaError_t launch_stage_ml(bool ml, int n, const StageArgs& a, const Geom& G, cudaStream_t s) {
-  return ml ? launch_stage_t<R, RD, U0, true>(n, a, G, s) : launch_stage_t<R, RD, U0, false>(n, a, G, s);
+  // full-tile fast path (block extents multiples of the tile): minmod, uniform-level meshes
+  const bool full = (R == 0) && !ml && (G.n[0] % TX == 0) && (G.n[1] % TY == 0);
+  if (full) return launch_stage_t<0, RD, U0, false, true>(n, a, G, s);
+  return ml ? launch_stage_t<R, RD, U0, true, false>(n, a, G, s) : launch_stage_t<R, RD, U0, false, false>(n, a, G, s);
 }
 
 template <int R>
