@@ -101,6 +101,10 @@ struct ph_mesh {
   Plan plan[2];
   bool no_direct_halo = false;  // config: force materialised ghosts every exchange
   bool ghosts_stale = false;
+  bool overlap = false;                 // multi-GPU direct halo: interior blocks overlap the exchange
+  int n_int = 0;                        // slots [0, n_int) of slot_order have no remote / physical face
+  std::vector<int> slot_order;
+  ncclComm_t comm2 = nullptr;           // split communicator for the dt / totals allgather
   bool use_graph = true;                 // PH_NO_GRAPH=1 disables
   cudaGraphExec_t graph_exec = nullptr;  // one captured cycle
   cudaStream_t gstream = nullptr;        // private capture / replay stream
@@ -530,6 +534,24 @@ static ph_status build_plan(ph_mesh* m) {
       }
     }
   }
+  // stage launch order: with the multi-GPU direct halo, blocks that have no remote or physical
+  // face come first so their stage can run while the halo exchange is in flight
+  m->overlap = m->direct_halo && m->nranks > 1;
+  m->slot_order.clear();
+  std::vector<int> bnd;
+  for (int64_t s = 0; s < nloc; ++s) {
+    const BlockInfo& b = m->blocks[m->local_gids[s]];
+    bool boundary = false;
+    for (int d = 0; d < 3; ++d) boundary = boundary || b.phys_lo[d] || b.phys_hi[d];
+    for (auto& e : b.nbrs) {
+      int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
+      if (nz == 1 && m->blocks[e.gid].rank != me) boundary = true;
+    }
+    if (m->overlap && boundary) bnd.push_back((int)s);
+    else m->slot_order.push_back((int)s);
+  }
+  m->n_int = m->overlap ? (int)m->slot_order.size() : (int)nloc;
+  for (int s : bnd) m->slot_order.push_back(s);
   return PH_OK;
 }
 
@@ -550,9 +572,7 @@ static ph_status setup_device(ph_mesh* m) {
   if (m->n_cslots) TRY(dalloc(m, (void**)&m->C, (size_t)m->n_cslots * G.cbstride * sizeof(double)));
   if (m->n_fslots) TRY(dalloc(m, (void**)&m->fbuf, (size_t)m->n_fslots * G.fstride * sizeof(double)));
   TRY(upload(m, &m->d_meta, m->meta));
-  std::vector<int> slots(nloc);
-  for (int64_t s = 0; s < nloc; ++s) slots[s] = (int)s;
-  TRY(upload(m, &m->d_slots, slots));
+  TRY(upload(m, &m->d_slots, m->slot_order));
   for (Plan& pl : m->plan)
     for (Phase* P : pl.phases()) TRY(upload_phase(m, *P));
   m->sbuf_n = std::max(m->plan[0].sbuf_n, m->plan[1].sbuf_n);
@@ -622,52 +642,74 @@ static cudaEvent_t pool_event(ph_mesh* m) {
   return e;
 }
 
-static ph_status exchange(ph_mesh* m, double* U, int which) {
+/* Exchange, split in two so that compute can run between them (O7; remote buffers first,
+ * P:1279-1285).  begin: pack remote buffers and start the grouped NCCL send/recv on the comm
+ * stream.  end: rank-local fills, unpack, staging completion, prolongation, physical BCs. */
+static ph_status exchange_begin(ph_mesh* m, double* U, int which) {
   Plan& PL = m->plan[which];
-  const Geom& G = m->G;
+  const bool remote = (m->nranks > 1) && (PL.sbuf_n > 0 || PL.rbuf_n > 0);
+  if (!remote) return PH_OK;
   XArgs a{};
   a.U = U;
   a.C = m->C;
   a.sbuf = m->sbuf;
   a.rbuf = m->rbuf;
+  if (PL.pack.nchunks()) {
+    a.tasks = PL.pack.d_tasks;
+    a.chunks = PL.pack.d_chunks;
+    CU(launch_xfill(PL.pack.nchunks(), a, m->G, m->stream));
+    m->launches++;
+  }
+  CU(cudaEventRecord(m->ev_pack, m->stream));
+  CU(cudaStreamWaitEvent(m->comm_stream, m->ev_pack, 0));
+  NC(ncclGroupStart());
+  for (int p = 0; p < m->nranks; ++p) {
+    if (p == m->rank) continue;
+    if (PL.send_cnt[p]) NC(ncclSend(m->sbuf + PL.send_off[p], PL.send_cnt[p], ncclDouble, p, m->comm, m->comm_stream));
+    if (PL.recv_cnt[p]) NC(ncclRecv(m->rbuf + PL.recv_off[p], PL.recv_cnt[p], ncclDouble, p, m->comm, m->comm_stream));
+  }
+  NC(ncclGroupEnd());
+  CU(cudaEventRecord(m->ev_comm, m->comm_stream));
+  return PH_OK;
+}
+
+static ph_status exchange_end(ph_mesh* m, double* U, int which) {
+  Plan& PL = m->plan[which];
+  const bool remote = (m->nranks > 1) && (PL.sbuf_n > 0 || PL.rbuf_n > 0);
+  XArgs a{};
+  a.U = U;
+  a.C = m->C;
+  a.sbuf = m->sbuf;
+  a.rbuf = m->rbuf;
+  auto run = [&](Phase& P) -> ph_status {
+    if (P.nchunks() == 0) return PH_OK;
+    a.tasks = P.d_tasks;
+    a.chunks = P.d_chunks;
+    CU(launch_xfill(P.nchunks(), a, m->G, m->stream));
+    m->launches++;
+    return PH_OK;
+  };
+  TRY(run(PL.local));
+  if (remote) {
+    CU(cudaStreamWaitEvent(m->stream, m->ev_comm, 0));
+    TRY(run(PL.unpack));
+  }
+  TRY(run(PL.b1));
+  TRY(run(PL.b2));
+  TRY(run(PL.pro));
+  TRY(run(PL.bcf));
+  return PH_OK;
+}
+
+static ph_status exchange(ph_mesh* m, double* U, int which) {
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   if (m->timing) {
     t0 = pool_event(m);
     t1 = pool_event(m);
     CU(cudaEventRecord(t0, m->stream));
   }
-  auto run = [&](Phase& P, cudaStream_t s) -> ph_status {
-    if (P.nchunks() == 0) return PH_OK;
-    a.tasks = P.d_tasks;
-    a.chunks = P.d_chunks;
-    CU(launch_xfill(P.nchunks(), a, G, s));
-    m->launches++;
-    return PH_OK;
-  };
-  const bool remote = (m->nranks > 1) && (PL.sbuf_n > 0 || PL.rbuf_n > 0);
-  if (remote) {
-    // remote buffers first, then the local copies overlap the NCCL transfer
-    TRY(run(PL.pack, m->stream));
-    CU(cudaEventRecord(m->ev_pack, m->stream));
-    CU(cudaStreamWaitEvent(m->comm_stream, m->ev_pack, 0));
-    NC(ncclGroupStart());
-    for (int p = 0; p < m->nranks; ++p) {
-      if (p == m->rank) continue;
-      if (PL.send_cnt[p]) NC(ncclSend(m->sbuf + PL.send_off[p], PL.send_cnt[p], ncclDouble, p, m->comm, m->comm_stream));
-      if (PL.recv_cnt[p]) NC(ncclRecv(m->rbuf + PL.recv_off[p], PL.recv_cnt[p], ncclDouble, p, m->comm, m->comm_stream));
-    }
-    NC(ncclGroupEnd());
-    CU(cudaEventRecord(m->ev_comm, m->comm_stream));
-  }
-  TRY(run(PL.local, m->stream));
-  if (remote) {
-    CU(cudaStreamWaitEvent(m->stream, m->ev_comm, 0));
-    TRY(run(PL.unpack, m->stream));
-  }
-  TRY(run(PL.b1, m->stream));
-  TRY(run(PL.b2, m->stream));
-  TRY(run(PL.pro, m->stream));
-  TRY(run(PL.bcf, m->stream));
+  TRY(exchange_begin(m, U, which));
+  TRY(exchange_end(m, U, which));
   if (m->timing) {
     CU(cudaEventRecord(t1, m->stream));
     m->t_exch.push_back({t0, t1});
@@ -679,7 +721,8 @@ static ph_status exchange(ph_mesh* m, double* U, int which) {
 static ph_status reduce_finalize(ph_mesh* m, int ncta, int mode) {
   CU(launch_rank_reduce(m->partials, ncta, m->nranks > 1 ? m->my6 : m->all6, m->stream));
   m->launches++;
-  if (m->nranks > 1) NC(ncclAllGather(m->my6, m->all6, 6, ncclDouble, m->comm, m->stream));
+  if (m->nranks > 1)
+    NC(ncclAllGather(m->my6, m->all6, 6, ncclDouble, m->comm2 ? m->comm2 : m->comm, m->stream));
   CU(launch_finalize(m->all6, m->nranks, m->d_st, m->hist, m->hist_cap, m->G.cfl, mode, m->tot5, m->stream));
   m->launches++;
   return PH_OK;
@@ -696,11 +739,12 @@ static ph_status standalone_reduce(ph_mesh* m, double* U, int mode) {
 
 /* one stage over all local blocks, pack by pack (a2-a5) */
 static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a0, double b1, double cdt,
-                           bool reduce, int stage) {
+                           bool reduce, int stage, int s0 = 0, int s1 = -1, bool post = true) {
   const int nloc = (int)m->local_gids.size();
+  if (s1 < 0) s1 = nloc;
   const int per_blk = m->ntx * m->nty * m->nkc;
-  for (int p0 = 0; p0 < nloc; p0 += m->pack_size) {
-    int np = std::min(m->pack_size, nloc - p0);
+  for (int p0 = s0; p0 < s1; p0 += m->pack_size) {
+    int np = std::min(m->pack_size, s1 - p0);
     StageArgs A{};
     A.Uin = Uin;
     A.U0 = m->U0;
@@ -733,7 +777,7 @@ static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a
       m->t_stage.push_back({t0, t1});
     }
   }
-  if (m->multilevel) {
+  if (m->multilevel && post) {
     if (m->nranks > 1 && (m->fsbuf_n > 0 || m->frbuf_n > 0)) {
       // fine ranks restrict and send their coarse-fine face fluxes to the coarse blocks' ranks
       if (!m->fpack.empty()) {
@@ -766,6 +810,20 @@ static ph_status one_cycle(ph_mesh* m) {
   const bool adaptive = m->cfg.refinement == PH_REF_ADAPTIVE;
   const bool fuse_reduce = !m->multilevel && !adaptive;
   const int nloc = (int)m->local_gids.size();
+  if (m->overlap && fuse_reduce) {
+    // multi-GPU, uniform mesh: stage 2 of the interior blocks overlaps the U1 halo exchange,
+    // the dt / totals reduction (split communicator) overlaps the U0 exchange
+    const bool vl2 = m->cfg.integrator == PH_INT_VL2;
+    TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, vl2 ? 0.5 : 1.0, false, 1));
+    TRY(exchange_begin(m, m->U1, 1));
+    TRY(run_stage(m, m->U1, m->U0, vl2 ? 1.0 : 0.5, vl2 ? 0.0 : 0.5, vl2 ? 1.0 : 0.5, true, 2, 0, m->n_int));
+    TRY(exchange_end(m, m->U1, 1));
+    TRY(run_stage(m, m->U1, m->U0, vl2 ? 1.0 : 0.5, vl2 ? 0.0 : 0.5, vl2 ? 1.0 : 0.5, true, 2, m->n_int, nloc));
+    TRY(exchange_begin(m, m->U0, 1));
+    TRY(reduce_finalize(m, nloc > 0 ? m->stage_ctas : 0, 1));
+    TRY(exchange_end(m, m->U0, 1));
+    return PH_OK;
+  }
   if (m->cfg.integrator == PH_INT_VL2) {
     TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, 0.5, false, 1));
     TRY(exchange(m, m->U1, 1));
@@ -1140,6 +1198,9 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
         delete m;
         return fail(PH_ERR_COMM, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
       }
+      // a second communicator for the scalar reductions, so they never queue behind the halo
+      r = ncclCommSplit(m->comm, 0, m->rank, &m->comm2, nullptr);
+      if (r != ncclSuccess) m->comm2 = nullptr;
     }
     st = setup_persistent(m);
     if (st == PH_OK) st = setup_device(m);
@@ -1170,6 +1231,7 @@ ph_status ph_mesh_destroy(ph_mesh* m) {
   if (m->ev_comm) cudaEventDestroy(m->ev_comm);
   if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
   if (m->gstream) cudaStreamDestroy(m->gstream);
+  if (m->comm2) ncclCommDestroy(m->comm2);
   if (m->comm) ncclCommDestroy(m->comm);
   delete m->tree;
   delete m;

@@ -108,6 +108,12 @@ __device__ __forceinline__ void set_error(ErrWord* err, int stage, long long gid
 // the x and y faces of plane q-2 and the z faces between planes q-2 and q-1 (a3 PLM + a4 HLLE,
 // one shared code path per face), and finishes the cells of plane q-2: flux divergence and the
 // RK stage combine (a5).  The final stage also reduces the CFL term and the totals (a6, a10).
+#ifndef PH_PREFETCH
+#define PH_PREFETCH 0
+#endif
+#ifndef PH_PREFETCH_L1
+#define PH_PREFETCH_L1 1
+#endif
 constexpr int TX = TILE_X, TY = TILE_Y, NT = TX * TY;
 constexpr int SWX = TX + 4, SWY = TY + 4;
 constexpr int VS = SWY * SWX;           // var stride in a ring slot
@@ -210,14 +216,38 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   const double* zhi = M.nb[5] >= 0 ? A.Uin + (int64_t)M.nb[5] * G.bstride + colo - (int64_t)G.n[2] * plane : obase;
 
   double pf[2][NVAR];
-  auto issue_load = [&](int q) {
+  auto slot_ptr = [&](int q, int s) -> const double* {
     const bool halo = (q < k0) || (q >= k1);
     const int64_t qo = (int64_t)(q + g) * plane;
+    return halo ? ((q < 0 ? zlo : (q >= G.n[2] ? zhi : obase)) + qo) : (sbase[s] + qo);
+  };
+  auto slot_ok = [&](int q, int s) -> bool {
+    const bool halo = (q < k0) || (q >= k1);
+    return halo ? (s == 0 && own) : sl_ok[s];
+  };
+  // The next plane is only *prefetched* (no destination register, so no scoreboard is held across
+  // the face phase); the real loads at store time then hit in cache.
+  auto prefetch_plane = [&](int q) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
-      bool ok = halo ? (s == 0 && own) : sl_ok[s];
-      if (ok) {
-        const double* p = halo ? ((q < 0 ? zlo : (q >= G.n[2] ? zhi : obase)) + qo) : (sbase[s] + qo);
+      if (slot_ok(q, s)) {
+        const double* p = slot_ptr(q, s);
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) {
+#if PH_PREFETCH_L1
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(p + v * G.vstride));
+#else
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p + v * G.vstride));
+#endif
+        }
+      }
+    }
+  };
+  auto issue_load = [&](int q) {
+#pragma unroll
+    for (int s = 0; s < 2; ++s) {
+      if (slot_ok(q, s)) {
+        const double* p = slot_ptr(q, s);
 #pragma unroll
         for (int v = 0; v < NVAR; ++v) pf[s][v] = __ldg(p + v * G.vstride);
       }
@@ -250,10 +280,17 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   double tmax = 0.0, tsum[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};
   double topz[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};  // z top state of plane q-2 (my column)
   const int qbeg = k0 - 2, qend = k1 + 2;
+#if PH_PREFETCH
+  for (int q = qbeg; q < qend; ++q) {
+    issue_load(q);
+    store_prims(q);
+    if (q + 1 < qend) prefetch_plane(q + 1);
+#else
   issue_load(qbeg);
   for (int q = qbeg; q < qend; ++q) {
     store_prims(q);
     if (q + 1 < qend) issue_load(q + 1);
+#endif
     __syncthreads();
     const int c = q - 2;                 // plane whose x/y faces and cells are done now
     const int fz = q - 1;                // z face between planes q-2 and q-1

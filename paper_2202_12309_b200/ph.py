@@ -11,7 +11,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIBPATH = os.path.join(_HERE, "libph.so")
+_LIBPATH = os.environ.get("PH_LIB") or os.path.join(_HERE, "libph.so")  # PH_LIB: A/B builds
 
 PERIODIC, OUTFLOW, REFLECT = 0, 1, 2
 MINMOD, VANLEER, MC = 0, 1, 2
