@@ -56,7 +56,7 @@ typedef enum {
 typedef enum { PH_BC_PERIODIC = 0, PH_BC_OUTFLOW = 1, PH_BC_REFLECT = 2 } ph_bc;       /* A9 */
 typedef enum { PH_RECON_PLM_MINMOD = 0, PH_RECON_PLM_VANLEER = 1, PH_RECON_PLM_MC = 2 } ph_recon; /* A3 */
 typedef enum { PH_INT_RK2 = 0, PH_INT_VL2 = 1 } ph_integrator;                      /* A1 */
-typedef enum { PH_PROB_LINEAR_WAVE = 0, PH_PROB_SOD = 1, PH_PROB_BLAST = 2 } ph_problem;
+typedef enum { PH_PROB_LINEAR_WAVE = 0, PH_PROB_SOD = 1, PH_PROB_BLAST = 2, PH_PROB_KH = 3 } ph_problem;
 typedef enum { PH_REF_NONE = 0, PH_REF_STATIC = 1, PH_REF_ADAPTIVE = 2 } ph_refinement;
 
 typedef struct {
@@ -141,7 +141,8 @@ ph_status ph_mesh_destroy(ph_mesh* m);
 
 /* ---- state -------------------------------------------------------------------------------- */
 /* Problem generator on the device (O4): LINEAR_WAVE p = {A, k1, k2, k3};
- * SOD p = {x_split}; BLAST p = {p_in, p_out, radius[, cx, cy, cz]}.  Runs AMR pre-refinement
+ * SOD p = {x_split}; BLAST p = {p_in, p_out, radius[, cx, cy, cz]}; KH p = {A, sigma}
+ * (Kelvin-Helmholtz shear layers, the paper's AMR demo P:702, A36).  Runs AMR pre-refinement
  * when refinement is adaptive, fills ghosts and computes the initial dt.  Collective. */
 ph_status ph_set_problem(ph_mesh* m, int32_t problem, const double* p, int32_t np);
 /* Upload one block's interior [5][n3][n2][n1] (only the rank owning gid copies; others no-op).

@@ -28,7 +28,7 @@ _LIB = os.path.join(_HERE, "liboracle.so")
 PERIODIC, OUTFLOW, REFLECT = 0, 1, 2
 MINMOD, VANLEER, MC = 0, 1, 2
 RK2, VL2 = 0, 1
-LINEAR_WAVE, SOD, BLAST = 0, 1, 2
+LINEAR_WAVE, SOD, BLAST, KH = 0, 1, 2, 3
 REF_NONE, REF_STATIC, REF_ADAPTIVE = 0, 1, 2
 
 

@@ -416,6 +416,20 @@ void pgen_block(const orc_mesh* m, Block& b) {
           if (x < xs) { W[0] = 1.0; W[4] = 1.0; }
           else { W[0] = 0.125; W[4] = 0.1; }
           W[1] = W[2] = W[3] = 0.0;
+        } else if (m->problem == ORC_PROB_KH) {
+          /* Kelvin-Helmholtz (reading A36): dense (rho 2) slab |y' - 1/2| < 1/4 moving at
+           * +1/2 in x through rho 1 at -1/2, p = 2.5, vy = A sin(4 pi x') (exp(-((y'-1/4)/s)^2) +
+           * exp(-((y'-3/4)/s)^2)), x', y' the coordinates scaled to [0,1) */
+          double A = pp[0], sig = pp[1];
+          double xx = (x - m->cfg.xmin[0]) / (m->cfg.xmax[0] - m->cfg.xmin[0]);
+          double yy = (y - m->cfg.xmin[1]) / (m->cfg.xmax[1] - m->cfg.xmin[1]);
+          bool in = std::fabs(yy - 0.5) < 0.25;
+          double e1 = (yy - 0.25) / sig, e2 = (yy - 0.75) / sig;
+          W[0] = in ? 2.0 : 1.0;
+          W[1] = in ? 0.5 : -0.5;
+          W[2] = A * std::sin(4.0 * M_PI * xx) * (std::exp(-(e1 * e1)) + std::exp(-(e2 * e2)));
+          W[3] = 0.0;
+          W[4] = 2.5;
         } else {
           double pin = pp[0], pout = pp[1], r = pp[2];
           double dx = x - pp[3], dy = y - pp[4], dz = z - pp[5];
@@ -1150,6 +1164,10 @@ int orc_set_problem(orc_mesh* m, int32_t problem, const double* p, int32_t np) {
       for (int d = 0; d < 3; ++d) pp[3 + d] = 0.5 * (m->cfg.xmin[d] + m->cfg.xmax[d]);
     }
     if (!(pp[0] > 0 && pp[1] > 0 && pp[2] > 0)) return fail(ORC_ERR_INVALID_ARG, "blast parameters out of range");
+  } else if (problem == ORC_PROB_KH) {
+    if (np < 1) pp.push_back(0.01);
+    if (pp.size() < 2) pp.push_back(0.05);
+    if (!(pp[1] > 0)) return fail(ORC_ERR_INVALID_ARG, "KH sigma must be positive");
   } else {
     return fail(ORC_ERR_INVALID_ARG, "unknown problem");
   }

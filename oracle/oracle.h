@@ -26,7 +26,7 @@ enum { ORC_OK = 0, ORC_ERR_INVALID_ARG = 1, ORC_ERR_CONFIG = 2, ORC_ERR_PHYSICS 
 enum { ORC_BC_PERIODIC = 0, ORC_BC_OUTFLOW = 1, ORC_BC_REFLECT = 2 };
 enum { ORC_RECON_MINMOD = 0, ORC_RECON_VANLEER = 1, ORC_RECON_MC = 2 };
 enum { ORC_INT_RK2 = 0, ORC_INT_VL2 = 1 };
-enum { ORC_PROB_LINEAR_WAVE = 0, ORC_PROB_SOD = 1, ORC_PROB_BLAST = 2 };
+enum { ORC_PROB_LINEAR_WAVE = 0, ORC_PROB_SOD = 1, ORC_PROB_BLAST = 2, ORC_PROB_KH = 3 };
 enum { ORC_REF_NONE = 0, ORC_REF_STATIC = 1, ORC_REF_ADAPTIVE = 2 };
 
 typedef struct {
@@ -55,7 +55,8 @@ typedef struct orc_mesh orc_mesh;
 int orc_mesh_create(const orc_config* cfg, orc_mesh** out);
 int orc_mesh_destroy(orc_mesh* m);
 /* Problem generators.  LINEAR_WAVE p = {A, k1, k2, k3}; SOD p = {x_split};
- * BLAST p = {p_in, p_out, radius, cx, cy, cz}.  Applies AMR pre-refinement when adaptive. */
+ * BLAST p = {p_in, p_out, radius, cx, cy, cz}; KH p = {A, sigma} (reading A36).
+ * Applies AMR pre-refinement when adaptive. */
 int orc_set_problem(orc_mesh* m, int32_t problem, const double* p, int32_t np);
 int orc_set_state(orc_mesh* m, int64_t gid, const double* cons, int64_t nelem); /* [5][n3][n2][n1] */
 int orc_get_state(const orc_mesh* m, int64_t gid, double* cons, int64_t nelem);

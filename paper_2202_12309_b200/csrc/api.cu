@@ -1277,6 +1277,10 @@ ph_status ph_set_problem(ph_mesh* m, int32_t problem, const double* p, int32_t n
     if (np < 6)
       for (int d = 0; d < 3; ++d) P.p[3 + d] = 0.5 * (m->cfg.xmin[d] + m->cfg.xmax[d]);
     if (!(P.p[0] > 0 && P.p[1] > 0 && P.p[2] > 0)) return fail(PH_ERR_INVALID_ARG, "blast parameters out of range");
+  } else if (problem == PH_PROB_KH) {
+    if (np < 1) P.p[0] = 0.01;
+    if (np < 2) P.p[1] = 0.05;
+    if (!(P.p[1] > 0)) return fail(PH_ERR_INVALID_ARG, "KH sigma must be positive");
   } else {
     return fail(PH_ERR_INVALID_ARG, "unknown problem");
   }

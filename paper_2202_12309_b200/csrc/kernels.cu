@@ -699,6 +699,17 @@ __global__ void pgen_kernel(double* U, const BlockMeta* meta, int nslots, PgenAr
       W[0] = left ? 1.0 : 0.125;
       W[4] = left ? 1.0 : 0.1;
       W[1] = W[2] = W[3] = 0.0;
+    } else if (P.problem == 3) {  // Kelvin-Helmholtz (A36)
+      double xx = __ddiv_rn(__dsub_rn(x, P.xmin[0]), P.L[0]);
+      double yy = __ddiv_rn(__dsub_rn(y, P.xmin[1]), P.L[1]);
+      bool in = fabs(__dsub_rn(yy, 0.5)) < 0.25;
+      double e1 = __ddiv_rn(__dsub_rn(yy, 0.25), P.p[1]), e2 = __ddiv_rn(__dsub_rn(yy, 0.75), P.p[1]);
+      W[0] = in ? 2.0 : 1.0;
+      W[1] = in ? 0.5 : -0.5;
+      W[2] = __dmul_rn(__dmul_rn(P.p[0], sin(__dmul_rn(4.0 * 3.14159265358979323846, xx))),
+                       __dadd_rn(exp(-__dmul_rn(e1, e1)), exp(-__dmul_rn(e2, e2))));
+      W[3] = 0.0;
+      W[4] = 2.5;
     } else {  // blast (A21)
       double dx = __dsub_rn(x, P.p[3]), dy = __dsub_rn(y, P.p[4]), dz = __dsub_rn(z, P.p[5]);
       double r2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));

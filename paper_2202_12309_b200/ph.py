@@ -16,7 +16,7 @@ _LIBPATH = os.environ.get("PH_LIB") or os.path.join(_HERE, "libph.so")  # PH_LIB
 PERIODIC, OUTFLOW, REFLECT = 0, 1, 2
 MINMOD, VANLEER, MC = 0, 1, 2
 RK2, VL2 = 0, 1
-LINEAR_WAVE, SOD, BLAST = 0, 1, 2
+LINEAR_WAVE, SOD, BLAST, KH = 0, 1, 2, 3
 REF_NONE, REF_STATIC, REF_ADAPTIVE = 0, 1, 2
 ABI_VERSION = 1
 

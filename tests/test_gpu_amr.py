@@ -100,3 +100,23 @@ def test_config3_amr_blast_full_size(oracle_mod, P):
     _same_mesh(o, g)
     assert np.array_equal(o.refine_flags(), g.refine_flags())
     assert_parity(gather(g), gather(o))
+
+
+@pytest.mark.parametrize("adaptive", [False, True])
+def test_kh_matches_oracle(oracle_mod, P, adaptive):
+    """Kelvin-Helmholtz (the paper's AMR demo; A36): static two-level and adaptive."""
+    kw = dict(mesh_nx=(32, 32, 8), block_nx=(8, 8, 8), gamma=1.4, max_level=1,
+              regions=[(1, 0.0, 1.0, 0.2, 0.3, 0.0, 1.0)])
+    if adaptive:
+        kw.update(refinement=P.REF_ADAPTIVE, refine_tol=2e-3, derefine_tol=1e-4, derefine_interval=4)
+    else:
+        kw.update(refinement=P.REF_STATIC)
+    o, g = oracle_mod.Mesh(**kw), P.Mesh(**kw)
+    for m in (o, g):
+        m.set_problem(P.KH, [0.01, 0.05])
+    _same_mesh(o, g)
+    for c in range(3):
+        o.step(4)
+        g.step(4)
+        _same_mesh(o, g)
+        assert_parity(gather(g), gather(o))
