@@ -26,7 +26,7 @@ _SRC = os.path.join(_HERE, "oracle.cpp")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 PERIODIC, OUTFLOW, REFLECT = 0, 1, 2
-MINMOD, VANLEER, MC = 0, 1, 2
+MINMOD, VANLEER, MC, PPM, WENOZ = 0, 1, 2, 3, 4
 RK2, VL2 = 0, 1
 LINEAR_WAVE, SOD, BLAST, KH = 0, 1, 2, 3
 REF_NONE, REF_STATIC, REF_ADAPTIVE = 0, 1, 2
@@ -86,6 +86,8 @@ def lib():
         L.orc_prim_to_cons.restype = None
         L.orc_plm.argtypes = [C.c_double, C.c_double, C.c_double, C.c_int32, dp, dp]
         L.orc_plm.restype = None
+        L.orc_recon5.argtypes = [dp, C.c_int32, dp, dp]
+        L.orc_recon5.restype = None
         L.orc_hlle.argtypes = [dp, dp, C.c_double, dp]
         L.orc_hlle.restype = None
         L.orc_flux_phys.argtypes = [dp, C.c_double, dp]
@@ -152,6 +154,13 @@ def prim_to_cons(W, gamma):
 def plm(qm, q0, qp, recon=MINMOD):
     a, b = C.c_double(), C.c_double()
     lib().orc_plm(qm, q0, qp, recon, C.byref(a), C.byref(b))
+    return a.value, b.value
+
+
+def recon5(q, recon):
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    a, b = C.c_double(), C.c_double()
+    lib().orc_recon5(_dp(q), recon, C.byref(a), C.byref(b))
     return a.value, b.value
 
 

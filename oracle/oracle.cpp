@@ -115,6 +115,66 @@ double plm_slope(double qm, double q0, double qp, int recon) {
   return minmod(dl, dr);
 }
 
+/* NEXT 3, reading A37: PPM of Colella & Woodward (1984) eqs. 1.6-1.10 on primitives.
+ * q[0..4] = q_{i-2} .. q_{i+2}; returns the left-face (i-1/2) and right-face (i+1/2) values. */
+double ppm_dm(double a, double b, double c) {
+  /* limited centred slope: sgn(dq) min(|dq|, 2|b-a|, 2|c-b|) if b is not an extremum, else 0 */
+  double dl = b - a, dr = c - b;
+  bool same = (dl > 0.0 && dr > 0.0) || (dl < 0.0 && dr < 0.0);
+  if (!same) return 0.0;
+  double dq = 0.5 * (c - a);
+  double m = std::fabs(dq);
+  if (2.0 * std::fabs(dl) < m) m = 2.0 * std::fabs(dl);
+  if (2.0 * std::fabs(dr) < m) m = 2.0 * std::fabs(dr);
+  return dq > 0.0 ? m : -m;
+}
+
+void ppm_cell(const double* q, double* ql, double* qr) {
+  double dm_m = ppm_dm(q[0], q[1], q[2]), dm_0 = ppm_dm(q[1], q[2], q[3]), dm_p = ppm_dm(q[2], q[3], q[4]);
+  double L = q[1] + 0.5 * (q[2] - q[1]) - (dm_0 - dm_m) / 6.0; /* eq. 1.6 at i-1/2 */
+  double R = q[2] + 0.5 * (q[3] - q[2]) - (dm_p - dm_0) / 6.0; /* eq. 1.6 at i+1/2 */
+  double c = q[2];
+  if ((R - c) * (c - L) <= 0.0) {
+    L = c;
+    R = c;                                                       /* eq. 1.10, local extremum */
+  } else {
+    double d = R - L, m6 = 6.0 * (c - 0.5 * (L + R));
+    if (d * m6 > d * d) L = 3.0 * c - 2.0 * R;                   /* overshoot at the left */
+    else if (-(d * d) > d * m6) R = 3.0 * c - 2.0 * L;           /* overshoot at the right */
+  }
+  *ql = L;
+  *qr = R;
+}
+
+/* NEXT 3, reading A38: WENO-Z of Borges et al. (2008), 5th order, p = 2, eps = 1e-40, on
+ * primitives.  Value at the right face of c from the stencil a, b, c, d, e. */
+double wenoz_face(double a, double b, double c, double d, double e) {
+  double t0 = a - 2.0 * b + c, u0 = a - 4.0 * b + 3.0 * c;
+  double t1 = b - 2.0 * c + d, u1 = b - d;
+  double t2 = c - 2.0 * d + e, u2 = 3.0 * c - 4.0 * d + e;
+  double b0 = (13.0 / 12.0) * (t0 * t0) + 0.25 * (u0 * u0);
+  double b1 = (13.0 / 12.0) * (t1 * t1) + 0.25 * (u1 * u1);
+  double b2 = (13.0 / 12.0) * (t2 * t2) + 0.25 * (u2 * u2);
+  double tau = std::fabs(b0 - b2);
+  const double eps = 1e-40;
+  double r0 = tau / (b0 + eps), r1 = tau / (b1 + eps), r2 = tau / (b2 + eps);
+  double a0 = 0.1 * (1.0 + r0 * r0), a1 = 0.6 * (1.0 + r1 * r1), a2 = 0.3 * (1.0 + r2 * r2);
+  double q0 = (2.0 * a - 7.0 * b + 11.0 * c) / 6.0;
+  double q1 = (-b + 5.0 * c + 2.0 * d) / 6.0;
+  double q2 = (2.0 * c + 5.0 * d - e) / 6.0;
+  return ((a0 * q0 + a1 * q1) + a2 * q2) / ((a0 + a1) + a2);
+}
+
+/* face values of cell q[2] for the high-order reconstructions (q[0..4] = q_{i-2} .. q_{i+2}) */
+void recon5(const double* q, int recon, double* ql, double* qr) {
+  if (recon == ORC_RECON_PPM) {
+    ppm_cell(q, ql, qr);
+  } else {
+    *qr = wenoz_face(q[0], q[1], q[2], q[3], q[4]);
+    *ql = wenoz_face(q[4], q[3], q[2], q[1], q[0]);
+  }
+}
+
 /* physical flux and conserved state of a face state in the normal frame (O5 a4) */
 void phys(const double* W, double gamma, double* U, double* F) {
   double rho = W[0], u = W[1], v = W[2], w = W[3], p = W[4];
@@ -702,6 +762,20 @@ int compute_fluxes(const orc_mesh* m, const Block& b, const std::vector<double>&
           int64_t c[3] = {i, j, k};
           double WL[5], WR[5];
           for (int v = 0; v < 5; ++v) {
+            if (m->cfg.recon >= ORC_RECON_PPM) {
+              /* 6 points c-3 .. c+2: cell c-1 uses q[0..4], cell c uses q[1..5] */
+              double q[6], a, bb;
+              for (int s = 0; s < 6; ++s) {
+                int64_t cc[3] = {c[0], c[1], c[2]};
+                cc[d] += s - 3;
+                q[s] = W[m->idx(v, cc[2], cc[1], cc[0])];
+              }
+              recon5(q, m->cfg.recon, &a, &WL[v]);      /* right face of cell c-1 */
+              recon5(q + 1, m->cfg.recon, &WR[v], &bb); /* left face of cell c */
+              (void)a;
+              (void)bb;
+              continue;
+            }
             double q[4];
             for (int s = 0; s < 4; ++s) {
               int64_t cc[3] = {c[0], c[1], c[2]};
@@ -1051,6 +1125,7 @@ void orc_plm(double qm, double q0, double qp, int32_t recon, double* ql, double*
   *ql = q0 - 0.5 * D;
   *qr = q0 + 0.5 * D;
 }
+void orc_recon5(const double q[5], int32_t recon, double* ql, double* qr) { recon5(q, recon, ql, qr); }
 void orc_hlle(const double WL[5], const double WR[5], double gamma, double F[5]) { hlle(WL, WR, gamma, F); }
 void orc_flux_phys(const double W[5], double gamma, double F[5]) {
   double U[5];
@@ -1069,7 +1144,10 @@ double orc_pairwise_sum(const double* a, int64_t n) { return pairwise_sum(a, n);
 int orc_mesh_create(const orc_config* cfg, orc_mesh** out) {
   if (!cfg || !out) return fail(ORC_ERR_INVALID_ARG, "null argument");
   *out = nullptr;
-  if (cfg->nghost != 2) return fail(ORC_ERR_CONFIG, "nghost must be 2 (PLM)");
+  if (cfg->nghost != 2 && cfg->nghost != 3) return fail(ORC_ERR_CONFIG, "nghost must be 2 (PLM) or 3 (PPM, WENO-Z)");
+  if (cfg->recon >= ORC_RECON_PPM && cfg->nghost != 3) return fail(ORC_ERR_CONFIG, "PPM / WENO-Z need nghost = 3 (A8)");
+  if (cfg->nghost == 3 && cfg->max_level > 0)
+    return fail(ORC_ERR_CONFIG, "nghost = 3 is supported on uniform meshes only (reading A39)");
   if (!(cfg->gamma > 1.0)) return fail(ORC_ERR_CONFIG, "gamma must exceed 1");
   if (!(cfg->cfl > 0.0)) return fail(ORC_ERR_CONFIG, "cfl must be positive");
   if (cfg->max_level < 0 || cfg->max_level > 10) return fail(ORC_ERR_CONFIG, "max_level out of range");

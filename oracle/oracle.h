@@ -24,7 +24,7 @@ extern "C" {
 
 enum { ORC_OK = 0, ORC_ERR_INVALID_ARG = 1, ORC_ERR_CONFIG = 2, ORC_ERR_PHYSICS = 6, ORC_ERR_STATE = 7 };
 enum { ORC_BC_PERIODIC = 0, ORC_BC_OUTFLOW = 1, ORC_BC_REFLECT = 2 };
-enum { ORC_RECON_MINMOD = 0, ORC_RECON_VANLEER = 1, ORC_RECON_MC = 2 };
+enum { ORC_RECON_MINMOD = 0, ORC_RECON_VANLEER = 1, ORC_RECON_MC = 2, ORC_RECON_PPM = 3, ORC_RECON_WENOZ = 4 };
 enum { ORC_INT_RK2 = 0, ORC_INT_VL2 = 1 };
 enum { ORC_PROB_LINEAR_WAVE = 0, ORC_PROB_SOD = 1, ORC_PROB_BLAST = 2, ORC_PROB_KH = 3 };
 enum { ORC_REF_NONE = 0, ORC_REF_STATIC = 1, ORC_REF_ADAPTIVE = 2 };
@@ -32,7 +32,7 @@ enum { ORC_REF_NONE = 0, ORC_REF_STATIC = 1, ORC_REF_ADAPTIVE = 2 };
 typedef struct {
   int64_t mesh_nx[3];      /* root-grid cells per dim */
   int64_t block_nx[3];     /* cells per block per dim (must divide mesh_nx) */
-  int32_t nghost;          /* 2 */
+  int32_t nghost;          /* 2 (PLM) or 3 (PPM, WENO-Z; uniform meshes) */
   int32_t max_level;       /* levels above root */
   double xmin[3], xmax[3];
   int32_t bc_inner[3], bc_outer[3];
@@ -84,6 +84,8 @@ int orc_cons_to_prim(const double U[5], double gamma, double W[5]);
 void orc_prim_to_cons(const double W[5], double gamma, double U[5]);
 /* PLM on one component: returns the two face states of cell i: qR_{i-1/2}, qL_{i+1/2} */
 void orc_plm(double qm, double q0, double qp, int32_t recon, double* q_left_face, double* q_right_face);
+/* PPM (A37) / WENO-Z (A38) face values of cell q[2], q[0..4] = q_{i-2} .. q_{i+2} */
+void orc_recon5(const double q[5], int32_t recon, double* q_left_face, double* q_right_face);
 /* HLLE in the face-normal frame: W = (rho, u_normal, v_t1, v_t2, p) */
 void orc_hlle(const double WL[5], const double WR[5], double gamma, double F[5]);
 void orc_flux_phys(const double W[5], double gamma, double F[5]);
