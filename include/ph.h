@@ -54,14 +54,17 @@ typedef enum {
 } ph_status;
 
 typedef enum { PH_BC_PERIODIC = 0, PH_BC_OUTFLOW = 1, PH_BC_REFLECT = 2 } ph_bc;       /* A9 */
-typedef enum { PH_RECON_PLM_MINMOD = 0, PH_RECON_PLM_VANLEER = 1, PH_RECON_PLM_MC = 2 } ph_recon; /* A3 */
+typedef enum {
+  PH_RECON_PLM_MINMOD = 0, PH_RECON_PLM_VANLEER = 1, PH_RECON_PLM_MC = 2, /* A3; nghost 2 */
+  PH_RECON_PPM = 3, PH_RECON_WENOZ = 4                                   /* NEXT 3 (A37, A38); nghost 3 */
+} ph_recon;
 typedef enum { PH_INT_RK2 = 0, PH_INT_VL2 = 1 } ph_integrator;                      /* A1 */
 typedef enum { PH_PROB_LINEAR_WAVE = 0, PH_PROB_SOD = 1, PH_PROB_BLAST = 2, PH_PROB_KH = 3 } ph_problem;
 typedef enum { PH_REF_NONE = 0, PH_REF_STATIC = 1, PH_REF_ADAPTIVE = 2 } ph_refinement;
 
 typedef struct {
   int32_t abi_version;     /* must equal PH_ABI_VERSION, else PH_ERR_INVALID_ARG */
-  int32_t nghost;          /* ghost width; 2 (PLM needs 2, A8) */
+  int32_t nghost;          /* ghost width: 2 (PLM) or 3 (PPM / WENO-Z, uniform meshes only; A8, A39) */
   int64_t mesh_nx[3];      /* root-grid cells per dim */
   int64_t block_nx[3];     /* cells per MeshBlock per dim; must divide mesh_nx;
                               even and >= 2*nghost when max_level > 0 */

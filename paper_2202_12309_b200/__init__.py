@@ -5,5 +5,5 @@ Every step of the per-cycle update runs in the library's kernels; this package o
 marshals arguments and provides PyTorch plumbing (device allocator, stream, process group).
 There is no CPU fallback: if ``libph.so`` is missing the import fails loudly.
 """
-from .ph import Mesh, PhError, lib, PERIODIC, OUTFLOW, REFLECT, MINMOD, VANLEER, MC, RK2, VL2  # noqa: F401
+from .ph import Mesh, PhError, lib, PERIODIC, OUTFLOW, REFLECT, MINMOD, VANLEER, MC, PPM, WENOZ, RK2, VL2  # noqa: F401
 from .ph import LINEAR_WAVE, SOD, BLAST, KH, REF_NONE, REF_STATIC, REF_ADAPTIVE  # noqa: F401

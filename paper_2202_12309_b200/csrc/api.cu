@@ -101,6 +101,8 @@ struct ph_mesh {
   Plan plan[2];
   bool no_direct_halo = false;  // config: force materialised ghosts every exchange
   bool ghosts_stale = false;
+  bool ho = false;                      // nghost 3: generic high-order path (NEXT 3)
+  double *Wpool = nullptr, *Fxb = nullptr, *Fyb = nullptr, *Fzb = nullptr;
   bool overlap = false;                 // multi-GPU direct halo: interior blocks overlap the exchange
   int n_int = 0;                        // slots [0, n_int) of slot_order have no remote / physical face
   std::vector<int> slot_order;
@@ -435,7 +437,9 @@ static ph_status build_plan(ph_mesh* m) {
       if (fslot[b.gid][face] < 0) fslot[b.gid][face] = m->n_fslots++;
     }
   }
-  m->direct_halo = !m->multilevel && !m->no_direct_halo && m->cfg.refinement != PH_REF_ADAPTIVE;
+  m->ho = m->G.g == 3;
+  m->G.exact = m->ho ? 1 : 0;
+  m->direct_halo = !m->multilevel && !m->no_direct_halo && m->cfg.refinement != PH_REF_ADAPTIVE && !m->ho;
   build_exchange(m, m->plan[0], false, cslot);
   build_exchange(m, m->plan[1], m->direct_halo, cslot);
   // reflux tasks (coarse side) and, across ranks, the fine-side flux packs (O8).
@@ -593,6 +597,17 @@ static ph_status setup_device(ph_mesh* m) {
   m->nkc = (G.n[2] + m->KC - 1) / m->KC;
   m->pack_size = (m->cfg.pack_size > 0) ? (int)std::min<int64_t>(m->cfg.pack_size, nloc) : (int)nloc;
   m->stage_ctas = (int)(nloc * m->ntx * m->nty * m->nkc);
+  if (m->ho) {
+    // generic high-order path: primitives of the whole pool + face fluxes per direction
+    const int64_t nf[3] = {(int64_t)(G.n[0] + 1) * G.n[1] * G.n[2], (int64_t)G.n[0] * (G.n[1] + 1) * G.n[2],
+                           (int64_t)G.n[0] * G.n[1] * (G.n[2] + 1)};
+    const int64_t ns = std::max<int64_t>(nloc, 1);
+    TRY(dalloc(m, (void**)&m->Wpool, (size_t)ns * G.bstride * sizeof(double)));
+    TRY(dalloc(m, (void**)&m->Fxb, (size_t)ns * NVAR * nf[0] * sizeof(double)));
+    TRY(dalloc(m, (void**)&m->Fyb, (size_t)ns * NVAR * nf[1] * sizeof(double)));
+    TRY(dalloc(m, (void**)&m->Fzb, (size_t)ns * NVAR * nf[2] * sizeof(double)));
+    m->stage_ctas = (int)(nloc * G.n[2]);
+  }
   m->partials_n = std::max<int64_t>({(int64_t)m->stage_ctas, nloc * G.n[2], 1});
   TRY(dalloc(m, (void**)&m->partials, m->partials_n * 6 * sizeof(double)));
   CU(cudaMemsetAsync(m->partials, 0, m->partials_n * 6 * sizeof(double), m->stream));
@@ -723,7 +738,7 @@ static ph_status reduce_finalize(ph_mesh* m, int ncta, int mode) {
   m->launches++;
   if (m->nranks > 1)
     NC(ncclAllGather(m->my6, m->all6, 6, ncclDouble, m->comm2 ? m->comm2 : m->comm, m->stream));
-  CU(launch_finalize(m->all6, m->nranks, m->d_st, m->hist, m->hist_cap, m->G.cfl, mode, m->tot5, m->stream));
+  CU(launch_finalize(m->all6, m->nranks, m->d_st, m->hist, m->hist_cap, m->G.cfl, mode, m->tot5, m->G.exact, m->stream));
   m->launches++;
   return PH_OK;
 }
@@ -742,6 +757,34 @@ static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a
                            bool reduce, int stage, int s0 = 0, int s1 = -1, bool post = true) {
   const int nloc = (int)m->local_gids.size();
   if (s1 < 0) s1 = nloc;
+  if (m->ho) {
+    StageArgs A{};
+    A.Uin = Uin;
+    A.U0 = m->U0;
+    A.Uout = Uout;
+    A.meta = m->d_meta;
+    A.st = m->d_st;
+    A.partials = m->partials;
+    A.err = m->d_err;
+    A.a0 = a0;
+    A.b1 = b1;
+    A.cdt = cdt;
+    A.stage = stage;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (m->timing) {
+      t0 = pool_event(m);
+      t1 = pool_event(m);
+      CU(cudaEventRecord(t0, m->stream));
+    }
+    CU(launch_highorder_stage(m->cfg.recon, reduce, a0 != 0.0, nloc, A, m->Wpool, m->Fxb, m->Fyb, m->Fzb, m->G,
+                              m->stream));
+    m->launches += 5;
+    if (m->timing) {
+      CU(cudaEventRecord(t1, m->stream));
+      m->t_stage.push_back({t0, t1});
+    }
+    return PH_OK;
+  }
   const int per_blk = m->ntx * m->nty * m->nkc;
   for (int p0 = s0; p0 < s1; p0 += m->pack_size) {
     int np = std::min(m->pack_size, s1 - p0);
@@ -1100,11 +1143,14 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
   if (!cfg || !out) return fail(PH_ERR_INVALID_ARG, "null argument");
   *out = nullptr;
   if (cfg->abi_version != PH_ABI_VERSION) return fail(PH_ERR_INVALID_ARG, "abi_version mismatch");
-  if (cfg->nghost != 2) return fail(PH_ERR_CONFIG, "nghost must be 2 (PLM, A8)");
+  if (cfg->nghost != 2 && cfg->nghost != 3) return fail(PH_ERR_CONFIG, "nghost must be 2 (PLM) or 3 (PPM, WENO-Z; A8)");
+  if (cfg->recon >= PH_RECON_PPM && cfg->nghost != 3) return fail(PH_ERR_CONFIG, "PPM / WENO-Z need nghost = 3 (A8)");
+  if (cfg->nghost == 3 && cfg->max_level > 0 && cfg->refinement != PH_REF_NONE)
+    return fail(PH_ERR_CONFIG, "nghost = 3 is supported on uniform meshes only (reading A39)");
   if (!(cfg->gamma > 1.0) || !(cfg->cfl > 0.0)) return fail(PH_ERR_CONFIG, "gamma must exceed 1 and cfl be positive");
   if (cfg->nranks < 1 || cfg->nranks > 64 || cfg->rank < 0 || cfg->rank >= cfg->nranks)
     return fail(PH_ERR_INVALID_ARG, "bad rank / nranks");
-  if (cfg->recon < 0 || cfg->recon > 2 || cfg->integrator < 0 || cfg->integrator > 1)
+  if (cfg->recon < 0 || cfg->recon > 4 || cfg->integrator < 0 || cfg->integrator > 1)
     return fail(PH_ERR_CONFIG, "unknown recon / integrator");
   if (cfg->max_level < 0 || cfg->max_level > 10) return fail(PH_ERR_CONFIG, "max_level out of range");
   MeshCfg mc{};
@@ -1550,7 +1596,7 @@ ph_status ph_totals(ph_mesh* m, double out[5]) {
   CU(launch_rank_reduce(m->partials, nloc * m->G.n[2], m->nranks > 1 ? m->my6 : m->all6, m->stream));
   m->launches++;
   if (m->nranks > 1) NC(ncclAllGather(m->my6, m->all6, 6, ncclDouble, m->comm, m->stream));
-  CU(launch_finalize(m->all6, m->nranks, m->d_st, m->hist, m->hist_cap, m->G.cfl, 2, m->tot5, m->stream));
+  CU(launch_finalize(m->all6, m->nranks, m->d_st, m->hist, m->hist_cap, m->G.cfl, 2, m->tot5, m->G.exact, m->stream));
   m->launches++;
   TRY(check_err(m));
   CU(cudaMemcpy(out, m->tot5, 5 * sizeof(double), cudaMemcpyDeviceToHost));

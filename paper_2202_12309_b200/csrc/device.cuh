@@ -23,6 +23,7 @@ struct Geom {
   int64_t fstride; // doubles per face-flux slot (5 * max face cells)
   double gamma, gm1, inv_gm1;
   double cfl;
+  int exact;       // 1: high-order path computes in the oracle's exact operation order (NEXT 3)
 };
 
 // Per local block slot.
@@ -165,13 +166,15 @@ cudaError_t launch_reduce(const double* U, const BlockMeta* meta, int nslots, do
                           const Geom& G, cudaStream_t s);
 cudaError_t launch_rank_reduce(const double* partials, int n, double* out, cudaStream_t s);
 cudaError_t launch_finalize(const double* all, int nranks, CycleState* st, double* hist, int hist_cap, double cfl,
-                            int mode, double* tot_out, cudaStream_t s);
+                            int mode, double* tot_out, int exact, cudaStream_t s);
 cudaError_t launch_cycle_begin(CycleState* st, double tlim, int set_tlim, cudaStream_t s);
 cudaError_t launch_interior_copy(double* U, double* buf, int slot0, int nslots, int to_pool, const Geom& G,
                                  cudaStream_t s);
 cudaError_t launch_tag(const double* U, int nslots, unsigned long long* eps_bits, const Geom& G, cudaStream_t s);
 cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, double* Unew, const double* rbuf,
                           double* sbuf, const Geom& G, cudaStream_t s);
+cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslots, const StageArgs& a, double* W,
+                                   double* Fx, double* Fy, double* Fz, const Geom& G, cudaStream_t s);
 size_t stage_smem_bytes();
 
 }  // namespace ph

@@ -101,6 +101,142 @@ __device__ __forceinline__ void set_error(ErrWord* err, int stage, long long gid
   }
 }
 
+// ---- exact-arithmetic variants (explicitly rounded, the oracle's operation order).  WENO-Z's
+// nonlinear weights and PPM's extremum switch amplify round-off (a smoothness indicator that is 0
+// on one side and 1e-33 on the other changes a weight by 40 orders of magnitude), so the
+// high-order path computes bit for bit what the oracle computes: parity is then exact.
+__device__ __forceinline__ double slope_rn(double qm, double q0, double qp, int recon) {
+  const double dl = __dsub_rn(q0, qm), dr = __dsub_rn(qp, q0);
+  const bool same = (dl > 0.0 && dr > 0.0) || (dl < 0.0 && dr < 0.0);
+  if (!same) return 0.0;
+  if (recon == 1) return __ddiv_rn(__dmul_rn(__dmul_rn(2.0, dl), dr), __dadd_rn(dl, dr));
+  if (recon == 2) {
+    const double s = dl > 0.0 ? 1.0 : -1.0;
+    double m = __dmul_rn(2.0, fabs(dl)), b = __dmul_rn(2.0, fabs(dr)), c = __dmul_rn(0.5, fabs(__dadd_rn(dl, dr)));
+    m = m < b ? m : b;
+    m = m < c ? m : c;
+    return __dmul_rn(s, m);
+  }
+  if (dl > 0.0) return dl < dr ? dl : dr;
+  return dl > dr ? dl : dr;
+}
+
+__device__ __forceinline__ double ppm_dm_rn(double a, double b, double c) {
+  const double dl = __dsub_rn(b, a), dr = __dsub_rn(c, b);
+  const bool same = (dl > 0.0 && dr > 0.0) || (dl < 0.0 && dr < 0.0);
+  if (!same) return 0.0;
+  const double dq = __dmul_rn(0.5, __dsub_rn(c, a));
+  double m = fabs(dq);
+  if (__dmul_rn(2.0, fabs(dl)) < m) m = __dmul_rn(2.0, fabs(dl));
+  if (__dmul_rn(2.0, fabs(dr)) < m) m = __dmul_rn(2.0, fabs(dr));
+  return dq > 0.0 ? m : -m;
+}
+
+__device__ __forceinline__ void ppm_cell_rn(const double* q, double& ql, double& qr) {
+  const double dm_m = ppm_dm_rn(q[0], q[1], q[2]), dm_0 = ppm_dm_rn(q[1], q[2], q[3]), dm_p = ppm_dm_rn(q[2], q[3], q[4]);
+  double L = __dsub_rn(__dadd_rn(q[1], __dmul_rn(0.5, __dsub_rn(q[2], q[1]))), __ddiv_rn(__dsub_rn(dm_0, dm_m), 6.0));
+  double R = __dsub_rn(__dadd_rn(q[2], __dmul_rn(0.5, __dsub_rn(q[3], q[2]))), __ddiv_rn(__dsub_rn(dm_p, dm_0), 6.0));
+  const double c = q[2];
+  if (__dmul_rn(__dsub_rn(R, c), __dsub_rn(c, L)) <= 0.0) {
+    L = c;
+    R = c;
+  } else {
+    const double d = __dsub_rn(R, L), m6 = __dmul_rn(6.0, __dsub_rn(c, __dmul_rn(0.5, __dadd_rn(L, R))));
+    const double dd = __dmul_rn(d, d), dm6 = __dmul_rn(d, m6);
+    if (dm6 > dd) L = __dsub_rn(__dmul_rn(3.0, c), __dmul_rn(2.0, R));
+    else if (-dd > dm6) R = __dsub_rn(__dmul_rn(3.0, c), __dmul_rn(2.0, L));
+  }
+  ql = L;
+  qr = R;
+}
+
+__device__ __forceinline__ double wenoz_rn(double a, double b, double c, double d, double e) {
+  const double t0 = __dadd_rn(__dsub_rn(a, __dmul_rn(2.0, b)), c), u0 = __dadd_rn(__dsub_rn(a, __dmul_rn(4.0, b)), __dmul_rn(3.0, c));
+  const double t1 = __dadd_rn(__dsub_rn(b, __dmul_rn(2.0, c)), d), u1 = __dsub_rn(b, d);
+  const double t2 = __dadd_rn(__dsub_rn(c, __dmul_rn(2.0, d)), e), u2 = __dadd_rn(__dsub_rn(__dmul_rn(3.0, c), __dmul_rn(4.0, d)), e);
+  const double k13 = 13.0 / 12.0;
+  const double b0 = __dadd_rn(__dmul_rn(k13, __dmul_rn(t0, t0)), __dmul_rn(0.25, __dmul_rn(u0, u0)));
+  const double b1 = __dadd_rn(__dmul_rn(k13, __dmul_rn(t1, t1)), __dmul_rn(0.25, __dmul_rn(u1, u1)));
+  const double b2 = __dadd_rn(__dmul_rn(k13, __dmul_rn(t2, t2)), __dmul_rn(0.25, __dmul_rn(u2, u2)));
+  const double tau = fabs(__dsub_rn(b0, b2));
+  const double r0 = __ddiv_rn(tau, __dadd_rn(b0, 1e-40)), r1 = __ddiv_rn(tau, __dadd_rn(b1, 1e-40)),
+               r2 = __ddiv_rn(tau, __dadd_rn(b2, 1e-40));
+  const double a0 = __dmul_rn(0.1, __dadd_rn(1.0, __dmul_rn(r0, r0)));
+  const double a1 = __dmul_rn(0.6, __dadd_rn(1.0, __dmul_rn(r1, r1)));
+  const double a2 = __dmul_rn(0.3, __dadd_rn(1.0, __dmul_rn(r2, r2)));
+  const double q0 = __ddiv_rn(__dadd_rn(__dsub_rn(__dmul_rn(2.0, a), __dmul_rn(7.0, b)), __dmul_rn(11.0, c)), 6.0);
+  const double q1 = __ddiv_rn(__dadd_rn(__dadd_rn(-b, __dmul_rn(5.0, c)), __dmul_rn(2.0, d)), 6.0);
+  const double q2 = __ddiv_rn(__dsub_rn(__dadd_rn(__dmul_rn(2.0, c), __dmul_rn(5.0, d)), e), 6.0);
+  return __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(a0, q0), __dmul_rn(a1, q1)), __dmul_rn(a2, q2)),
+                   __dadd_rn(__dadd_rn(a0, a1), a2));
+}
+
+template <int RECON>
+__device__ __forceinline__ void recon_face6_rn(const double* q, double& wl, double& wr) {
+  if (RECON == 3) {
+    double a, b;
+    ppm_cell_rn(q, a, wl);
+    ppm_cell_rn(q + 1, wr, b);
+  } else if (RECON == 4) {
+    wl = wenoz_rn(q[0], q[1], q[2], q[3], q[4]);
+    wr = wenoz_rn(q[5], q[4], q[3], q[2], q[1]);
+  } else {
+    wl = __dadd_rn(q[2], __dmul_rn(0.5, slope_rn(q[1], q[2], q[3], RECON)));
+    wr = __dsub_rn(q[3], __dmul_rn(0.5, slope_rn(q[2], q[3], q[4], RECON)));
+  }
+}
+
+__device__ __forceinline__ void phys_rn(const double* W, double gm1, double* U, double* F) {
+  const double rho = W[0], u = W[1], v = W[2], w = W[3], p = W[4];
+  const double mu = __dmul_rn(rho, u);
+  const double E = __dadd_rn(__ddiv_rn(p, gm1), __dmul_rn(__dmul_rn(0.5, rho),
+                                                         __dadd_rn(__dmul_rn(u, u), __dadd_rn(__dmul_rn(v, v), __dmul_rn(w, w)))));
+  U[0] = rho; U[1] = mu; U[2] = __dmul_rn(rho, v); U[3] = __dmul_rn(rho, w); U[4] = E;
+  F[0] = mu; F[1] = __dadd_rn(__dmul_rn(mu, u), p); F[2] = __dmul_rn(mu, v); F[3] = __dmul_rn(mu, w);
+  F[4] = __dmul_rn(__dadd_rn(E, p), u);
+}
+
+__device__ __forceinline__ void hlle_rn(const double* WL, const double* WR, const Geom& G, double* F) {
+  const double cl = __dsqrt_rn(__ddiv_rn(__dmul_rn(G.gamma, WL[4]), WL[0]));
+  const double cr = __dsqrt_rn(__ddiv_rn(__dmul_rn(G.gamma, WR[4]), WR[0]));
+  double a = __dsub_rn(WL[1], cl), b = __dsub_rn(WR[1], cr);
+  const double sl = a < b ? a : b;
+  a = __dadd_rn(WL[1], cl);
+  b = __dadd_rn(WR[1], cr);
+  const double sr = a > b ? a : b;
+  const double bp = sr > 0.0 ? sr : 0.0, bm = sl < 0.0 ? sl : 0.0;
+  double UL[NVAR], FL[NVAR], UR[NVAR], FR[NVAR];
+  phys_rn(WL, G.gm1, UL, FL);
+  phys_rn(WR, G.gm1, UR, FR);
+  const double inv = __ddiv_rn(1.0, __dsub_rn(bp, bm));
+  const double bb = __dmul_rn(bp, bm);
+#pragma unroll
+  for (int n = 0; n < NVAR; ++n)
+    F[n] = __dmul_rn(__dadd_rn(__dsub_rn(__dmul_rn(bp, FL[n]), __dmul_rn(bm, FR[n])), __dmul_rn(bb, __dsub_rn(UR[n], UL[n]))), inv);
+}
+
+// exact cons -> prim (oracle order); returns false if rho <= 0 or p <= 0
+__device__ __forceinline__ bool cons2prim_rn(double rho, double m1, double m2, double m3, double E, double gm1,
+                                             double* W) {
+  const double ir = __ddiv_rn(1.0, rho);
+  const double v1 = __dmul_rn(m1, ir), v2 = __dmul_rn(m2, ir), v3 = __dmul_rn(m3, ir);
+  const double ke = __dmul_rn(0.5, __dadd_rn(__dadd_rn(__dmul_rn(m1, v1), __dmul_rn(m2, v2)), __dmul_rn(m3, v3)));
+  const double p = __dmul_rn(gm1, __dsub_rn(E, ke));
+  W[0] = rho; W[1] = v1; W[2] = v2; W[3] = v3; W[4] = p;
+  return (rho > 0.0) && (p > 0.0);
+}
+
+// exact per-cell CFL term (O6): min_d dx_d / (|v_d| + sqrt(gamma p / rho))
+__device__ __forceinline__ double cfl_term_rn(const double* W, const BlockMeta& M, double gamma) {
+  const double c = __dsqrt_rn(__ddiv_rn(__dmul_rn(gamma, W[4]), W[0]));
+  double r = __ddiv_rn(M.dx[0], __dadd_rn(fabs(W[1]), c));
+  const double r2 = __ddiv_rn(M.dx[1], __dadd_rn(fabs(W[2]), c));
+  const double r3 = __ddiv_rn(M.dx[2], __dadd_rn(fabs(W[3]), c));
+  r = r2 < r ? r2 : r;
+  return r3 < r ? r3 : r;
+}
+
+
 // ------------------------------------------------------------------------------ stage kernel
 // One CTA = a TX x TY tile of (i,j) columns of one block, marching up a k-range of KC planes.
 // Plane q is converted to primitives (a2) into slot q%4 of a 4-plane smem ring (plus-shaped
@@ -735,7 +871,7 @@ __global__ void reduce_kernel(const double* U, const BlockMeta* meta, int nslots
   const int row = blockIdx.x;  // (slot, k)
   const int k = row % G.n[2];
   const int slot = row / G.n[2];
-  double tmax = 0.0, ts[NVAR] = {0, 0, 0, 0, 0};
+  double tmax = -INFINITY, ts[NVAR] = {0, 0, 0, 0, 0};
   if (slot < nslots) {
     const BlockMeta& M = meta[slot];
     const int nij = G.n[0] * G.n[1];
@@ -745,14 +881,20 @@ __global__ void reduce_kernel(const double* U, const BlockMeta* meta, int nslots
       double un[NVAR];
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) un[v] = u[v * G.vstride];
-      double ir = rcp_nr(un[0]);
-      double v1 = un[1] * ir, v2 = un[2] * ir, v3 = un[3] * ir;
-      double ke = 0.5 * ((un[1] * v1 + un[2] * v2) + un[3] * v3);
-      double p = G.gm1 * (un[4] - ke);
-      if (!(un[0] > 0.0) || !(p > 0.0)) set_error(err, 0, M.gid, k, j, i);
-      double cs = sound_speed(un[0], p, G.gamma);
-      double s1 = (fabs(v1) + cs) * M.idx[0], s2 = (fabs(v2) + cs) * M.idx[1], s3 = (fabs(v3) + cs) * M.idx[2];
-      tmax = fmax(tmax, fmax(s1, fmax(s2, s3)));
+      if (G.exact) {
+        double Wn[NVAR];
+        if (!cons2prim_rn(un[0], un[1], un[2], un[3], un[4], G.gm1, Wn)) set_error(err, 0, M.gid, k, j, i);
+        tmax = fmax(tmax, -cfl_term_rn(Wn, M, G.gamma));
+      } else {
+        double ir = rcp_nr(un[0]);
+        double v1 = un[1] * ir, v2 = un[2] * ir, v3 = un[3] * ir;
+        double ke = 0.5 * ((un[1] * v1 + un[2] * v2) + un[3] * v3);
+        double p = G.gm1 * (un[4] - ke);
+        if (!(un[0] > 0.0) || !(p > 0.0)) set_error(err, 0, M.gid, k, j, i);
+        double cs = sound_speed(un[0], p, G.gamma);
+        double s1 = (fabs(v1) + cs) * M.idx[0], s2 = (fabs(v2) + cs) * M.idx[1], s3 = (fabs(v3) + cs) * M.idx[2];
+        tmax = fmax(tmax, fmax(s1, fmax(s2, s3)));
+      }
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) ts[v] += un[v];
     }
@@ -770,7 +912,7 @@ __global__ void reduce_kernel(const double* U, const BlockMeta* meta, int nslots
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    double m = 0.0, s[NVAR] = {0, 0, 0, 0, 0};
+    double m = -INFINITY, s[NVAR] = {0, 0, 0, 0, 0};
     for (int w = 0; w < (int)blockDim.x / 32; ++w) {
       m = fmax(m, red[w][0]);
       for (int v = 0; v < NVAR; ++v) s[v] += red[w][1 + v];
@@ -785,7 +927,7 @@ __global__ void reduce_kernel(const double* U, const BlockMeta* meta, int nslots
 // partials [n][6] -> out[6] (max, 5 sums), deterministic for fixed n
 __global__ void rank_reduce_kernel(const double* partials, int n, double* out) {
   __shared__ double sm[256][6];
-  double m = 0.0, s[NVAR] = {0, 0, 0, 0, 0};
+  double m = -INFINITY, s[NVAR] = {0, 0, 0, 0, 0};
   for (int c = threadIdx.x; c < n; c += 256) {
     const double* p = partials + (int64_t)c * 6;
     m = fmax(m, p[0]);
@@ -807,8 +949,8 @@ __global__ void rank_reduce_kernel(const double* partials, int n, double* out) {
 
 // mode 0: initial dt (no history); mode 1: end of cycle; mode 2: totals only (out6 -> tot)
 __global__ void finalize_kernel(const double* all, int nranks, CycleState* st, double* hist, int hist_cap,
-                                double cfl, int mode, double* tot_out) {
-  double m = 0.0, s[NVAR] = {0, 0, 0, 0, 0};
+                                double cfl, int mode, double* tot_out, int exact) {
+  double m = -INFINITY, s[NVAR] = {0, 0, 0, 0, 0};
   for (int r = 0; r < nranks; ++r) {
     m = fmax(m, all[r * 6]);
     for (int v = 0; v < NVAR; ++v) s[v] += all[r * 6 + 1 + v];
@@ -816,7 +958,8 @@ __global__ void finalize_kernel(const double* all, int nranks, CycleState* st, d
   if (tot_out)
     for (int v = 0; v < NVAR; ++v) tot_out[v] = s[v];
   if (mode == 2) return;
-  double dt_new = cfl / m;  // cfl * min(dx/(|v|+c)) (O6)
+  // cfl * min(dx/(|v|+c)) (O6); exact mode carries -min(dx/(|v|+c)) itself
+  double dt_new = exact ? __dmul_rn(cfl, -m) : cfl / m;
   if (mode == 0) {
     st->dt = dt_new;
     return;
@@ -856,6 +999,193 @@ __global__ void interior_copy_kernel(double* U, double* buf, int slot0, int to_p
   for (int i = threadIdx.x; i < G.n[0]; i += blockDim.x) {
     if (to_pool) u[i] = b[i];
     else b[i] = u[i];
+  }
+}
+
+// ------------------------------------------------------------------------------ NEXT 3: PPM / WENO-Z
+// Generic high-order path (nghost = 3, uniform meshes): primitives of every pool cell, one face-flux
+// kernel per direction (6-point stencils), then divergence + RK update.  Formulas as the oracle's
+// readings A37 (PPM, Colella & Woodward 1984 eqs. 1.6-1.10) and A38 (WENO-Z, Borges et al. 2008).
+__device__ __forceinline__ double ppm_dm(double a, double b, double c) {
+  const double dl = b - a, dr = c - b;
+  const bool same = (dl > 0.0 && dr > 0.0) || (dl < 0.0 && dr < 0.0);
+  if (!same) return 0.0;
+  const double dq = 0.5 * (c - a);
+  const double m = fmin(fabs(dq), fmin(2.0 * fabs(dl), 2.0 * fabs(dr)));
+  return dq > 0.0 ? m : -m;
+}
+
+__device__ __forceinline__ void ppm_cell(const double* q, double& ql, double& qr) {
+  const double dm_m = ppm_dm(q[0], q[1], q[2]), dm_0 = ppm_dm(q[1], q[2], q[3]), dm_p = ppm_dm(q[2], q[3], q[4]);
+  double L = q[1] + 0.5 * (q[2] - q[1]) - (dm_0 - dm_m) / 6.0;
+  double R = q[2] + 0.5 * (q[3] - q[2]) - (dm_p - dm_0) / 6.0;
+  const double c = q[2];
+  if ((R - c) * (c - L) <= 0.0) {
+    L = c;
+    R = c;
+  } else {
+    const double d = R - L, m6 = 6.0 * (c - 0.5 * (L + R));
+    if (d * m6 > d * d) L = 3.0 * c - 2.0 * R;
+    else if (-(d * d) > d * m6) R = 3.0 * c - 2.0 * L;
+  }
+  ql = L;
+  qr = R;
+}
+
+__device__ __forceinline__ double wenoz_face(double a, double b, double c, double d, double e) {
+  const double t0 = a - 2.0 * b + c, u0 = a - 4.0 * b + 3.0 * c;
+  const double t1 = b - 2.0 * c + d, u1 = b - d;
+  const double t2 = c - 2.0 * d + e, u2 = 3.0 * c - 4.0 * d + e;
+  const double b0 = (13.0 / 12.0) * (t0 * t0) + 0.25 * (u0 * u0);
+  const double b1 = (13.0 / 12.0) * (t1 * t1) + 0.25 * (u1 * u1);
+  const double b2 = (13.0 / 12.0) * (t2 * t2) + 0.25 * (u2 * u2);
+  const double tau = fabs(b0 - b2);
+  const double r0 = tau / (b0 + 1e-40), r1 = tau / (b1 + 1e-40), r2 = tau / (b2 + 1e-40);
+  const double a0 = 0.1 * (1.0 + r0 * r0), a1 = 0.6 * (1.0 + r1 * r1), a2 = 0.3 * (1.0 + r2 * r2);
+  const double q0 = (2.0 * a - 7.0 * b + 11.0 * c) / 6.0;
+  const double q1 = (-b + 5.0 * c + 2.0 * d) / 6.0;
+  const double q2 = (2.0 * c + 5.0 * d - e) / 6.0;
+  return ((a0 * q0 + a1 * q1) + a2 * q2) / ((a0 + a1) + a2);
+}
+
+template <int RECON>
+__device__ __forceinline__ void recon_face6(const double* q, double& wl, double& wr) {
+  // q[0..5] = cells c-3 .. c+2 of the face between c-1 and c
+  if (RECON == 3) {
+    double a, b;
+    ppm_cell(q, a, wl);
+    ppm_cell(q + 1, wr, b);
+  } else if (RECON == 4) {
+    wl = wenoz_face(q[0], q[1], q[2], q[3], q[4]);
+    wr = wenoz_face(q[5], q[4], q[3], q[2], q[1]);
+  } else {
+    plm_face<RECON>(q[1], q[2], q[3], q[4], wl, wr);
+  }
+}
+
+__global__ void prim_kernel(const double* U, double* W, const BlockMeta* meta, ErrWord* err, int stage, Geom G) {
+  const int kk = blockIdx.x % G.N[2];
+  const int slot = blockIdx.x / G.N[2];
+  const double* u = U + (int64_t)slot * G.bstride + (int64_t)kk * G.N[0] * G.N[1];
+  double* w = W + (int64_t)slot * G.bstride + (int64_t)kk * G.N[0] * G.N[1];
+  const int k = kk - G.g;
+  for (int c = threadIdx.x; c < G.N[0] * G.N[1]; c += blockDim.x) {
+    const int j = c / G.N[0] - G.g, i = c % G.N[0] - G.g;
+    const int out = (k < 0 || k >= G.n[2]) + (j < 0 || j >= G.n[1]) + (i < 0 || i >= G.n[0]);
+    if (out > 1) continue;  // only the cross-shaped halo is ever read
+    double Wc[NVAR];
+    if (!cons2prim_rn(u[c], u[c + G.vstride], u[c + 2 * G.vstride], u[c + 3 * G.vstride], u[c + 4 * G.vstride], G.gm1, Wc))
+      set_error(err, stage, meta[slot].gid, k, j, i);
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) w[c + v * G.vstride] = Wc[v];
+  }
+}
+
+template <int DIR, int RECON>
+__global__ void hoflux_kernel(const double* W, double* F, Geom G) {
+  const int e0 = G.n[0] + (DIR == 0), e1 = G.n[1] + (DIR == 1), e2 = G.n[2] + (DIR == 2);
+  const int k = blockIdx.x % e2;
+  const int slot = blockIdx.x / e2;
+  const int64_t st = (DIR == 0) ? 1 : ((DIR == 1) ? G.N[0] : (int64_t)G.N[0] * G.N[1]);
+  constexpr int CN = 1 + DIR, C1 = 1 + (DIR + 1) % 3, C2 = 1 + (DIR + 2) % 3;
+  const int64_t fvs = (int64_t)e0 * e1 * e2;
+  double* fb = F + (int64_t)slot * NVAR * fvs + (int64_t)k * e0 * e1;
+  const double* wb = W + (int64_t)slot * G.bstride;
+  for (int c = threadIdx.x; c < e0 * e1; c += blockDim.x) {
+    const int j = c / e0, i = c % e0;
+    const double* p = wb + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+    double wl[NVAR], wr[NVAR];
+    const int cv[NVAR] = {0, CN, C1, C2, 4};
+#pragma unroll
+    for (int s = 0; s < NVAR; ++s) {
+      const double* q0 = p + cv[s] * G.vstride;
+      double q[6];
+#pragma unroll
+      for (int t = 0; t < 6; ++t) q[t] = q0[(t - 3) * st];
+      recon_face6_rn<RECON>(q, wl[s], wr[s]);
+    }
+    double Fn[NVAR];
+    hlle_rn(wl, wr, G, Fn);
+    double Fo[NVAR];
+    Fo[0] = Fn[0];
+    Fo[CN] = Fn[1];
+    Fo[C1] = Fn[2];
+    Fo[C2] = Fn[3];
+    Fo[4] = Fn[4];
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) fb[v * fvs + c] = Fo[v];
+  }
+}
+
+template <bool REDUCE, bool USE_U0>
+__global__ void houpdate_kernel(StageArgs A, const double* Fx, const double* Fy, const double* Fz, Geom G) {
+  const int k = blockIdx.x % G.n[2];
+  const int slot = blockIdx.x / G.n[2];
+  const BlockMeta& M = A.meta[slot];
+  const double dt = A.st->dt_used;
+  const int64_t fx = (int64_t)(G.n[0] + 1) * G.n[1] * G.n[2], fy = (int64_t)G.n[0] * (G.n[1] + 1) * G.n[2],
+                fz = (int64_t)G.n[0] * G.n[1] * (G.n[2] + 1);
+  double tmax = -INFINITY, ts[NVAR] = {0, 0, 0, 0, 0};
+  for (int c = threadIdx.x; c < G.n[0] * G.n[1]; c += blockDim.x) {
+    const int j = c / G.n[0], i = c % G.n[0];
+    const int64_t cell = (int64_t)slot * G.bstride + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+    const int64_t ix = ((int64_t)k * G.n[1] + j) * (G.n[0] + 1) + i;
+    const int64_t iy = ((int64_t)k * (G.n[1] + 1) + j) * G.n[0] + i;
+    const int64_t iz = ((int64_t)k * G.n[1] + j) * G.n[0] + i;
+    double un[NVAR];
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) {
+      const double* px = Fx + (int64_t)slot * NVAR * fx + v * fx + ix;
+      const double* py = Fy + (int64_t)slot * NVAR * fy + v * fy + iy;
+      const double* pz = Fz + (int64_t)slot * NVAR * fz + v * fz + iz;
+      const double d1 = __ddiv_rn(__dsub_rn(px[1], px[0]), M.dx[0]);
+      const double d2 = __ddiv_rn(__dsub_rn(py[G.n[0]], py[0]), M.dx[1]);
+      const double d3 = __ddiv_rn(__dsub_rn(pz[(int64_t)G.n[0] * G.n[1]], pz[0]), M.dx[2]);
+      const double L = -__dadd_rn(__dadd_rn(d1, d2), d3);
+      const double dtw = __dmul_rn(A.cdt, dt);
+      const double uin = A.Uin[cell + v * G.vstride];
+      double out;
+      if (USE_U0 && A.b1 != 0.0)  // RK2 stage 2: 0.5 U0 + 0.5 (U1 + dt L)
+        out = __dadd_rn(__dmul_rn(0.5, A.U0[cell + v * G.vstride]), __dmul_rn(0.5, __dadd_rn(uin, __dmul_rn(dt, L))));
+      else if (USE_U0)            // VL2 stage 2: U0 + dt L
+        out = __dadd_rn(A.U0[cell + v * G.vstride], __dmul_rn(dtw, L));
+      else                        // stage 1: U0 + w dt L
+        out = __dadd_rn(uin, __dmul_rn(dtw, L));
+      un[v] = out;
+      A.Uout[cell + v * G.vstride] = out;
+    }
+    if (REDUCE) {
+      // exact CFL term, kept as -min(...) in the 'max' slot (finalize: dt = cfl * (-m), G.exact)
+      double Wn[NVAR];
+      cons2prim_rn(un[0], un[1], un[2], un[3], un[4], G.gm1, Wn);
+      tmax = fmax(tmax, -cfl_term_rn(Wn, M, G.gamma));
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) ts[v] += un[v];
+    }
+  }
+  if (REDUCE) {
+    __shared__ double red[32][6];
+    for (int off = 16; off > 0; off >>= 1) {
+      tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) ts[v] += __shfl_xor_sync(0xffffffffu, ts[v], off);
+    }
+    const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+    if (lane == 0) {
+      red[warp][0] = tmax;
+      for (int v = 0; v < NVAR; ++v) red[warp][1 + v] = ts[v];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double m = -INFINITY, s[NVAR] = {0, 0, 0, 0, 0};
+      for (int w = 0; w < (int)blockDim.x / 32; ++w) {
+        m = fmax(m, red[w][0]);
+        for (int v = 0; v < NVAR; ++v) s[v] += red[w][1 + v];
+      }
+      double* o = A.partials + (int64_t)(A.cta_base + blockIdx.x) * 6;
+      o[0] = m;
+      for (int v = 0; v < NVAR; ++v) o[1 + v] = s[v] * M.dV;
+    }
   }
 }
 
@@ -1042,8 +1372,8 @@ cudaError_t launch_rank_reduce(const double* partials, int n, double* out, cudaS
 }
 
 cudaError_t launch_finalize(const double* all, int nranks, CycleState* st, double* hist, int hist_cap, double cfl,
-                            int mode, double* tot_out, cudaStream_t s) {
-  finalize_kernel<<<1, 1, 0, s>>>(all, nranks, st, hist, hist_cap, cfl, mode, tot_out);
+                            int mode, double* tot_out, int exact, cudaStream_t s) {
+  finalize_kernel<<<1, 1, 0, s>>>(all, nranks, st, hist, hist_cap, cfl, mode, tot_out, exact);
   return PH_CHECK_LAUNCH();
 }
 
@@ -1057,6 +1387,39 @@ cudaError_t launch_interior_copy(double* U, double* buf, int slot0, int nslots, 
   if (nslots <= 0) return cudaSuccess;
   interior_copy_kernel<<<nslots * NVAR * G.n[2] * G.n[1], 128, 0, s>>>(U, buf, slot0, to_pool, G);
   return PH_CHECK_LAUNCH();
+}
+
+template <int R>
+static cudaError_t launch_hoflux_r(const double* W, double* Fx, double* Fy, double* Fz, int nslots, const Geom& G,
+                                   cudaStream_t s) {
+  hoflux_kernel<0, R><<<nslots * G.n[2], 128, 0, s>>>(W, Fx, G);
+  hoflux_kernel<1, R><<<nslots * G.n[2], 128, 0, s>>>(W, Fy, G);
+  hoflux_kernel<2, R><<<nslots * (G.n[2] + 1), 128, 0, s>>>(W, Fz, G);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslots, const StageArgs& a, double* W,
+                                   double* Fx, double* Fy, double* Fz, const Geom& G, cudaStream_t s) {
+  if (nslots <= 0) return cudaSuccess;
+  prim_kernel<<<nslots * G.N[2], 256, 0, s>>>(a.Uin, W, a.meta, a.err, a.stage, G);
+  cudaError_t e;
+  switch (recon) {
+    case 0: e = launch_hoflux_r<0>(W, Fx, Fy, Fz, nslots, G, s); break;
+    case 1: e = launch_hoflux_r<1>(W, Fx, Fy, Fz, nslots, G, s); break;
+    case 2: e = launch_hoflux_r<2>(W, Fx, Fy, Fz, nslots, G, s); break;
+    case 3: e = launch_hoflux_r<3>(W, Fx, Fy, Fz, nslots, G, s); break;
+    default: e = launch_hoflux_r<4>(W, Fx, Fy, Fz, nslots, G, s); break;
+  }
+  if (e != cudaSuccess) return e;
+  const int grid = nslots * G.n[2];
+  if (reduce) {
+    if (use_u0) houpdate_kernel<true, true><<<grid, 256, 0, s>>>(a, Fx, Fy, Fz, G);
+    else houpdate_kernel<true, false><<<grid, 256, 0, s>>>(a, Fx, Fy, Fz, G);
+  } else {
+    if (use_u0) houpdate_kernel<false, true><<<grid, 256, 0, s>>>(a, Fx, Fy, Fz, G);
+    else houpdate_kernel<false, false><<<grid, 256, 0, s>>>(a, Fx, Fy, Fz, G);
+  }
+  return cudaGetLastError();
 }
 
 cudaError_t launch_tag(const double* U, int nslots, unsigned long long* eps_bits, const Geom& G, cudaStream_t s) {

@@ -14,7 +14,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIBPATH = os.environ.get("PH_LIB") or os.path.join(_HERE, "libph.so")  # PH_LIB: A/B builds
 
 PERIODIC, OUTFLOW, REFLECT = 0, 1, 2
-MINMOD, VANLEER, MC = 0, 1, 2
+MINMOD, VANLEER, MC, PPM, WENOZ = 0, 1, 2, 3, 4
 RK2, VL2 = 0, 1
 LINEAR_WAVE, SOD, BLAST, KH = 0, 1, 2, 3
 REF_NONE, REF_STATIC, REF_ADAPTIVE = 0, 1, 2

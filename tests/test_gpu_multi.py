@@ -26,7 +26,7 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("case", ["blast", "sod_walls", "wave64", "smr2", "smr3_walls", "amr2"])
+@pytest.mark.parametrize("case", ["blast", "sod_walls", "wave64", "smr2", "smr3_walls", "amr2", "wenoz"])
 @pytest.mark.parametrize("world", [2, 4])
 def test_multi_gpu_matches_oracle_and_single_gpu(case, world):
     if _ngpu() < world:

@@ -220,3 +220,19 @@ def test_graph_replay_equals_eager(P, monkeypatch):
     assert np.array_equal(outs[0][0], outs[1][0])
     assert np.array_equal(outs[0][1], outs[1][1])
     assert outs[0][2] == outs[1][2]
+
+
+@pytest.mark.parametrize("recon", [0, 3, 4])
+def test_high_order_blast_and_sod(oracle_mod, P, recon):
+    """NEXT 3: PPM / WENO-Z (nghost 3) through the generic high-order GPU path vs the oracle.
+    This path computes in the oracle's exact operation order (WENO-Z weights and the PPM extremum
+    switch amplify round-off), so the states and dt must agree bit for bit."""
+    o, g = _run_both(oracle_mod, P, P.BLAST, [10.0, 0.1, 0.15], 8, recon=recon, nghost=3,
+                     mesh_nx=(48, 48, 48), block_nx=(16, 16, 16), xmin=(-.5,) * 3, xmax=(.5,) * 3)
+    _check_run(o, g)
+    assert np.array_equal(gather(g), gather(o)) and g.time() == o.time()
+    kw = dict(mesh_nx=(128, 6, 6), block_nx=(32, 6, 6), gamma=1.4, recon=recon, nghost=3,
+              bc_inner=(P.OUTFLOW, 0, 2), bc_outer=(P.OUTFLOW, 0, 2))
+    o, g = _run_both(oracle_mod, P, P.SOD, [0.5], 100000, tlim=0.1, **kw)
+    _check_run(o, g)
+    assert np.array_equal(gather(g), gather(o)) and g.time() == o.time()

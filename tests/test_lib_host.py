@@ -46,7 +46,13 @@ def test_config_errors(P):
     with pytest.raises(P.PhError):
         P.Mesh(host_only=True, bc_inner=(0, 0, 1), bc_outer=(0, 0, 0))
     with pytest.raises(P.PhError):
-        P.Mesh(host_only=True, nghost=3)
+        P.Mesh(host_only=True, nghost=4)
+    with pytest.raises(P.PhError):
+        P.Mesh(host_only=True, recon=P.WENOZ, nghost=2)
+    with pytest.raises(P.PhError):
+        P.Mesh(host_only=True, nghost=3, mesh_nx=(16,) * 3, block_nx=(8,) * 3, max_level=1, refinement=1,
+               regions=[(1, 0, 0.5, 0, 0.5, 0, 0.5)])
+    P.Mesh(host_only=True, recon=P.PPM, nghost=3)
 
 
 def _compare_meshes(O, P, nranks=1, **kw):

@@ -28,6 +28,9 @@ CASES = {
     "smr3_walls": dict(kw=dict(mesh_nx=(32, 16, 16), block_nx=(8, 8, 8), max_level=2, refinement=1, gamma=1.4,
                                regions=[(2, 0.45, 0.55, 0.2, 0.6, 0.3, 0.7)], bc_inner=(1, 1, 2), bc_outer=(1, 2, 1)),
                        problem=1, params=[0.5], cycles=10),
+    # NEXT 3: WENO-Z with nghost 3 (generic high-order path) across GPUs
+    "wenoz": dict(kw=dict(mesh_nx=(64, 32, 32), block_nx=(16, 16, 16), xmin=(-.5,) * 3, xmax=(.5,) * 3, recon=4,
+                          nghost=3), problem=2, params=[10.0, 0.1, 0.15], cycles=8),
     # AMR: tagging gathered across ranks, remesh with block migration between GPUs
     "amr2": dict(kw=dict(mesh_nx=(32, 32, 32), block_nx=(8, 8, 8), xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=2,
                          refinement=2, refine_tol=0.1, derefine_tol=0.025, derefine_interval=2),

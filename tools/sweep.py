@@ -34,6 +34,10 @@ def cases():
     c["3"] = dict(kw=dict(mesh_nx=(128,) * 3, block_nx=(32,) * 3, max_level=3, refinement=2, refine_tol=0.1,
                           derefine_tol=0.025, derefine_interval=8, **u), prob=2, par=BLAST)
     c["4"] = dict(kw=dict(mesh_nx=(256,) * 3, block_nx=(64,) * 3, **u), prob=2, par=BLAST)
+    # NEXT 3: PPM / WENO-Z (nghost 3, generic high-order path, exact arithmetic)
+    c["ho-ppm"] = dict(kw=dict(mesh_nx=(256,) * 3, block_nx=(64,) * 3, recon=3, nghost=3, **u), prob=2, par=BLAST)
+    c["ho-wenoz"] = dict(kw=dict(mesh_nx=(256,) * 3, block_nx=(64,) * 3, recon=4, nghost=3, **u), prob=2, par=BLAST)
+    c["ho-plm"] = dict(kw=dict(mesh_nx=(256,) * 3, block_nx=(64,) * 3, recon=0, nghost=3, **u), prob=2, par=BLAST)
     # NEXT 1: the paper's own multilevel mesh: 256^3 root, 32^3 blocks, [0.3,0.7]^3 at
     # level 3 -> 296/1216/1352/21952 blocks (24,816; 813M cells; ~93 GB of block pools)
     c["nx1"] = dict(kw=dict(mesh_nx=(256,) * 3, block_nx=(32,) * 3, max_level=3, refinement=1,
