@@ -28,21 +28,23 @@ def _stale() -> bool:
     return any(os.path.getmtime(f) > t for f in files if os.path.exists(f))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = None) -> str:
+    target = out or LIB
+    if not force and not defines and out is None and not _stale():
         return LIB
     nccl = nccl_root()
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", f"-I{nccl}/include",
-           "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES],
+           *[f"-D{d}" for d in defines],
+           "-o", target + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES],
            f"-L{nccl}/lib", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={nccl}/lib"]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd, cwd=CSRC)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(target + ".tmp", target)
+    return target
 
 
 if __name__ == "__main__":

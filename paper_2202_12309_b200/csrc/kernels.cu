@@ -22,6 +22,20 @@ __device__ __forceinline__ double minmod_i(double a, double b) {
   return ((ha ^ hb) >= 0) ? m : 0.0;
 }
 
+#ifndef PH_PREFETCH_UIN
+#define PH_PREFETCH_UIN 1
+#endif
+#ifndef PH_PREFETCH_U0
+#define PH_PREFETCH_U0 1
+#endif
+#ifndef PH_MINMOD_HALF
+#define PH_MINMOD_HALF 1
+#endif
+__device__ __forceinline__ double minmod_pick(double a, double b) { return (fabs(a) < fabs(b)) ? a : b; }
+__device__ __forceinline__ double minmod_half(double a, double b) {
+  return ((__double2hiint(a) ^ __double2hiint(b)) >= 0) ? 0.5 : 0.0;
+}
+
 template <int RECON>
 __device__ __forceinline__ double slope(double dl, double dr) {
   if (RECON == 0) return minmod_i(dl, dr);
@@ -37,6 +51,15 @@ __device__ __forceinline__ double slope(double dl, double dr) {
 template <int RECON>
 __device__ __forceinline__ void plm_face(double q0, double q1, double q2, double q3, double& wl, double& wr) {
   double d0 = q1 - q0, d1 = q2 - q1, d2 = q3 - q2;
+#if PH_MINMOD_HALF
+  if (RECON == 0) {
+    // minmod with the sign test folded into the coefficient: h = same sign ? 0.5 : 0 (one select
+    // on the high word), state = q + h * (smaller-magnitude difference); equals q + 0.5*minmod
+    wl = fma(minmod_half(d0, d1), minmod_pick(d0, d1), q1);
+    wr = fma(-minmod_half(d1, d2), minmod_pick(d1, d2), q2);
+    return;
+  }
+#endif
   double s1 = slope<RECON>(d0, d1);
   double s2 = slope<RECON>(d1, d2);
   wl = fma(0.5, s1, q1);   // == q1 + 0.5*s1 exactly (0.5*s1 is exact)
@@ -440,8 +463,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
     if (xy && own) {
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
-        uin[v] = __ldg(A.Uin + cell + v * G.vstride);
-        if (USE_U0) u0v[v] = A.U0[cell + v * G.vstride];
+        if (PH_PREFETCH_UIN) uin[v] = __ldg(A.Uin + cell + v * G.vstride);
+        if (USE_U0 && PH_PREFETCH_U0) u0v[v] = A.U0[cell + v * G.vstride];
       }
     }
     // x faces of plane c: 33 per row, item t -> (row t/33, face t%33); rounds 0,1 (warp 0 only)
@@ -503,6 +526,15 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
         const double a = p0[v * VS];
+#if PH_MINMOD_HALF
+        if (RECON == 0) {
+          const double dl = a - pm[v * VS], dr = pp[v * VS] - a;
+          const double h = minmod_half(dl, dr), mp = minmod_pick(dl, dr);
+          bot[v] = fma(-h, mp, a);
+          top[v] = fma(h, mp, a);
+          continue;
+        }
+#endif
         const double s = slope<RECON>(a - pm[v * VS], pp[v * VS] - a);
         bot[v] = fma(-0.5, s, a);
         top[v] = fma(0.5, s, a);
@@ -540,8 +572,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
         double d2 = (sFy[v * FYS + (ty + 1) * TX + tx] - sFy[v * FYS + ty * TX + tx]) * idx2;
         double d3 = (fzu[v * FZS] - fzl[v * FZS]) * idx3;
         double L = -((d1 + d2) + d3);
-        double out = fma(A.b1, uin[v], (A.cdt * dt) * L);
-        if (USE_U0) out = fma(A.a0, u0v[v], out);
+        const double ui = PH_PREFETCH_UIN ? uin[v] : __ldg(A.Uin + cell + v * G.vstride);
+        double out = fma(A.b1, ui, (A.cdt * dt) * L);
+        if (USE_U0) out = fma(A.a0, PH_PREFETCH_U0 ? u0v[v] : A.U0[cell + v * G.vstride], out);
         un[v] = out;
         A.Uout[cell + v * G.vstride] = out;
       }
