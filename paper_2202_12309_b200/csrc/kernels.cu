@@ -91,14 +91,35 @@ __device__ __forceinline__ double sound_speed(double rho, double p, double gamma
   return gp * rsqrt_nr(gp * rho);
 }
 
+// min / max as plain compare-selects (DSETP + 2 FSEL).  fmin/fmax carry IEEE NaN semantics that
+// cost a SEL, a predicated LOP3 and register moves per call; a NaN state is already flagged by
+// the cons->prim positivity check, so only finite operands matter here.
+#ifndef PH_FAST_MINMAX
+#define PH_FAST_MINMAX 1
+#endif
+__device__ __forceinline__ double dmin(double a, double b) {
+#if PH_FAST_MINMAX
+  return a < b ? a : b;
+#else
+  return fmin(a, b);
+#endif
+}
+__device__ __forceinline__ double dmax(double a, double b) {
+#if PH_FAST_MINMAX
+  return a > b ? a : b;
+#else
+  return fmax(a, b);
+#endif
+}
+
 // HLLE, Davis speeds, clamped branch-free form (a4; A4, A5).  w = (rho, u_n, v_t1, v_t2, p).
 __device__ __forceinline__ void hlle(const double* wl, const double* wr, const Geom& G, double* F) {
   double cl = sound_speed(wl[0], wl[4], G.gamma);
   double cr = sound_speed(wr[0], wr[4], G.gamma);
-  double sl = fmin(wl[1] - cl, wr[1] - cr);
-  double sr = fmax(wl[1] + cl, wr[1] + cr);
-  double bp = fmax(sr, 0.0);
-  double bm = fmin(sl, 0.0);
+  double sl = dmin(wl[1] - cl, wr[1] - cr);
+  double sr = dmax(wl[1] + cl, wr[1] + cr);
+  double bp = dmax(sr, 0.0);
+  double bm = dmin(sl, 0.0);
   double inv = rcp_nr(bp - bm);
   double bb = bp * bm;
   double mul = wl[0] * wl[1];
@@ -585,7 +606,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
         double p = G.gm1 * (un[4] - ke);
         double cs = sound_speed(un[0], p, G.gamma);
         double s1 = (fabs(v1) + cs) * idx1, s2 = (fabs(v2) + cs) * idx2, s3 = (fabs(v3) + cs) * idx3;
-        tmax = fmax(tmax, fmax(s1, fmax(s2, s3)));
+        tmax = dmax(tmax, dmax(s1, dmax(s2, s3)));
 #pragma unroll
         for (int v = 0; v < NVAR; ++v) tsum[v] += un[v];
       }
@@ -926,7 +947,7 @@ __global__ void reduce_kernel(const double* U, const BlockMeta* meta, int nslots
         if (!(un[0] > 0.0) || !(p > 0.0)) set_error(err, 0, M.gid, k, j, i);
         double cs = sound_speed(un[0], p, G.gamma);
         double s1 = (fabs(v1) + cs) * M.idx[0], s2 = (fabs(v2) + cs) * M.idx[1], s3 = (fabs(v3) + cs) * M.idx[2];
-        tmax = fmax(tmax, fmax(s1, fmax(s2, s3)));
+        tmax = dmax(tmax, dmax(s1, dmax(s2, s3)));
       }
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) ts[v] += un[v];
