@@ -170,7 +170,11 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     W = workload(args.config, world)
-    mesh = P.Mesh(device=local, rank=rank, nranks=world, stream=stream, **W)
+    transport = {"auto": P.HALO_AUTO, "nccl": P.HALO_NCCL, "peer": P.HALO_PEER}[args.halo]
+    mesh = P.Mesh(device=local, rank=rank, nranks=world, stream=stream, halo_transport=transport, **W)
+    halo = "local direct halo" if world == 1 else (
+        "peer memory (stage kernels read remote faces over NVLink)" if mesh.plan_info()["peer_halo"]
+        else "NCCL send/recv of remote faces")
     nglob = mesh.num_blocks()
     n = W["block_nx"][0]
     cells = nglob * n ** 3
@@ -236,6 +240,13 @@ def run_ours(args):
                "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
                "note": "each step: H2D of the rank's whole state, refresh + 1 cycle, D2H of the state (ph_step_host)"}
 
+    # per-rank stage-kernel time: a slow GPU paces every rank through the halo / dt dependencies
+    stage_ranks = [stage_ms / max(stage_n, 1)]
+    if world > 1:
+        tl = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(world)]
+        dist.all_gather(tl, torch.tensor([stage_ms / max(stage_n, 1)], dtype=torch.float64, device="cuda"))
+        stage_ranks = [float(x.item()) for x in tl]
+
     # ---- roofline of the dominant kernel (the fused stage kernel)
     peak, peak_kind = measured_peaks()
     r = ((n + 4) / n) ** 3
@@ -266,13 +277,14 @@ def run_ours(args):
                                f"{nglob} blocks, all local blocks per launch, PLM-minmod + HLLE + RK2, CFL 0.3",
                    "global_blocks": nglob, "block": n, "nghost": 2,
                    "l2": "inputs larger than L2 (state %.1f GB per GPU vs 126 MB L2)" % (2 * nloc * 5 * (n + 4) ** 3 * 8 / 1e9),
-                   "parallelism": f"morton-partition dp{world}"},
+                   "parallelism": f"morton-partition dp{world}", "halo": halo},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "kernel": "stage_kernel (fused cons->prim, PLM, HLLE x/y/z, divergence, RK combine)",
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "algorithmic_bytes_per_launch": stage_bytes,
                      "stage_ms_avg": stage_avg_ms, "stage_share_of_step": stage_ms / ms if ms else None,
+                     "stage_ms_avg_per_rank": stage_ranks,
                      "exchange_ms_per_step": exch_ms / args.steps,
                      "cycle_hbm_frac_B_ghost": value / world * b_ghost / (peak * 1e9),
                      "B_ghost_bytes_per_zone_cycle": b_ghost},
@@ -302,6 +314,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="2b", choices=["2b", "4"])
+    ap.add_argument("--halo", default="auto", choices=["auto", "nccl", "peer"],
+                    help="multi-GPU halo transport (auto: peer memory when every rank can map its peers)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)

@@ -1,5 +1,5 @@
 /*
- * ph.h -- C ABI of the B200-native Parthenon-hydro hot path (ABI version 1).
+ * ph.h -- C ABI of the B200-native Parthenon-hydro hot path (ABI version 2).
  *
  * What it computes (PAPER.md = arXiv 2202.12309, cited P:line):
  *   the per-cycle update of the Parthenon-hydro miniapp (§4.1: "a two-stage
@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PH_ABI_VERSION 1
+#define PH_ABI_VERSION 2
 
 typedef struct ph_mesh ph_mesh; /* opaque; owned by the caller until ph_mesh_destroy */
 
@@ -61,6 +61,15 @@ typedef enum {
 typedef enum { PH_INT_RK2 = 0, PH_INT_VL2 = 1 } ph_integrator;                      /* A1 */
 typedef enum { PH_PROB_LINEAR_WAVE = 0, PH_PROB_SOD = 1, PH_PROB_BLAST = 2, PH_PROB_KH = 3 } ph_problem;
 typedef enum { PH_REF_NONE = 0, PH_REF_STATIC = 1, PH_REF_ADAPTIVE = 2 } ph_refinement;
+/* How the per-cycle halo of a uniform multi-GPU mesh travels between GPUs.  Either way blocks with
+ * remote faces are updated first and their faces sent while the interior blocks compute. */
+typedef enum {
+  PH_HALO_AUTO = 0,  /* peer memory when every rank can map its peers' receive buffers, else NCCL */
+  PH_HALO_NCCL = 1,  /* pack -> grouped ncclSend/ncclRecv -> unpack into ghost cells */
+  PH_HALO_PEER = 2   /* peer memory, or PH_ERR_UNSUPPORTED: the pack kernel stores boundary faces
+                        straight into the receiving GPU's buffer over NVLink (CUDA IPC) and raises
+                        a flag there; the receiver waits on the flag and unpacks.  No NCCL. */
+} ph_halo_transport;
 
 typedef struct {
   int32_t abi_version;     /* must equal PH_ABI_VERSION, else PH_ERR_INVALID_ARG */
@@ -90,6 +99,10 @@ typedef struct {
   void* (*dev_alloc)(size_t bytes, void* ctx); /* optional device allocator (torch caching allocator) */
   void (*dev_free)(void* ptr, void* ctx);
   void* alloc_ctx;
+  int32_t halo_transport;           /* ph_halo_transport (ABI 2).  Peer memory applies to uniform,
+                                       non-adaptive, nghost-2 meshes with nranks > 1; its receive
+                                       buffers come from cudaMalloc (CUDA IPC), not dev_alloc.
+                                       The full exchange (ph_refresh, ph_exchange) stays on NCCL. */
 } ph_config;
 
 /* One leaf block.  gid = position in Z-order (A19); rank from the contiguous Morton partition. */
@@ -132,6 +145,7 @@ typedef struct {
   uint64_t cyc_recv_hash_from[64];
   int32_t direct_halo;          /* 1 if stage kernels read local same-level face neighbours directly */
   int64_t n_cyc_local_tasks;
+  int32_t peer_halo;            /* 1 if the per-cycle halo travels by peer-memory puts (ABI 2) */
 } ph_plan_info;
 
 /* ---- lifecycle ---------------------------------------------------------------------------- */

@@ -133,6 +133,23 @@ struct ph_mesh {
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> t_stage, t_exch;
   std::vector<cudaEvent_t> ev_pool;
+  // peer transport of the per-cycle halo (uniform multi-GPU meshes): [64 flags | recv half 0 |
+  // recv half 1] in one IPC-exported cudaMalloc region per rank.  The pack kernel stores boundary
+  // faces straight into the peers' receive halves (U1 exchange: half 0, U0 exchange: half 1),
+  // then signals; the receiver waits on its flags and unpacks locally.
+  bool peer = false;
+  void* peer_region = nullptr;
+  std::vector<void*> peer_open;                     // per rank: mapped peer region (nullptr for me)
+  double** d_prbuf[2] = {nullptr, nullptr};         // device [R]: every rank's receive half 0 / 1
+  double* my_rbuf[2] = {nullptr, nullptr};
+  unsigned long long** d_pflags = nullptr;          // device [R]: every rank's flag array
+  unsigned long long* my_flags = nullptr;           // [64] in my region, written by peers
+  unsigned long long* d_ctr = nullptr;              // [2] signal / wait epoch counters (device)
+  unsigned long long send_mask = 0, recv_mask = 0;  // peers I put to / receive from per exchange
+  // boundary-first schedule of the multi-GPU cycle: B (high priority) runs boundary blocks and the
+  // halo, I runs interior blocks concurrently
+  cudaStream_t bstream = nullptr, istream = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_b1 = nullptr, ev_i1 = nullptr, ev_b2 = nullptr, ev_i2 = nullptr;
 };
 
 /* ------------------------------------------------------------------------------- helpers */
@@ -280,6 +297,7 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
       } else if (src_here) {  // pack for b.rank
         int peer = b.rank;
         t.dst_slot = -1;
+        t.bc = -1;
         t.src_slot = (int)s.local;
         t.buf = soff[peer];
         soff[peer] += (int64_t)NVAR * t.ncell;
@@ -623,6 +641,118 @@ static ph_status setup_device(ph_mesh* m) {
   return PH_OK;
 }
 
+/* Peer transport set-up (collective; after build_plan).  Each rank cudaMallocs [64 flags | recv
+ * half 0 | recv half 1] (each half sized for the per-cycle plan), exports it with CUDA IPC and
+ * allgathers handle, half size and its per-source receive offsets over NCCL; then maps the regions
+ * of the peers it sends to.  The ranks agree (NCCL min) on whether every mapping succeeded; if not,
+ * *ok = false and the halo stays on NCCL.  On success the per-cycle pack tasks become puts: each
+ * writes at the offset the receiving rank's unpack task reads.  Flags are zeroed before the
+ * agreement, so no peer can signal into them earlier. */
+static ph_status setup_peer(ph_mesh* m, bool* ok_out) {
+  *ok_out = false;
+  const int R = m->nranks, me = m->rank;
+  Plan& PL = m->plan[1];
+  const int64_t rb = std::max<int64_t>(PL.rbuf_n, 1);
+  struct Rec {
+    cudaIpcMemHandle_t h;
+    int64_t rb;
+    int32_t ok, pad;
+    int64_t recv_off[64];
+  };
+  Rec mine{};
+  mine.rb = rb;
+  mine.ok = 1;
+  for (int p = 0; p < R; ++p) mine.recv_off[p] = PL.recv_off[p];
+  const size_t flag_bytes = 64 * sizeof(unsigned long long);
+  if (cudaMalloc(&m->peer_region, flag_bytes + 2 * (size_t)rb * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    m->peer_region = nullptr;
+    mine.ok = 0;
+  } else if (cudaIpcGetMemHandle(&mine.h, m->peer_region) != cudaSuccess) {
+    cudaGetLastError();
+    mine.ok = 0;
+  }
+  if (m->peer_region) {
+    m->my_flags = (unsigned long long*)m->peer_region;
+    CU(cudaMemsetAsync(m->my_flags, 0, flag_bytes, m->stream));
+  }
+  m->send_mask = m->recv_mask = 0;
+  for (int p = 0; p < R; ++p) {
+    if (p == me) continue;
+    if (PL.send_cnt[p] > 0) m->send_mask |= 1ull << p;
+    if (PL.recv_cnt[p] > 0) m->recv_mask |= 1ull << p;
+  }
+  void* dbuf = nullptr;
+  TRY(dalloc(m, &dbuf, (size_t)(R + 1) * sizeof(Rec), true));
+  CU(cudaMemcpyAsync((char*)dbuf + (size_t)R * sizeof(Rec), &mine, sizeof(Rec), cudaMemcpyHostToDevice, m->stream));
+  NC(ncclAllGather((char*)dbuf + (size_t)R * sizeof(Rec), dbuf, sizeof(Rec), ncclUint8, m->comm, m->stream));
+  std::vector<Rec> all(R);
+  CU(cudaMemcpyAsync(all.data(), dbuf, (size_t)R * sizeof(Rec), cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  int32_t ok = 1;
+  m->peer_open.assign(R, nullptr);
+  for (int p = 0; p < R; ++p) {
+    if (!all[p].ok) ok = 0;
+    if (p == me || !all[p].ok || !m->peer_region || !((m->send_mask >> p) & 1ull)) continue;
+    void* ptr = nullptr;
+    if (cudaIpcOpenMemHandle(&ptr, all[p].h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) m->peer_open[p] = ptr;
+    else {
+      cudaGetLastError();
+      ok = 0;
+    }
+  }
+  int32_t* dok = (int32_t*)dbuf;
+  CU(cudaMemcpyAsync(dok, &ok, sizeof ok, cudaMemcpyHostToDevice, m->stream));
+  NC(ncclAllReduce(dok, dok, 1, ncclInt32, ncclMin, m->comm, m->stream));
+  CU(cudaMemcpyAsync(&ok, dok, sizeof ok, cudaMemcpyDeviceToHost, m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  if (!ok) {
+    for (void* p : m->peer_open)
+      if (p) cudaIpcCloseMemHandle(p);
+    m->peer_open.clear();
+    if (m->peer_region) cudaFree(m->peer_region);
+    m->peer_region = nullptr;
+    m->my_flags = nullptr;
+    return PH_OK;
+  }
+  std::vector<double*> h0(R, nullptr), h1(R, nullptr);
+  std::vector<unsigned long long*> fl(R, nullptr);
+  for (int p = 0; p < R; ++p) {
+    char* base = (char*)(p == me ? m->peer_region : m->peer_open[p]);
+    if (!base) continue;
+    fl[p] = (unsigned long long*)base;
+    h0[p] = (double*)(base + flag_bytes);
+    h1[p] = (double*)(base + flag_bytes + (size_t)all[p].rb * sizeof(double));
+  }
+  m->my_rbuf[0] = h0[me];
+  m->my_rbuf[1] = h1[me];
+  TRY(dalloc(m, (void**)&m->d_prbuf[0], R * sizeof(double*), true));
+  TRY(dalloc(m, (void**)&m->d_prbuf[1], R * sizeof(double*), true));
+  TRY(dalloc(m, (void**)&m->d_pflags, R * sizeof(void*), true));
+  TRY(dalloc(m, (void**)&m->d_ctr, 2 * sizeof(unsigned long long), true));
+  CU(cudaMemcpyAsync(m->d_prbuf[0], h0.data(), R * sizeof(double*), cudaMemcpyHostToDevice, m->stream));
+  CU(cudaMemcpyAsync(m->d_prbuf[1], h1.data(), R * sizeof(double*), cudaMemcpyHostToDevice, m->stream));
+  CU(cudaMemcpyAsync(m->d_pflags, fl.data(), R * sizeof(void*), cudaMemcpyHostToDevice, m->stream));
+  CU(cudaMemsetAsync(m->d_ctr, 0, 2 * sizeof(unsigned long long), m->stream));
+  CU(cudaStreamSynchronize(m->stream));
+  // per-cycle pack tasks -> puts at the receiver's offsets (both sides enumerate in the same order)
+  for (XTask& t : PL.pack.tasks) {
+    int p = 0;
+    while (p + 1 < R && t.buf >= PL.send_off[p] + PL.send_cnt[p]) ++p;
+    t.bc = p;
+    t.buf = t.buf - PL.send_off[p] + all[p].recv_off[me];
+  }
+  *ok_out = true;
+  return PH_OK;
+}
+
+/* Host-side rendezvous of all ranks (teardown of the peer mappings). */
+static void host_barrier(ph_mesh* m) {
+  if (m->nranks < 2 || !m->comm || !m->my6) return;
+  ncclAllReduce(m->my6, m->my6 + 1, 1, ncclDouble, ncclSum, m->comm, m->stream);
+  cudaStreamSynchronize(m->stream);
+}
+
 static ph_status setup_persistent(ph_mesh* m) {
   TRY(dalloc(m, (void**)&m->my6, 8 * sizeof(double), true));
   TRY(dalloc(m, (void**)&m->all6, (size_t)6 * m->nranks * sizeof(double), true));
@@ -642,6 +772,10 @@ static ph_status check_err(const ph_mesh* m) {
   CU(cudaMemcpy(&e, m->d_err, sizeof(e), cudaMemcpyDeviceToHost));
   if (e.flag) {
     char buf[256];
+    if (e.stage == -2) {
+      snprintf(buf, sizeof buf, "peer-halo barrier timed out waiting for rank %lld", (long long)e.gid);
+      return fail(PH_ERR_COMM, buf);
+    }
     snprintf(buf, sizeof buf, "non-positive density or pressure at gid %lld cell (k,j,i)=(%d,%d,%d) stage %d",
              (long long)e.gid, e.k, e.j, e.i, e.stage);
     return fail(PH_ERR_PHYSICS, buf);
@@ -669,11 +803,18 @@ static ph_status exchange_begin(ph_mesh* m, double* U, int which) {
   a.C = m->C;
   a.sbuf = m->sbuf;
   a.rbuf = m->rbuf;
+  const bool put = m->peer && which == 1;  // peer transport: pack straight into the peers' receive halves
+  if (put) a.peer_rbuf = m->d_prbuf[U == m->U1 ? 0 : 1];
   if (PL.pack.nchunks()) {
     a.tasks = PL.pack.d_tasks;
     a.chunks = PL.pack.d_chunks;
     CU(launch_xfill(PL.pack.nchunks(), a, m->G, m->stream));
     m->launches++;
+  }
+  if (put) {
+    CU(launch_peer_signal(m->d_pflags, m->d_ctr, m->rank, m->send_mask, m->stream));
+    m->launches++;
+    return PH_OK;
   }
   CU(cudaEventRecord(m->ev_pack, m->stream));
   CU(cudaStreamWaitEvent(m->comm_stream, m->ev_pack, 0));
@@ -706,7 +847,13 @@ static ph_status exchange_end(ph_mesh* m, double* U, int which) {
   };
   TRY(run(PL.local));
   if (remote) {
-    CU(cudaStreamWaitEvent(m->stream, m->ev_comm, 0));
+    if (m->peer && which == 1) {
+      CU(launch_peer_wait(m->my_flags, m->d_ctr + 1, m->recv_mask, m->d_err, m->stream));
+      m->launches++;
+      a.rbuf = m->my_rbuf[U == m->U1 ? 0 : 1];
+    } else {
+      CU(cudaStreamWaitEvent(m->stream, m->ev_comm, 0));
+    }
     TRY(run(PL.unpack));
   }
   TRY(run(PL.b1));
@@ -854,17 +1001,45 @@ static ph_status one_cycle(ph_mesh* m) {
   const bool fuse_reduce = !m->multilevel && !adaptive;
   const int nloc = (int)m->local_gids.size();
   if (m->overlap && fuse_reduce) {
-    // multi-GPU, uniform mesh: stage 2 of the interior blocks overlaps the U1 halo exchange,
-    // the dt / totals reduction (split communicator) overlaps the U0 exchange
+    // multi-GPU, uniform mesh, boundary first: stream B (high priority) runs the blocks
+    // with remote or physical faces and then their halo (NCCL, or puts into peer memory); stream I
+    // runs the interior blocks at the same time, so each exchange hides behind interior work.
+    //   B: S1(bnd) -> send U1 -> [I: S1(int) done] -> recv U1 -> S2(bnd) -> send U0 -> recv U0
+    //   I: S1(int) -> [B: S1(bnd) done] -> S2(int)
+    // then the caller's stream joins both and reduces dt / totals (split communicator).
     const bool vl2 = m->cfg.integrator == PH_INT_VL2;
-    TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, vl2 ? 0.5 : 1.0, false, 1));
+    const double c1 = vl2 ? 0.5 : 1.0, a2 = vl2 ? 1.0 : 0.5, b2 = vl2 ? 0.0 : 0.5, c2 = vl2 ? 1.0 : 0.5;
+    cudaStream_t S = m->stream;
+    struct Restore {
+      ph_mesh* m;
+      cudaStream_t s;
+      ~Restore() { m->stream = s; }
+    } restore{m, S};
+    CU(cudaEventRecord(m->ev_a, S));
+    CU(cudaStreamWaitEvent(m->bstream, m->ev_a, 0));
+    CU(cudaStreamWaitEvent(m->istream, m->ev_a, 0));
+    m->stream = m->bstream;
+    TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, c1, false, 1, m->n_int, nloc));
+    CU(cudaEventRecord(m->ev_b1, m->bstream));
     TRY(exchange_begin(m, m->U1, 1));
-    TRY(run_stage(m, m->U1, m->U0, vl2 ? 1.0 : 0.5, vl2 ? 0.0 : 0.5, vl2 ? 1.0 : 0.5, true, 2, 0, m->n_int));
+    m->stream = m->istream;
+    TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, c1, false, 1, 0, m->n_int));
+    CU(cudaEventRecord(m->ev_i1, m->istream));
+    m->stream = m->bstream;
     TRY(exchange_end(m, m->U1, 1));
-    TRY(run_stage(m, m->U1, m->U0, vl2 ? 1.0 : 0.5, vl2 ? 0.0 : 0.5, vl2 ? 1.0 : 0.5, true, 2, m->n_int, nloc));
+    CU(cudaStreamWaitEvent(m->bstream, m->ev_i1, 0));
+    TRY(run_stage(m, m->U1, m->U0, a2, b2, c2, true, 2, m->n_int, nloc));
     TRY(exchange_begin(m, m->U0, 1));
-    TRY(reduce_finalize(m, nloc > 0 ? m->stage_ctas : 0, 1));
     TRY(exchange_end(m, m->U0, 1));
+    CU(cudaEventRecord(m->ev_b2, m->bstream));
+    m->stream = m->istream;
+    CU(cudaStreamWaitEvent(m->istream, m->ev_b1, 0));
+    TRY(run_stage(m, m->U1, m->U0, a2, b2, c2, true, 2, 0, m->n_int));
+    CU(cudaEventRecord(m->ev_i2, m->istream));
+    m->stream = S;
+    CU(cudaStreamWaitEvent(S, m->ev_b2, 0));
+    CU(cudaStreamWaitEvent(S, m->ev_i2, 0));
+    TRY(reduce_finalize(m, nloc > 0 ? m->stage_ctas : 0, 1));
     return PH_OK;
   }
   if (m->cfg.integrator == PH_INT_VL2) {
@@ -904,6 +1079,7 @@ static ph_status one_cycle(ph_mesh* m) {
  * the new blocks in gid order, so buffer offsets agree without a handshake. */
 static ph_status remesh(ph_mesh* m, const std::unordered_set<LocKey>& leaves, bool move) {
   const int R = m->nranks, me = m->rank;
+  if (m->peer) return fail(PH_ERR_STATE, "remesh of a peer-halo mesh (peer halo is for static uniform meshes)");
   if (m->graph_exec) {
     cudaGraphExecDestroy(m->graph_exec);
     m->graph_exec = nullptr;
@@ -1213,12 +1389,27 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
     delete m;
     return fail(PH_ERR_CONFIG, e.what());
   }
+  if (cfg->halo_transport < PH_HALO_AUTO || cfg->halo_transport > PH_HALO_PEER) {
+    delete m->tree;
+    delete m;
+    return fail(PH_ERR_CONFIG, "unknown halo_transport");
+  }
+  bool uniform = true;
+  for (auto& b : m->blocks) uniform = uniform && b.loc.level == 0;
+  const bool peer_cfg = m->nranks > 1 && uniform && cfg->refinement != PH_REF_ADAPTIVE && !m->no_direct_halo &&
+                        G.g == 2 && cfg->halo_transport != PH_HALO_NCCL;
+  if (cfg->halo_transport == PH_HALO_PEER && !peer_cfg) {
+    delete m->tree;
+    delete m;
+    return fail(PH_ERR_UNSUPPORTED, "peer halo needs nranks > 1 and a static uniform nghost-2 mesh with the direct halo");
+  }
   ph_status st = build_plan(m);
   if (st != PH_OK) {
     delete m->tree;
     delete m;
     return st;
   }
+  if (m->host_only) m->peer = peer_cfg;  // plan only (the per-cycle plan is the same for both transports)
   if (!m->host_only) {
     cudaError_t e = cudaSetDevice(cfg->device);
     if (e != cudaSuccess) {
@@ -1248,7 +1439,22 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
       r = ncclCommSplit(m->comm, 0, m->rank, &m->comm2, nullptr);
       if (r != ncclSuccess) m->comm2 = nullptr;
     }
+    if (m->nranks > 1) {
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      cudaStreamCreateWithPriority(&m->bstream, cudaStreamNonBlocking, hi);
+      cudaStreamCreateWithFlags(&m->istream, cudaStreamNonBlocking);
+      for (cudaEvent_t* e : {&m->ev_a, &m->ev_b1, &m->ev_i1, &m->ev_b2, &m->ev_i2})
+        cudaEventCreateWithFlags(e, cudaEventDisableTiming);
+    }
     st = setup_persistent(m);
+    if (st == PH_OK && peer_cfg) {
+      bool ok = false;
+      st = setup_peer(m, &ok);
+      m->peer = ok;
+      if (st == PH_OK && !ok && cfg->halo_transport == PH_HALO_PEER)
+        st = fail(PH_ERR_UNSUPPORTED, "peer halo requested but some rank cannot map its peers' memory (CUDA IPC)");
+    }
     if (st == PH_OK) st = setup_device(m);
     if (st == PH_OK) {
       cudaError_t e2 = cudaStreamSynchronize(m->stream);
@@ -1270,12 +1476,26 @@ ph_status ph_mesh_destroy(ph_mesh* m) {
   if (m->graph_exec) cudaGraphExecDestroy(m->graph_exec);
   if (m->ev_fork) cudaEventDestroy(m->ev_fork);
   if (m->ev_join) cudaEventDestroy(m->ev_join);
+  if (m->peer_region) {
+    // nobody may still read my pools when I unmap / free: rendezvous before and after unmapping
+    cudaStreamSynchronize(m->stream);
+    host_barrier(m);
+    for (void* p : m->peer_open)
+      if (p) cudaIpcCloseMemHandle(p);
+    host_barrier(m);
+    cudaFree(m->peer_region);
+    m->peer_region = nullptr;
+  }
   free_all(m);
   for (auto& p : m->t_stage) (void)p;
   for (cudaEvent_t e : m->ev_pool) cudaEventDestroy(e);
   if (m->ev_pack) cudaEventDestroy(m->ev_pack);
   if (m->ev_comm) cudaEventDestroy(m->ev_comm);
   if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
+  if (m->bstream) cudaStreamDestroy(m->bstream);
+  if (m->istream) cudaStreamDestroy(m->istream);
+  for (cudaEvent_t e : {m->ev_a, m->ev_b1, m->ev_i1, m->ev_b2, m->ev_i2})
+    if (e) cudaEventDestroy(e);
   if (m->gstream) cudaStreamDestroy(m->gstream);
   if (m->comm2) ncclCommDestroy(m->comm2);
   if (m->comm) ncclCommDestroy(m->comm);
@@ -1621,6 +1841,7 @@ ph_status ph_get_plan_info(const ph_mesh* m, ph_plan_info* out) {
     out->cyc_recv_hash_from[p] = m->plan[1].recv_hash[p];
   }
   out->direct_halo = m->direct_halo ? 1 : 0;
+  out->peer_halo = m->peer ? 1 : 0;
   out->n_cyc_local_tasks = (int64_t)m->plan[1].local.tasks.size();
   return PH_OK;
 }

@@ -59,7 +59,8 @@ struct XTask {
   int lo[3];         // first destination cell
   int ext[3];        // box extents
   int so[3];         // source shift (see kinds)
-  int bc;            // BC kinds: per dim d, bits [4d,4d+2) low face, [4d+2,4d+4) high face: 0 none, 1 outflow, 2 reflect
+  int bc;            // BC kinds: per dim d, bits [4d,4d+2) low face, [4d+2,4d+4) high face: 0 none, 1 outflow, 2 reflect;
+                     // pack tasks: -1 = my send buffer, else the peer rank whose receive buffer is written (put)
   int ncell;
   int64_t buf;       // offset (doubles) into the send / recv buffer; payload [v][cell]
 };
@@ -129,6 +130,7 @@ struct XArgs {
   double* C;           // coarse staging pool
   double* sbuf;        // send buffer (pack tasks)
   const double* rbuf;  // recv buffer (unpack tasks)
+  double* const* peer_rbuf;  // peer transport: [nranks] IPC-mapped receive buffers (put tasks)
 };
 
 struct PgenArgs {
@@ -155,6 +157,11 @@ constexpr int XCHUNK = 256;  // cells per exchange chunk (one CTA, one cell per 
 // launchers (kernels.cu)
 cudaError_t launch_stage(int recon, bool reduce, bool use_u0, int nblk_cta, const StageArgs& a, const Geom& G,
                          cudaStream_t s);
+// Peer halo transport: signal / wait on IPC-mapped epoch flags (see kernels.cu).
+cudaError_t launch_peer_signal(unsigned long long* const* peer_flags, unsigned long long* ctr, int me,
+                               unsigned long long mask, cudaStream_t s);
+cudaError_t launch_peer_wait(const unsigned long long* my_flags, unsigned long long* ctr, unsigned long long mask,
+                             ErrWord* err, cudaStream_t s);
 cudaError_t launch_xfill(int nchunks, const XArgs& a, const Geom& G, cudaStream_t s);
 cudaError_t launch_reflux(int ntasks, const RefluxTask* t, double* U, const BlockMeta* meta, const double* fbuf,
                           const double* rbuf, const CycleState* st, double w, const Geom& G, cudaStream_t s);

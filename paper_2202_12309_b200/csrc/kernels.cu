@@ -683,7 +683,9 @@ __global__ void __launch_bounds__(XT) xfill_kernel(XArgs A, Geom G) {
         const double* s = A.U + (int64_t)t.src_slot * G.bstride +
                           ((int64_t)(k + t.so[2] + G.g) * G.N[1] + (j + t.so[1] + G.g)) * G.N[0] + (i + t.so[0] + G.g);
         if (t.dst_slot < 0) {
-          double* d = A.sbuf + t.buf + c;
+          // pack: into my send buffer, or (T_PUT kind stored in bc >= 0) straight into the receive
+          // buffer of peer bc over NVLink -- [v][cell] layout, so a warp stores 256 contiguous bytes
+          double* d = (t.bc >= 0 ? A.peer_rbuf[t.bc] : A.sbuf) + t.buf + c;
 #pragma unroll
           for (int v = 0; v < NVAR; ++v) d[(int64_t)v * t.ncell] = s[v * G.vstride];
         } else if (t.kind == T_COPY) {
@@ -1375,6 +1377,66 @@ cudaError_t launch_stage(int recon, bool reduce, bool use_u0, int nblk_cta, cons
   if (recon == 1) return launch_stage_r<1>(reduce, use_u0, ml, nblk_cta, a, G, s);
   if (recon == 2) return launch_stage_r<2>(reduce, use_u0, ml, nblk_cta, a, G, s);
   return cudaErrorInvalidValue;
+}
+
+// ------------------------------------------------------------------------------ peer signal / wait
+// Peer transport of the halo (one-sided over NVLink).  After the put kernel has stored this rank's
+// boundary faces into its peers' receive buffers, signal publishes a new epoch into the flag slot
+// for me of every peer in `mask` (system fence, then a system-scope release store).  wait spins
+// (system-scope acquire) until every peer in `mask` has published that epoch into my flags.  Each
+// rank runs the same sequence of exchanges, so the signal and wait counters advance in lockstep.
+// A peer that never arrives ends the spin after ~35 s with the error word set (stage -2).
+__global__ void peer_signal_kernel(unsigned long long* const* peer_flags, unsigned long long* ctr, int me,
+                                   unsigned long long mask) {
+  __shared__ unsigned long long e;
+  if (threadIdx.x == 0) e = *ctr + 1;
+  __syncthreads();
+  const int p = threadIdx.x;
+  if (p < 64 && ((mask >> p) & 1ull)) {
+    __threadfence_system();
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(peer_flags[p] + me), "l"(e) : "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *ctr = e;
+}
+
+__global__ void peer_wait_kernel(const unsigned long long* my_flags, unsigned long long* ctr, unsigned long long mask,
+                                 ErrWord* err) {
+  __shared__ unsigned long long e;
+  if (threadIdx.x == 0) e = *ctr + 1;
+  __syncthreads();
+  const int p = threadIdx.x;
+  if (p < 64 && ((mask >> p) & 1ull)) {
+    const long long t0 = clock64();
+    unsigned long long v = 0;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(my_flags + p) : "memory");
+      if (v >= e) break;
+      if (clock64() - t0 > (1ll << 36)) {
+        if (atomicCAS(&err->flag, 0, 1) == 0) {
+          err->stage = -2;
+          err->gid = p;
+          __threadfence();
+        }
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *ctr = e;
+}
+
+cudaError_t launch_peer_signal(unsigned long long* const* peer_flags, unsigned long long* ctr, int me,
+                               unsigned long long mask, cudaStream_t s) {
+  peer_signal_kernel<<<1, 64, 0, s>>>(peer_flags, ctr, me, mask);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_peer_wait(const unsigned long long* my_flags, unsigned long long* ctr, unsigned long long mask,
+                             ErrWord* err, cudaStream_t s) {
+  peer_wait_kernel<<<1, 64, 0, s>>>(my_flags, ctr, mask, err);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_xfill(int nchunks, const XArgs& a, const Geom& G, cudaStream_t s) {

@@ -18,7 +18,8 @@ MINMOD, VANLEER, MC, PPM, WENOZ = 0, 1, 2, 3, 4
 RK2, VL2 = 0, 1
 LINEAR_WAVE, SOD, BLAST, KH = 0, 1, 2, 3
 REF_NONE, REF_STATIC, REF_ADAPTIVE = 0, 1, 2
-ABI_VERSION = 1
+ABI_VERSION = 2
+HALO_AUTO, HALO_NCCL, HALO_PEER = 0, 1, 2
 
 _ALLOC = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
 _FREE = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p)
@@ -41,6 +42,7 @@ class _Cfg(C.Structure):
         ("no_direct_halo", C.c_int32),
         ("stream", C.c_void_p), ("nccl_id", C.c_void_p),
         ("dev_alloc", _ALLOC), ("dev_free", _FREE), ("alloc_ctx", C.c_void_p),
+        ("halo_transport", C.c_int32),
     ]
 
 
@@ -64,7 +66,7 @@ class PhPlanInfo(C.Structure):
                 ("send_hash_to", C.c_uint64 * 64), ("recv_hash_from", C.c_uint64 * 64),
                 ("cyc_send_doubles_to", C.c_int64 * 64), ("cyc_recv_doubles_from", C.c_int64 * 64),
                 ("cyc_send_hash_to", C.c_uint64 * 64), ("cyc_recv_hash_from", C.c_uint64 * 64),
-                ("direct_halo", C.c_int32), ("n_cyc_local_tasks", C.c_int64)]
+                ("direct_halo", C.c_int32), ("n_cyc_local_tasks", C.c_int64), ("peer_halo", C.c_int32)]
 
 
 EXPORTS = ["ph_nccl_unique_id", "ph_mesh_create", "ph_mesh_destroy", "ph_set_problem", "ph_set_state",
@@ -144,7 +146,7 @@ DEFAULTS = dict(
     bc_inner=(PERIODIC,) * 3, bc_outer=(PERIODIC,) * 3,
     gamma=5.0 / 3.0, cfl=0.3, recon=MINMOD, integrator=RK2,
     refine_tol=0.1, derefine_tol=0.025, derefine_interval=8, regions=(), pack_size=0,
-    direct_halo=True,
+    direct_halo=True, halo_transport=HALO_AUTO,
 )
 
 
@@ -185,6 +187,7 @@ class Mesh:
         cfg.rank, cfg.nranks, cfg.device = rank, nranks, device
         cfg.host_only = 1 if host_only else 0
         cfg.no_direct_halo = 0 if c["direct_halo"] else 1
+        cfg.halo_transport = c["halo_transport"]
         self._keep = []
         if not host_only:
             import torch
@@ -358,7 +361,8 @@ class Mesh:
                     cyc_send_doubles_to=list(p.cyc_send_doubles_to[:R]),
                     cyc_recv_doubles_from=list(p.cyc_recv_doubles_from[:R]),
                     cyc_send_hash_to=list(p.cyc_send_hash_to[:R]), cyc_recv_hash_from=list(p.cyc_recv_hash_from[:R]),
-                    direct_halo=bool(p.direct_halo), n_cyc_local_tasks=p.n_cyc_local_tasks)
+                    direct_halo=bool(p.direct_halo), n_cyc_local_tasks=p.n_cyc_local_tasks,
+                    peer_halo=bool(p.peer_halo))
 
     def launch_count(self):
         n = C.c_int64()

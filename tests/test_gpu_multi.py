@@ -1,4 +1,4 @@
-"""Multi-GPU (NCCL) parity through torchrun; needs >= 2 GPUs (gpurun --gpus 2), else skipped."""
+"""Multi-GPU parity through torchrun (NCCL and peer-memory halo); needs >= 2 GPUs (gpurun --gpus 2), else skipped."""
 import os
 import socket
 import subprocess
@@ -26,15 +26,20 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("case", ["blast", "sod_walls", "wave64", "smr2", "smr3_walls", "amr2", "wenoz"])
+CASES = [(c, "auto") for c in ("smr2", "smr3_walls", "amr2", "wenoz")]
+# uniform meshes: both halo transports (NCCL pack/send/unpack, and peer memory read in place)
+CASES += [(c, h) for c in ("blast", "sod_walls", "wave64") for h in ("nccl", "peer")]
+
+
+@pytest.mark.parametrize("case,halo", CASES)
 @pytest.mark.parametrize("world", [2, 4])
-def test_multi_gpu_matches_oracle_and_single_gpu(case, world):
+def test_multi_gpu_matches_oracle_and_single_gpu(case, halo, world):
     if _ngpu() < world:
         pytest.skip(f"needs {world} GPUs")
     for attempt in range(4):  # the free-port probe can race with another rendezvous: retry
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
                "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-               os.path.join(ROOT, "tools", "multi_check.py"), "--case", case]
+               os.path.join(ROOT, "tools", "multi_check.py"), "--case", case, "--halo", halo]
         r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
         if "EADDRINUSE" not in r.stderr:
             break

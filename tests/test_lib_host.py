@@ -136,13 +136,43 @@ def test_direct_halo_cycle_plan(P):
     info = P.Mesh(host_only=True, mesh_nx=(64, 64, 64), block_nx=(16, 16, 16), max_level=1, refinement=1,
                   regions=[(1, 0.1, 0.3, 0.1, 0.3, 0.1, 0.3)]).plan_info()
     assert not info["direct_halo"]
-    # multi-rank uniform: the cycle plan keeps only remote faces, symmetric across ranks
+    # multi-rank uniform, NCCL halo: the cycle plan keeps only remote faces, symmetric across ranks
     R = 4
-    kw = dict(mesh_nx=(128, 64, 64), block_nx=(16, 16, 16))
+    kw = dict(mesh_nx=(128, 64, 64), block_nx=(16, 16, 16), halo_transport=P.HALO_NCCL)
     infos = [P.Mesh(host_only=True, rank=r, nranks=R, **kw).plan_info() for r in range(R)]
     for s in range(R):
         for d in range(R):
             assert infos[s]["cyc_send_doubles_to"][d] == infos[d]["cyc_recv_doubles_from"][s]
             assert infos[s]["cyc_send_hash_to"][d] == infos[d]["cyc_recv_hash_from"][s]
             assert infos[s]["cyc_send_doubles_to"][d] <= infos[s]["send_doubles_to"][d]
-    assert all(i["n_cyc_local_tasks"] == 0 for i in infos)
+    assert any(i["cyc_send_doubles_to"][d] > 0 for i in infos for d in range(R))
+    assert all(i["n_cyc_local_tasks"] == 0 and not i["peer_halo"] for i in infos)
+
+
+def test_peer_halo_plan(P):
+    """Peer transport (uniform, N > 1): the per-cycle plan is the NCCL one -- what rank s puts into d's
+    receive buffer is exactly what d unpacks from s -- and only the transport differs."""
+    R = 4
+    for bc in (P.PERIODIC, P.OUTFLOW):
+        kw = dict(mesh_nx=(128, 64, 64), block_nx=(16, 16, 16), bc_inner=(bc,) * 3, bc_outer=(bc,) * 3)
+        peer = [P.Mesh(host_only=True, rank=r, nranks=R, **kw).plan_info() for r in range(R)]
+        nccl = [P.Mesh(host_only=True, rank=r, nranks=R, halo_transport=P.HALO_NCCL, **kw).plan_info()
+                for r in range(R)]
+        for i, j in zip(peer, nccl):
+            assert i["peer_halo"] and i["direct_halo"] and not j["peer_halo"]
+            for key in ("cyc_send_doubles_to", "cyc_recv_doubles_from", "cyc_send_hash_to", "cyc_recv_hash_from"):
+                assert i[key] == j[key]
+            assert sum(i["cyc_send_doubles_to"]) > 0
+    # not eligible: one rank, multilevel, adaptive, nghost 3, NCCL forced, no direct halo
+    assert not P.Mesh(host_only=True, mesh_nx=(64,) * 3, block_nx=(16,) * 3).plan_info()["peer_halo"]
+    ml = dict(max_level=1, refinement=1, regions=[(1, 0.1, 0.3, 0.1, 0.3, 0.1, 0.3)])
+    for extra in (ml, dict(nghost=3, recon=P.PPM), dict(direct_halo=False), dict(halo_transport=P.HALO_NCCL)):
+        i = P.Mesh(host_only=True, rank=0, nranks=2, mesh_nx=(64,) * 3, block_nx=(16,) * 3, **extra).plan_info()
+        assert not i["peer_halo"]
+    # requiring it where it cannot apply is an error, as is an unknown transport
+    with pytest.raises(P.PhError) as e:
+        P.Mesh(host_only=True, rank=0, nranks=2, mesh_nx=(64,) * 3, block_nx=(16,) * 3, halo_transport=P.HALO_PEER,
+               direct_halo=False)
+    assert e.value.code == 8
+    with pytest.raises(P.PhError):
+        P.Mesh(host_only=True, mesh_nx=(64,) * 3, block_nx=(16,) * 3, halo_transport=7)

@@ -1,6 +1,6 @@
 """Multi-GPU parity check, launched with torchrun (one process per GPU, NCCL):
 
-    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port P tools/multi_check.py [--case blast]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port P tools/multi_check.py [--case blast] [--halo peer]
 
 Every rank runs its Morton range; rank 0 gathers all blocks and compares them with (a) the CPU
 oracle (1e-12, tests/parity.py) and (b) a single-GPU run of the same problem (bitwise)."""
@@ -41,6 +41,7 @@ CASES = {
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", default="blast")
+    ap.add_argument("--halo", default="auto", choices=["auto", "nccl", "peer"])
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -50,7 +51,8 @@ def main():
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     C = CASES[a.case]
-    m = P.Mesh(device=local, rank=rank, nranks=world, **C["kw"])
+    transport = {"auto": P.HALO_AUTO, "nccl": P.HALO_NCCL, "peer": P.HALO_PEER}[a.halo]
+    m = P.Mesh(device=local, rank=rank, nranks=world, halo_transport=transport, **C["kw"])
     m.set_problem(C["problem"], C["params"])
     m.step(C["cycles"])
     mine = {b["gid"]: m.get_state(b["gid"]) for b in m.blocks() if b["rank"] == rank}
@@ -85,8 +87,9 @@ def main():
                    same_mesh=same_mesh, nblocks=len(allb),
                    t=tm, t_oracle=to, dt_rel=abs(tm[1] - to[1]) / to[1],
                    mass_rel=float(abs(hist[-1, 2] - ho[-1, 2]) / ho[-1, 2]),
-                   send_doubles=info["send_doubles_to"])
+                   send_doubles=info["send_doubles_to"], halo=a.halo, peer_halo=info["peer_halo"])
         ok = res["max_err"] <= 1e-12 and bitwise and same_mesh and res["dt_rel"] <= 1e-12 and tm[2] == to[2]
+        ok = ok and (info["peer_halo"] == (a.halo == "peer") or a.halo == "auto")
         res["ok"] = ok
         print("MULTI_CHECK " + json.dumps(res), flush=True)
     m.close()
