@@ -266,6 +266,21 @@ def run_ours(args):
         except Exception:
             traffic = None
     b_ghost = (6 * r - 1) * 40.0
+    # co-limiter (SURVEY §8(d) "report both"): the fp64 pipe.  Instructions per cell-stage from the
+    # committed ncu capture of this kernel; peak = 148 SMs x 64 fp64 lanes/clk x 1965 MHz (B200 unit
+    # counts and max clock).
+    fp64 = None
+    pp = os.path.join(ROOT, "profiles", "r01_stage_2b_v8.json")
+    if os.path.exists(pp) and stage_n:
+        try:
+            per_cell = float(json.load(open(pp))["fp64_inst_per_cell"])
+            ach = per_cell * nloc_cells / (stage_avg_ms * 1e-3)
+            fpk = 148 * 64 * 1965e6
+            fp64 = {"bound": "alu", "achieved": ach, "peak": fpk, "unit": "fp64-pipe thread instr/s",
+                    "frac": ach / fpk, "inst_per_cell_stage": per_cell,
+                    "source": "inst count: ncu profiles/r01_stage_2b_v8.json; peak: 148 SM x 64 lanes x 1.965 GHz"}
+        except Exception:
+            fp64 = None
     line = {
         "metric": "zone-cycles/s", "value": value, "unit": "zone-cycles/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -287,7 +302,7 @@ def run_ours(args):
                      "stage_ms_avg_per_rank": stage_ranks,
                      "exchange_ms_per_step": exch_ms / args.steps,
                      "cycle_hbm_frac_B_ghost": value / world * b_ghost / (peak * 1e9),
-                     "B_ghost_bytes_per_zone_cycle": b_ghost},
+                     "B_ghost_bytes_per_zone_cycle": b_ghost, "fp64_pipe": fp64},
         "gpu_launches": launches,
         "clocks": clocks,
         "e2e": e2e,

@@ -182,6 +182,6 @@ cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, d
                           double* sbuf, const Geom& G, cudaStream_t s);
 cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslots, const StageArgs& a, double* W,
                                    double* Fx, double* Fy, double* Fz, const Geom& G, cudaStream_t s);
-size_t stage_smem_bytes();
+size_t stage_smem_bytes(bool use_u0);
 
 }  // namespace ph

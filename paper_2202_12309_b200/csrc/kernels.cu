@@ -31,6 +31,12 @@ __device__ __forceinline__ double minmod_i(double a, double b) {
 #ifndef PH_MINMOD_HALF
 #define PH_MINMOD_HALF 1
 #endif
+// stage 2: stage the finish operand U^n in shared memory with cp.async instead of holding it in
+// registers across the face phase.  Off: removes the 32 B spill but the extra 10 KB of smem per CTA
+// costs L1 and is 2.4 % slower on 2b (profiles/r01_ab_finish_prefetch.md)
+#ifndef PH_U0_SMEM
+#define PH_U0_SMEM 0
+#endif
 __device__ __forceinline__ double minmod_pick(double a, double b) { return (fabs(a) < fabs(b)) ? a : b; }
 __device__ __forceinline__ double minmod_half(double a, double b) {
   return ((__double2hiint(a) ^ __double2hiint(b)) >= 0) ? 0.5 : 0.0;
@@ -330,6 +336,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   double* sFx = sW + 3 * SLOT;             // [5][TY][TX+1]
   double* sFy = sFx + NVAR * FXS;          // [5][TY+1][TX]
   double* sFz = sFy + NVAR * FYS;          // [2][5][TY][TX]
+  double* sU0 = sFz + 2 * NVAR * FZS;      // [5][TY][TX]: U^n of the cells being finished (stage 2)
 
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
@@ -485,8 +492,14 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
         if (PH_PREFETCH_UIN) uin[v] = __ldg(A.Uin + cell + v * G.vstride);
-        if (USE_U0 && PH_PREFETCH_U0) u0v[v] = A.U0[cell + v * G.vstride];
+        if (USE_U0 && PH_U0_SMEM) {
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(sU0 + v * NT + tid);
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(A.U0 + cell + v * G.vstride) : "memory");
+        } else if (USE_U0 && PH_PREFETCH_U0) {
+          u0v[v] = A.U0[cell + v * G.vstride];
+        }
       }
+      if (USE_U0 && PH_U0_SMEM) asm volatile("cp.async.commit_group;" ::: "memory");
     }
     // x faces of plane c: 33 per row, item t -> (row t/33, face t%33); rounds 0,1 (warp 0 only)
     if (xy) {
@@ -587,6 +600,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
       const double* fzl = sFz + (c & 1) * NVAR * FZS + tid;        // face c   (lower)
       const double* fzu = sFz + ((c + 1) & 1) * NVAR * FZS + tid;  // face c+1 (upper)
       double un[NVAR];
+      if (USE_U0 && PH_U0_SMEM) asm volatile("cp.async.wait_all;" ::: "memory");  // my own copies only
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
         double d1 = (sFx[v * FXS + ty * (TX + 1) + tx + 1] - sFx[v * FXS + ty * (TX + 1) + tx]) * idx1;
@@ -595,7 +609,8 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
         double L = -((d1 + d2) + d3);
         const double ui = PH_PREFETCH_UIN ? uin[v] : __ldg(A.Uin + cell + v * G.vstride);
         double out = fma(A.b1, ui, (A.cdt * dt) * L);
-        if (USE_U0) out = fma(A.a0, PH_PREFETCH_U0 ? u0v[v] : A.U0[cell + v * G.vstride], out);
+        if (USE_U0)
+          out = fma(A.a0, PH_U0_SMEM ? sU0[v * NT + tid] : (PH_PREFETCH_U0 ? u0v[v] : A.U0[cell + v * G.vstride]), out);
         un[v] = out;
         A.Uout[cell + v * G.vstride] = out;
       }
@@ -641,7 +656,9 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   }
 }
 
-size_t stage_smem_bytes() { return sizeof(double) * (3 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS); }
+size_t stage_smem_bytes(bool use_u0) {
+  return sizeof(double) * (3 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS + ((use_u0 && PH_U0_SMEM) ? NVAR * NT : 0));
+}
 
 // ------------------------------------------------------------------------------ exchange kernel
 // One CTA per chunk of <= XCHUNK cells of one task; all tasks of one phase in one launch
@@ -1343,7 +1360,7 @@ __global__ void remesh_kernel(const RemeshTask* tasks, const double* Uold, doubl
 
 template <int R, bool RD, bool U0, bool ML, bool FULL>
 static cudaError_t launch_stage_t(int nblk_cta, const StageArgs& a, const Geom& G, cudaStream_t s) {
-  const size_t sm = stage_smem_bytes();
+  const size_t sm = stage_smem_bytes(U0);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL>,
