@@ -7,6 +7,7 @@
 //
 // No tensor cores: every kernel here is an fp64 stencil or copy (bandwidth / fp64-issue bound).
 #include <cstdio>
+#include <cstdlib>
 
 #include "device.cuh"
 
@@ -1366,6 +1367,12 @@ static cudaError_t launch_stage_t(int nblk_cta, const StageArgs& a, const Geom& 
     cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
+    // shared-memory carveout hint (percent of the maximum); the rest of the 256 KB is L1
+    if (const char* cv = getenv("PH_CARVEOUT")) {
+      e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                               atoi(cv));
+      if (e != cudaSuccess) return e;
+    }
     attr = true;
   }
   stage_kernel<R, RD, U0, ML, FULL><<<nblk_cta, NT, sm, s>>>(a, G);
