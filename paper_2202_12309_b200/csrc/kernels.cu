@@ -35,6 +35,17 @@ __device__ __forceinline__ double minmod_i(double a, double b) {
 // stage 2: stage the finish operand U^n in shared memory with cp.async instead of holding it in
 // registers across the face phase.  Off: removes the 32 B spill but the extra 10 KB of smem per CTA
 // costs L1 and is 2.4 % slower on 2b (profiles/r01_ab_finish_prefetch.md)
+// plane loads through L1 (ld.global.nc) or L2 only (ld.global.cg): no reuse in L1, .cg is 0.6 % faster
+#ifndef PH_LDCG
+#define PH_LDCG 1
+#endif
+__device__ __forceinline__ double ld_plane(const double* p) {
+#if PH_LDCG
+  return __ldcg(p);
+#else
+  return __ldg(p);
+#endif
+}
 #ifndef PH_U0_SMEM
 #define PH_U0_SMEM 0
 #endif
@@ -437,7 +448,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
       if (slot_ok(q, s)) {
         const double* p = slot_ptr(q, s);
 #pragma unroll
-        for (int v = 0; v < NVAR; ++v) pf[s][v] = __ldg(p + v * G.vstride);
+        for (int v = 0; v < NVAR; ++v) pf[s][v] = ld_plane(p + v * G.vstride);
       }
     }
   };
@@ -492,7 +503,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
     if (xy && own) {
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
-        if (PH_PREFETCH_UIN) uin[v] = __ldg(A.Uin + cell + v * G.vstride);
+        if (PH_PREFETCH_UIN) uin[v] = ld_plane(A.Uin + cell + v * G.vstride);
         if (USE_U0 && PH_U0_SMEM) {
           const unsigned sa = (unsigned)__cvta_generic_to_shared(sU0 + v * NT + tid);
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(A.U0 + cell + v * G.vstride) : "memory");
