@@ -105,7 +105,10 @@ struct CycleState {
   long long hist_count;
 };
 
-constexpr int TILE_X = 32, TILE_Y = 8;  // stage-kernel tile (i, j); 256 threads
+#ifndef PH_TILE_Y
+#define PH_TILE_Y 8
+#endif
+constexpr int TILE_X = 32, TILE_Y = PH_TILE_Y;  // stage-kernel tile (i, j)
 
 struct StageArgs {
   const double* Uin;   // pool with valid ghosts (stage input)

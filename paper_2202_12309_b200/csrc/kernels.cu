@@ -312,7 +312,15 @@ __device__ __forceinline__ double cfl_term_rn(const double* W, const BlockMeta& 
 #ifndef PH_PREFETCH_L1
 #define PH_PREFETCH_L1 1
 #endif
-constexpr int TX = TILE_X, TY = TILE_Y, NT = TX * TY;
+// threads per CTA (>= cells per tile; extra warps take x/y face items only) and CTAs per SM
+#ifndef PH_STAGE_NT
+#define PH_STAGE_NT (TILE_X * TILE_Y)
+#endif
+#ifndef PH_STAGE_MINB
+#define PH_STAGE_MINB 2
+#endif
+constexpr int TX = TILE_X, TY = TILE_Y, NCELL = TX * TY, NT = PH_STAGE_NT;
+static_assert(NT >= NCELL && NT % 32 == 0, "stage kernel: one thread per tile column at least");
 constexpr int SWX = TX + 4, SWY = TY + 4;
 constexpr int VS = SWY * SWX;           // var stride in a ring slot
 
@@ -339,10 +347,14 @@ __device__ __forceinline__ void face_flux(const double* p0, const double* p1, co
 constexpr int SLOT = NVAR * VS;         // doubles per ring slot
 constexpr int FXS = TY * (TX + 1);      // var stride of sFx
 constexpr int FYS = (TY + 1) * TX;      // var stride of sFy
-constexpr int FZS = NT;                 // var stride of sFz
+constexpr int FZS = NCELL;              // var stride of sFz
 
 template <int RECON, bool REDUCE, bool USE_U0, bool ML, bool FULL>
-__global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
+#ifdef PH_STAGE_MAXREG
+__global__ void __maxnreg__(PH_STAGE_MAXREG) stage_kernel(StageArgs A, Geom G) {
+#else
+__global__ void __launch_bounds__(NT, PH_STAGE_MINB) stage_kernel(StageArgs A, Geom G) {
+#endif
   extern __shared__ double smem[];
   double* sW = smem;                       // [3][5][SWY][SWX]: planes q-2, q-1, q
   double* sFx = sW + 3 * SLOT;             // [5][TY][TX+1]
@@ -370,7 +382,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
   const double* Ub = A.Uin + (int64_t)slot * G.bstride;
   const double dt = A.st->dt_used;
   const double idx1 = M.idx[0], idx2 = M.idx[1], idx3 = M.idx[2];
-  const bool own = FULL || ((tx < nxt) && (ty < nyt));
+  const bool own = (NT == NCELL || tid < NCELL) && (FULL || ((tx < nxt) && (ty < nyt)));
 
   // ---- load-slot geometry: the plus-shaped halo plane is 2 cells per thread ----
   int sl_i[2], sl_j[2];
@@ -505,7 +517,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
       for (int v = 0; v < NVAR; ++v) {
         if (PH_PREFETCH_UIN) uin[v] = ld_plane(A.Uin + cell + v * G.vstride);
         if (USE_U0 && PH_U0_SMEM) {
-          const unsigned sa = (unsigned)__cvta_generic_to_shared(sU0 + v * NT + tid);
+          const unsigned sa = (unsigned)__cvta_generic_to_shared(sU0 + v * NCELL + tid);
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(A.U0 + cell + v * G.vstride) : "memory");
         } else if (USE_U0 && PH_PREFETCH_U0) {
           u0v[v] = A.U0[cell + v * G.vstride];
@@ -539,7 +551,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
       // y faces: 9 rows of 32; items rotated by 128 so the 9th row lands on warps 4-7
 #pragma unroll 1
       for (int r = 0; r < 2; ++r) {
-        const int t = ((tid + 128) & (NT - 1)) + r * NT;
+        const int t = (tid + NT / 2) % NT + r * NT;
         if (t >= TX * (TY + 1)) break;
         const int jf = t / TX, i = t - jf * TX;
         if (FULL || (jf <= nyt && i < nxt)) {
@@ -622,7 +634,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
         const double ui = PH_PREFETCH_UIN ? uin[v] : __ldg(A.Uin + cell + v * G.vstride);
         double out = fma(A.b1, ui, (A.cdt * dt) * L);
         if (USE_U0)
-          out = fma(A.a0, PH_U0_SMEM ? sU0[v * NT + tid] : (PH_PREFETCH_U0 ? u0v[v] : A.U0[cell + v * G.vstride]), out);
+          out = fma(A.a0, PH_U0_SMEM ? sU0[v * NCELL + tid] : (PH_PREFETCH_U0 ? u0v[v] : A.U0[cell + v * G.vstride]), out);
         un[v] = out;
         A.Uout[cell + v * G.vstride] = out;
       }
@@ -669,7 +681,7 @@ __global__ void __launch_bounds__(NT, 2) stage_kernel(StageArgs A, Geom G) {
 }
 
 size_t stage_smem_bytes(bool use_u0) {
-  return sizeof(double) * (3 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS + ((use_u0 && PH_U0_SMEM) ? NVAR * NT : 0));
+  return sizeof(double) * (3 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS + ((use_u0 && PH_U0_SMEM) ? NVAR * NCELL : 0));
 }
 
 // ------------------------------------------------------------------------------ exchange kernel
@@ -1378,6 +1390,13 @@ static cudaError_t launch_stage_t(int nblk_cta, const StageArgs& a, const Geom& 
     cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
+    if (getenv("PH_DEBUG_ATTR")) {
+      cudaFuncAttributes fa;
+      cudaFuncGetAttributes(&fa, stage_kernel<R, RD, U0, ML, FULL>);
+      fprintf(stderr, "stage_kernel<%d,%d,%d,%d,%d>: regs %d maxThreads %d static smem %zu local %zu dyn %zu (max dyn %d) NT %d\n",
+              R, (int)RD, (int)U0, (int)ML, (int)FULL, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
+              fa.localSizeBytes, sm, fa.maxDynamicSharedSizeBytes, NT);
+    }
     // shared-memory carveout hint (percent of the maximum); the rest of the 256 KB is L1
     if (const char* cv = getenv("PH_CARVEOUT")) {
       e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout,
