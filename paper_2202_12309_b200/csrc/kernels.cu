@@ -1298,22 +1298,52 @@ __device__ __forceinline__ double pressure_rn(const double* u, int64_t vs, doubl
   return __dmul_rn(gm1, __dsub_rn(u[4 * vs], ke));
 }
 
-__global__ void tag_kernel(const double* U, unsigned long long* eps_bits, Geom G) {
-  const int k = blockIdx.x % G.n[2];
-  const int slot = blockIdx.x / G.n[2];
+// AMR indicator (O9, A14): eps_B = max over the block of |grad p| / p with central differences, in
+// the oracle's exact operation order (flags must be bit-exact).  One CTA = a 32x8 tile of (i,j)
+// columns marching up the block; the pressure of every cell is computed once into a 3-plane smem
+// ring with a plus-shaped halo of 1 (x/y neighbours) -- the z neighbours come from the ring.
+constexpr int TGX = 32, TGY = 8, TGT = TGX * TGY, TGW = TGX + 2, TGP = (TGY + 2) * TGW;
+__global__ void __launch_bounds__(TGT) tag_kernel(const double* U, unsigned long long* eps_bits, Geom G) {
+  __shared__ double sp[3][TGP];
+  const int ntx = (G.n[0] + TGX - 1) / TGX, nty = (G.n[1] + TGY - 1) / TGY;
+  int b = blockIdx.x;
+  const int txi = b % ntx;
+  b /= ntx;
+  const int tyi = b % nty;
+  const int slot = b / nty;
+  const int x0 = txi * TGX, y0 = tyi * TGY;
+  const int nxt = min(TGX, G.n[0] - x0), nyt = min(TGY, G.n[1] - y0);
   const double* ub = U + (int64_t)slot * G.bstride;
-  const int64_t sj = G.N[0], sk = (int64_t)G.N[0] * G.N[1];
+  const int64_t vs = G.vstride;
+  const int tid = threadIdx.x, tx = tid % TGX, ty = tid / TGX;
+  const bool own = tx < nxt && ty < nyt;
   double mx = 0.0;
-  for (int c = threadIdx.x; c < G.n[0] * G.n[1]; c += blockDim.x) {
-    const int j = c / G.n[0], i = c % G.n[0];
-    const double* u = ub + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
-    const int64_t vs = G.vstride;
-    double g1 = __dmul_rn(0.5, __dsub_rn(pressure_rn(u + 1, vs, G.gm1), pressure_rn(u - 1, vs, G.gm1)));
-    double g2 = __dmul_rn(0.5, __dsub_rn(pressure_rn(u + sj, vs, G.gm1), pressure_rn(u - sj, vs, G.gm1)));
-    double g3 = __dmul_rn(0.5, __dsub_rn(pressure_rn(u + sk, vs, G.gm1), pressure_rn(u - sk, vs, G.gm1)));
-    double s = __dadd_rn(__dadd_rn(__dmul_rn(g1, g1), __dmul_rn(g2, g2)), __dmul_rn(g3, g3));
-    double e = __ddiv_rn(__dsqrt_rn(s), pressure_rn(u, vs, G.gm1));
-    mx = fmax(mx, e);
+  for (int q = -1; q <= G.n[2]; ++q) {
+    double* P = sp[(q + 3) % 3];
+    // pressures of plane q over the tile and its plus-shaped halo: (TGY+2) x (TGX+2) minus corners
+    for (int c = tid; c < TGP; c += TGT) {
+      const int j = c / TGW - 1, i = c % TGW - 1;
+      const bool xin = i >= 0 && i < nxt, yin = j >= 0 && j < nyt;
+      const bool need = (xin && j >= -1 && j <= nyt) || (yin && i >= -1 && i <= nxt);
+      if (need) {
+        const double* u = ub + ((int64_t)(q + G.g) * G.N[1] + (y0 + j + G.g)) * G.N[0] + (x0 + i + G.g);
+        P[c] = pressure_rn(u, vs, G.gm1);
+      }
+    }
+    __syncthreads();
+    const int c = q - 1;  // plane whose indicator is complete now
+    if (c >= 0 && own) {
+      const double* Pm = sp[(c + 2) % 3];
+      const double* P0 = sp[(c + 3) % 3];
+      const double* Pp = sp[(c + 4) % 3];
+      const int o = (ty + 1) * TGW + (tx + 1);
+      const double g1 = __dmul_rn(0.5, __dsub_rn(P0[o + 1], P0[o - 1]));
+      const double g2 = __dmul_rn(0.5, __dsub_rn(P0[o + TGW], P0[o - TGW]));
+      const double g3 = __dmul_rn(0.5, __dsub_rn(Pp[o], Pm[o]));
+      const double s = __dadd_rn(__dadd_rn(__dmul_rn(g1, g1), __dmul_rn(g2, g2)), __dmul_rn(g3, g3));
+      mx = fmax(mx, __ddiv_rn(__dsqrt_rn(s), P0[o]));
+    }
+    __syncthreads();
   }
   for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
   if ((threadIdx.x & 31) == 0) atomicMax(eps_bits + slot, (unsigned long long)__double_as_longlong(mx));
@@ -1596,7 +1626,8 @@ cudaError_t launch_tag(const double* U, int nslots, unsigned long long* eps_bits
   if (nslots <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(eps_bits, 0, sizeof(unsigned long long) * nslots, s);
   if (e != cudaSuccess) return e;
-  tag_kernel<<<nslots * G.n[2], 128, 0, s>>>(U, eps_bits, G);
+  const int tiles = ((G.n[0] + TGX - 1) / TGX) * ((G.n[1] + TGY - 1) / TGY);
+  tag_kernel<<<nslots * tiles, TGT, 0, s>>>(U, eps_bits, G);
   return cudaGetLastError();
 }
 
