@@ -103,6 +103,7 @@ struct ph_mesh {
   bool ghosts_stale = false;
   bool ho = false;                      // nghost 3: generic high-order path (NEXT 3)
   double *Wpool = nullptr, *Fxb = nullptr, *Fyb = nullptr, *Fzb = nullptr;
+  double* Hpool = nullptr;  // stage-2 base H = a0 U^n + b1 U^1 (uniform full-tile minmod path)
   bool overlap = false;                 // multi-GPU direct halo: interior blocks overlap the exchange
   int n_int = 0;                        // slots [0, n_int) of slot_order have no remote / physical face
   std::vector<int> slot_order;
@@ -626,6 +627,12 @@ static ph_status setup_device(ph_mesh* m) {
     TRY(dalloc(m, (void**)&m->Fzb, (size_t)ns * NVAR * nf[2] * sizeof(double)));
     m->stage_ctas = (int)(nloc * G.n[2]);
   }
+  // stage-2 base pool: on the uniform full-tile minmod path (the kernels' H template), not under
+  // flux correction (it would also have to correct H) nor AMR
+  m->Hpool = nullptr;
+  if (!m->ho && !m->multilevel && m->cfg.refinement != PH_REF_ADAPTIVE && m->cfg.recon == PH_RECON_PLM_MINMOD &&
+      G.n[0] % TX == 0 && G.n[1] % TY == 0 && !getenv("PH_NO_HBASE"))
+    TRY(dalloc(m, (void**)&m->Hpool, (size_t)std::max<int64_t>(nloc, 1) * G.bstride * sizeof(double)));
   m->partials_n = std::max<int64_t>({(int64_t)m->stage_ctas, nloc * G.n[2], 1});
   TRY(dalloc(m, (void**)&m->partials, m->partials_n * 6 * sizeof(double)));
   CU(cudaMemsetAsync(m->partials, 0, m->partials_n * 6 * sizeof(double), m->stream));
@@ -954,6 +961,12 @@ static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a
     A.KC = m->KC;
     A.cta_base = p0 * per_blk;
     A.stage = stage;
+    if (m->Hpool) {
+      const bool vl2 = m->cfg.integrator == PH_INT_VL2;
+      A.H = m->Hpool;
+      A.ha0 = vl2 ? 1.0 : 0.5;  // the stage-2 coefficients of U^n and U^1 (O5)
+      A.hb1 = vl2 ? 0.0 : 0.5;
+    }
     cudaEvent_t t0 = nullptr, t1 = nullptr;
     if (m->timing) {
       t0 = pool_event(m);

@@ -124,6 +124,10 @@ struct StageArgs {
   int ntx, nty, nkc, KC;
   int cta_base;        // offset of this launch's CTAs in partials
   int stage;
+  // uniform full-tile path: stage 1 also writes the cell-local base of stage 2,
+  // H = ha0 U^n + hb1 U^1, and stage 2 reads H instead of U^n and U^1 at the cell (null = off)
+  double* H;
+  double ha0, hb1;
 };
 
 struct XArgs {

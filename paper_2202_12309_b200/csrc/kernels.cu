@@ -35,6 +35,19 @@ __device__ __forceinline__ double minmod_i(double a, double b) {
 // stage 2: stage the finish operand U^n in shared memory with cp.async instead of holding it in
 // registers across the face phase.  Off: removes the 32 B spill but the extra 10 KB of smem per CTA
 // costs L1 and is 2.4 % slower on 2b (profiles/r01_ab_finish_prefetch.md)
+// stage 2: reduce the CFL max and the 5 totals per plane with warp shuffles into per-warp smem
+// accumulators (fixed order: plane, then warp) instead of 6 per-thread accumulators live for the
+// whole k-march -- frees 12 registers in the reducing kernel
+#ifndef PH_WARP_RED
+#define PH_WARP_RED 0
+#endif
+// timing-only decomposition knobs (wrong results; never set in a product build)
+#ifndef PH_TIMING_NO_REDUCE
+#define PH_TIMING_NO_REDUCE 0
+#endif
+#ifndef PH_TIMING_NO_U0
+#define PH_TIMING_NO_U0 0
+#endif
 // plane loads through L1 (ld.global.nc) or L2 only (ld.global.cg): no reuse in L1, .cg is 0.6 % faster
 #ifndef PH_LDCG
 #define PH_LDCG 1
@@ -349,7 +362,7 @@ constexpr int FXS = TY * (TX + 1);      // var stride of sFx
 constexpr int FYS = (TY + 1) * TX;      // var stride of sFy
 constexpr int FZS = NCELL;              // var stride of sFz
 
-template <int RECON, bool REDUCE, bool USE_U0, bool ML, bool FULL>
+template <int RECON, bool REDUCE, bool USE_U0, bool ML, bool FULL, bool HB>
 #ifdef PH_STAGE_MAXREG
 __global__ void __maxnreg__(PH_STAGE_MAXREG) stage_kernel(StageArgs A, Geom G) {
 #else
@@ -361,6 +374,7 @@ __global__ void __launch_bounds__(NT, PH_STAGE_MINB) stage_kernel(StageArgs A, G
   double* sFy = sFx + NVAR * FXS;          // [5][TY+1][TX]
   double* sFz = sFy + NVAR * FYS;          // [2][5][TY][TX]
   double* sU0 = sFz + 2 * NVAR * FZS;      // [5][TY][TX]: U^n of the cells being finished (stage 2)
+  double* sRed = sU0 + ((USE_U0 && PH_U0_SMEM) ? NVAR * NCELL : 0);  // [NT/32][6] warp accumulators
 
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
@@ -489,6 +503,8 @@ __global__ void __launch_bounds__(NT, PH_STAGE_MINB) stage_kernel(StageArgs A, G
   };
 
   double tmax = 0.0, tsum[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if (REDUCE && PH_WARP_RED && (tid & 31) == 0)
+    for (int v = 0; v < 6; ++v) sRed[(tid >> 5) * 6 + v] = 0.0;  // first read after >= 1 barrier
   double topz[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};  // z top state of plane q-2 (my column)
   const int qbeg = k0 - 2, qend = k1 + 2;
 #if PH_PREFETCH
@@ -515,8 +531,13 @@ __global__ void __launch_bounds__(NT, PH_STAGE_MINB) stage_kernel(StageArgs A, G
     if (xy && own) {
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
+        if (HB && USE_U0) {  // stage 2 of the H path: the base H is the only cell operand
+          uin[v] = ld_plane(A.H + cell + v * G.vstride);
+          continue;
+        }
         if (PH_PREFETCH_UIN) uin[v] = ld_plane(A.Uin + cell + v * G.vstride);
-        if (USE_U0 && PH_U0_SMEM) {
+        if (USE_U0 && PH_TIMING_NO_U0) {
+        } else if (USE_U0 && PH_U0_SMEM) {
           const unsigned sa = (unsigned)__cvta_generic_to_shared(sU0 + v * NCELL + tid);
           asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(A.U0 + cell + v * G.vstride) : "memory");
         } else if (USE_U0 && PH_PREFETCH_U0) {
@@ -631,27 +652,70 @@ __global__ void __launch_bounds__(NT, PH_STAGE_MINB) stage_kernel(StageArgs A, G
         double d2 = (sFy[v * FYS + (ty + 1) * TX + tx] - sFy[v * FYS + ty * TX + tx]) * idx2;
         double d3 = (fzu[v * FZS] - fzl[v * FZS]) * idx3;
         double L = -((d1 + d2) + d3);
-        const double ui = PH_PREFETCH_UIN ? uin[v] : __ldg(A.Uin + cell + v * G.vstride);
-        double out = fma(A.b1, ui, (A.cdt * dt) * L);
-        if (USE_U0)
-          out = fma(A.a0, PH_U0_SMEM ? sU0[v * NCELL + tid] : (PH_PREFETCH_U0 ? u0v[v] : A.U0[cell + v * G.vstride]), out);
+        double out;
+        if (HB && USE_U0) {
+          out = fma(A.cdt * dt, L, uin[v]);  // H + cdt dt L
+        } else {
+          const double ui = PH_PREFETCH_UIN ? uin[v] : __ldg(A.Uin + cell + v * G.vstride);
+          out = fma(A.b1, ui, (A.cdt * dt) * L);
+          if (USE_U0 && !PH_TIMING_NO_U0)
+            out = fma(A.a0, PH_U0_SMEM ? sU0[v * NCELL + tid] : (PH_PREFETCH_U0 ? u0v[v] : A.U0[cell + v * G.vstride]), out);
+          if (HB && !USE_U0) A.H[cell + v * G.vstride] = fma(A.hb1, out, A.ha0 * ui);  // stage 1: write H
+        }
         un[v] = out;
         A.Uout[cell + v * G.vstride] = out;
       }
-      if (REDUCE) {
+      if (REDUCE && !PH_TIMING_NO_REDUCE) {
         double ir = rcp_nr(un[0]);
         double v1 = un[1] * ir, v2 = un[2] * ir, v3 = un[3] * ir;
         double ke = 0.5 * ((un[1] * v1 + un[2] * v2) + un[3] * v3);
         double p = G.gm1 * (un[4] - ke);
         double cs = sound_speed(un[0], p, G.gamma);
         double s1 = (fabs(v1) + cs) * idx1, s2 = (fabs(v2) + cs) * idx2, s3 = (fabs(v3) + cs) * idx3;
-        tmax = dmax(tmax, dmax(s1, dmax(s2, s3)));
+        if (PH_WARP_RED) {
+          tmax = dmax(s1, dmax(s2, s3));  // this cell only; reduced over the warp below
 #pragma unroll
-        for (int v = 0; v < NVAR; ++v) tsum[v] += un[v];
+          for (int v = 0; v < NVAR; ++v) tsum[v] = un[v];
+        } else {
+          tmax = dmax(tmax, dmax(s1, dmax(s2, s3)));
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) tsum[v] += un[v];
+        }
       }
     }
+    if (REDUCE && PH_WARP_RED && xy) {
+      // plane c of this warp: shuffle tree, then lane 0 adds to the warp's accumulators
+#pragma unroll
+      for (int off = 16; off > 0; off >>= 1) {
+        tmax = dmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) tsum[v] += __shfl_xor_sync(0xffffffffu, tsum[v], off);
+      }
+      if ((tid & 31) == 0) {
+        double* r = sRed + (tid >> 5) * 6;
+        r[0] = dmax(r[0], tmax);
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) r[1 + v] += tsum[v];
+      }
+      tmax = 0.0;
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) tsum[v] = 0.0;
+    }
   }
-  if (REDUCE) {
+  if (REDUCE && PH_WARP_RED) {
+    __syncthreads();
+    if (tid == 0) {
+      double m = PH_TIMING_NO_REDUCE ? 1e5 : 0.0, s[NVAR] = {0, 0, 0, 0, 0};
+      for (int w = 0; w < NT / 32; ++w) {
+        m = fmax(m, sRed[w * 6]);
+        for (int v = 0; v < NVAR; ++v) s[v] += sRed[w * 6 + 1 + v];
+      }
+      double* o = A.partials + (int64_t)(A.cta_base + blockIdx.x) * 6;
+      o[0] = m;
+      for (int v = 0; v < NVAR; ++v) o[1 + v] = s[v] * M.dV;
+    }
+  } else if (REDUCE) {
+    if (PH_TIMING_NO_REDUCE) tmax = 1e5;  // timing-only: keep dt finite and small
     // deterministic CTA reduction: warp shuffles then thread 0 in fixed warp order
     __syncthreads();
     double* red = smem;
@@ -681,7 +745,8 @@ __global__ void __launch_bounds__(NT, PH_STAGE_MINB) stage_kernel(StageArgs A, G
 }
 
 size_t stage_smem_bytes(bool use_u0) {
-  return sizeof(double) * (3 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS + ((use_u0 && PH_U0_SMEM) ? NVAR * NCELL : 0));
+  return sizeof(double) * (3 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS + ((use_u0 && PH_U0_SMEM) ? NVAR * NCELL : 0) +
+                           (PH_WARP_RED ? 6 * (NT / 32) : 0));
 }
 
 // ------------------------------------------------------------------------------ exchange kernel
@@ -1412,30 +1477,30 @@ __global__ void remesh_kernel(const RemeshTask* tasks, const double* Uold, doubl
 // ------------------------------------------------------------------------------ launchers
 #define PH_CHECK_LAUNCH() cudaGetLastError()
 
-template <int R, bool RD, bool U0, bool ML, bool FULL>
+template <int R, bool RD, bool U0, bool ML, bool FULL, bool HB = false>
 static cudaError_t launch_stage_t(int nblk_cta, const StageArgs& a, const Geom& G, cudaStream_t s) {
   const size_t sm = stage_smem_bytes(U0);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL>,
+    cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     if (getenv("PH_DEBUG_ATTR")) {
       cudaFuncAttributes fa;
-      cudaFuncGetAttributes(&fa, stage_kernel<R, RD, U0, ML, FULL>);
+      cudaFuncGetAttributes(&fa, stage_kernel<R, RD, U0, ML, FULL, HB>);
       fprintf(stderr, "stage_kernel<%d,%d,%d,%d,%d>: regs %d maxThreads %d static smem %zu local %zu dyn %zu (max dyn %d) NT %d\n",
               R, (int)RD, (int)U0, (int)ML, (int)FULL, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
               fa.localSizeBytes, sm, fa.maxDynamicSharedSizeBytes, NT);
     }
     // shared-memory carveout hint (percent of the maximum); the rest of the 256 KB is L1
     if (const char* cv = getenv("PH_CARVEOUT")) {
-      e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL>, cudaFuncAttributePreferredSharedMemoryCarveout,
+      e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                atoi(cv));
       if (e != cudaSuccess) return e;
     }
     attr = true;
   }
-  stage_kernel<R, RD, U0, ML, FULL><<<nblk_cta, NT, sm, s>>>(a, G);
+  stage_kernel<R, RD, U0, ML, FULL, HB><<<nblk_cta, NT, sm, s>>>(a, G);
   return cudaGetLastError();
 }
 
@@ -1443,6 +1508,8 @@ template <int R, bool RD, bool U0>
 static cudaError_t launch_stage_ml(bool ml, int n, const StageArgs& a, const Geom& G, cudaStream_t s) {
   // full-tile fast path (block extents multiples of the tile): minmod, uniform-level meshes
   const bool full = (R == 0) && !ml && (G.n[0] % TX == 0) && (G.n[1] % TY == 0);
+  if (full && a.H) return launch_stage_t<0, RD, U0, false, true, true>(n, a, G, s);
+  if (a.H) return cudaErrorInvalidValue;  // the host enables H only where the full-tile path runs
   if (full) return launch_stage_t<0, RD, U0, false, true>(n, a, G, s);
   return ml ? launch_stage_t<R, RD, U0, true, false>(n, a, G, s) : launch_stage_t<R, RD, U0, false, false>(n, a, G, s);
 }
