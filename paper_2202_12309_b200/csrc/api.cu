@@ -150,6 +150,12 @@ struct ph_mesh {
   // boundary-first schedule of the multi-GPU cycle: B (high priority) runs boundary blocks and the
   // halo, I runs interior blocks concurrently
   cudaStream_t bstream = nullptr, istream = nullptr;
+  // concurrent packs (NEXT 4; the paper's best GPU setting is 2 packs per rank): when a
+  // stage is split into several pack launches they rotate over the caller's stream and pstream[]
+  static constexpr int kMaxPackStreams = 8;
+  int pack_streams = 8;
+  cudaStream_t pstream[kMaxPackStreams] = {};
+  cudaEvent_t ev_pfork = nullptr, ev_pjoin[kMaxPackStreams] = {};
   cudaEvent_t ev_a = nullptr, ev_b1 = nullptr, ev_i1 = nullptr, ev_b2 = nullptr, ev_i2 = nullptr;
 };
 
@@ -940,8 +946,26 @@ static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a
     return PH_OK;
   }
   const int per_blk = m->ntx * m->nty * m->nkc;
-  for (int p0 = s0; p0 < s1; p0 += m->pack_size) {
+  const cudaStream_t S = m->stream;
+  const int npacks = (s1 - s0 + m->pack_size - 1) / std::max(m->pack_size, 1);
+  const int nps = std::min(std::min(m->pack_streams, (int)ph_mesh::kMaxPackStreams), npacks);
+  const bool multi = nps > 1 && !m->timing;
+  if (multi) {
+    if (!m->ev_pfork) CU(cudaEventCreateWithFlags(&m->ev_pfork, cudaEventDisableTiming));
+    CU(cudaEventRecord(m->ev_pfork, S));
+    for (int i = 1; i < nps; ++i) {
+      if (!m->pstream[i]) {
+        CU(cudaStreamCreateWithFlags(&m->pstream[i], cudaStreamNonBlocking));
+        CU(cudaEventCreateWithFlags(&m->ev_pjoin[i], cudaEventDisableTiming));
+      }
+      CU(cudaStreamWaitEvent(m->pstream[i], m->ev_pfork, 0));
+    }
+  }
+  int ipack = 0;
+  for (int p0 = s0; p0 < s1; p0 += m->pack_size, ++ipack) {
     int np = std::min(m->pack_size, s1 - p0);
+    // packs rotate over the streams: packs of one stage write disjoint blocks and partials
+    const cudaStream_t ps = (multi && (ipack % nps)) ? m->pstream[ipack % nps] : S;
     StageArgs A{};
     A.Uin = Uin;
     A.U0 = m->U0;
@@ -973,11 +997,17 @@ static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a
       t1 = pool_event(m);
       CU(cudaEventRecord(t0, m->stream));
     }
-    CU(launch_stage(m->cfg.recon, reduce, a0 != 0.0, np * per_blk, A, m->G, m->stream));
+    CU(launch_stage(m->cfg.recon, reduce, a0 != 0.0, np * per_blk, A, m->G, ps));
     m->launches++;
     if (m->timing) {
       CU(cudaEventRecord(t1, m->stream));
       m->t_stage.push_back({t0, t1});
+    }
+  }
+  if (multi) {
+    for (int i = 1; i < nps; ++i) {
+      CU(cudaEventRecord(m->ev_pjoin[i], m->pstream[i]));
+      CU(cudaStreamWaitEvent(S, m->ev_pjoin[i], 0));
     }
   }
   if (m->multilevel && post) {
@@ -1373,6 +1403,7 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
   m->host_only = cfg->host_only != 0;
   m->no_direct_halo = cfg->no_direct_halo != 0;
   m->use_graph = !(getenv("PH_NO_GRAPH") && atoi(getenv("PH_NO_GRAPH")) != 0);
+  if (getenv("PH_PACK_STREAMS")) m->pack_streams = atoi(getenv("PH_PACK_STREAMS"));
   Geom& G = m->G;
   G.g = cfg->nghost;
   G.cg = (G.g + 1) / 2 + 1;
@@ -1506,6 +1537,11 @@ ph_status ph_mesh_destroy(ph_mesh* m) {
   if (m->ev_comm) cudaEventDestroy(m->ev_comm);
   if (m->comm_stream) cudaStreamDestroy(m->comm_stream);
   if (m->bstream) cudaStreamDestroy(m->bstream);
+  for (int i = 0; i < ph_mesh::kMaxPackStreams; ++i) {
+    if (m->pstream[i]) cudaStreamDestroy(m->pstream[i]);
+    if (m->ev_pjoin[i]) cudaEventDestroy(m->ev_pjoin[i]);
+  }
+  if (m->ev_pfork) cudaEventDestroy(m->ev_pfork);
   if (m->istream) cudaStreamDestroy(m->istream);
   for (cudaEvent_t e : {m->ev_a, m->ev_b1, m->ev_i1, m->ev_b2, m->ev_i2})
     if (e) cudaEventDestroy(e);
