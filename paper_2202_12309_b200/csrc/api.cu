@@ -290,7 +290,7 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
       const BlockInfo& s = m->blocks[e.gid];
       bool dst_here = (b.rank == me), src_here = (s.rank == me);
       if (!dst_here && !src_here) continue;
-      if (cyc) {
+      if (cyc && !b.has_coarser) {  // destination without coarse staging (all blocks of a uniform mesh)
         int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
         if (nz > 1) continue;                               // edges / corners: never read
         if (dst_here && src_here && e.dlevel == 0) continue;  // read directly by the stage kernel
@@ -412,7 +412,7 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
         if (q == 13) continue;
         int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
         if (!region_physical(b, o)) continue;
-        if (cyc && ((o[0] != 0) + (o[1] != 0) + (o[2] != 0)) > 1) continue;
+        if (cyc && !b.has_coarser && ((o[0] != 0) + (o[1] != 0) + (o[2] != 0)) > 1) continue;
         XTask r{};
         r.kind = T_BC_FINE;
         r.dst_slot = (int)b.local;
@@ -464,7 +464,10 @@ static ph_status build_plan(ph_mesh* m) {
   }
   m->ho = m->G.g == 3;
   m->G.exact = m->ho ? 1 : 0;
-  m->direct_halo = !m->multilevel && !m->no_direct_halo && m->cfg.refinement != PH_REF_ADAPTIVE && !m->ho;
+  // direct halo: stage kernels (and the AMR tag kernel) of blocks without a coarser neighbour read
+  // their local same-level face neighbours' interiors; blocks with coarse staging keep every ghost
+  // (their staging restricts first-layer ghosts incl. edges and corners, O7 B)
+  m->direct_halo = !m->no_direct_halo && !m->ho;
   build_exchange(m, m->plan[0], false, cslot);
   build_exchange(m, m->plan[1], m->direct_halo, cslot);
   // reflux tasks (coarse side) and, across ranks, the fine-side flux packs (O8).
@@ -554,7 +557,7 @@ static ph_status build_plan(ph_mesh* m) {
       M.fslot[f] = fslot[b.gid][f];
       M.nb[f] = -1;
     }
-    if (m->direct_halo) {
+    if (m->direct_halo && !b.has_coarser) {
       for (auto& e : b.nbrs) {
         int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
         if (nz != 1 || e.dlevel != 0 || m->blocks[e.gid].rank != me) continue;
@@ -565,7 +568,7 @@ static ph_status build_plan(ph_mesh* m) {
   }
   // stage launch order: with the multi-GPU direct halo, blocks that have no remote or physical
   // face come first so their stage can run while the halo exchange is in flight
-  m->overlap = m->direct_halo && m->nranks > 1;
+  m->overlap = m->direct_halo && m->nranks > 1 && !m->multilevel && m->cfg.refinement != PH_REF_ADAPTIVE;
   m->slot_order.clear();
   std::vector<int> bnd;
   for (int64_t s = 0; s < nloc; ++s) {
@@ -1306,7 +1309,7 @@ static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, 
   const int R = m->nranks;
   const int64_t nglob = (int64_t)m->blocks.size();
   const int64_t maxloc = (nglob + R - 1) / R;
-  CU(launch_tag(m->U0, nloc, m->d_eps, m->G, m->stream));
+  CU(launch_tag(m->U0, m->d_meta, nloc, m->d_eps, m->G, m->stream));
   m->launches++;
   std::vector<unsigned long long> bits((size_t)maxloc * R, 0ull);
   if (R > 1) {
@@ -1340,6 +1343,8 @@ static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, 
   if (!any) return PH_OK;
   std::unordered_set<LocKey> nl = normalize_flags(*m->tree, locs, flags, allow_deref && !refine_only);
   if (nl == m->tree->leaves()) return PH_OK;
+  // the prolongation of refined parents reads their ghosts (A11): materialise every ghost first
+  if (move && m->direct_halo) TRY(exchange(m, m->U0, 0));
   TRY(remesh(m, nl, move));
   *changed = true;
   return PH_OK;

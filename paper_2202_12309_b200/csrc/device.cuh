@@ -184,7 +184,8 @@ cudaError_t launch_finalize(const double* all, int nranks, CycleState* st, doubl
 cudaError_t launch_cycle_begin(CycleState* st, double tlim, int set_tlim, cudaStream_t s);
 cudaError_t launch_interior_copy(double* U, double* buf, int slot0, int nslots, int to_pool, const Geom& G,
                                  cudaStream_t s);
-cudaError_t launch_tag(const double* U, int nslots, unsigned long long* eps_bits, const Geom& G, cudaStream_t s);
+cudaError_t launch_tag(const double* U, const BlockMeta* meta, int nslots, unsigned long long* eps_bits, const Geom& G,
+                       cudaStream_t s);
 cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, double* Unew, const double* rbuf,
                           double* sbuf, const Geom& G, cudaStream_t s);
 cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslots, const StageArgs& a, double* W,

@@ -1368,7 +1368,8 @@ __device__ __forceinline__ double pressure_rn(const double* u, int64_t vs, doubl
 // columns marching up the block; the pressure of every cell is computed once into a 3-plane smem
 // ring with a plus-shaped halo of 1 (x/y neighbours) -- the z neighbours come from the ring.
 constexpr int TGX = 32, TGY = 8, TGT = TGX * TGY, TGW = TGX + 2, TGP = (TGY + 2) * TGW;
-__global__ void __launch_bounds__(TGT) tag_kernel(const double* U, unsigned long long* eps_bits, Geom G) {
+__global__ void __launch_bounds__(TGT) tag_kernel(const double* U, const BlockMeta* meta, unsigned long long* eps_bits,
+                                                  Geom G) {
   __shared__ double sp[3][TGP];
   const int ntx = (G.n[0] + TGX - 1) / TGX, nty = (G.n[1] + TGY - 1) / TGY;
   int b = blockIdx.x;
@@ -1379,21 +1380,34 @@ __global__ void __launch_bounds__(TGT) tag_kernel(const double* U, unsigned long
   const int x0 = txi * TGX, y0 = tyi * TGY;
   const int nxt = min(TGX, G.n[0] - x0), nyt = min(TGY, G.n[1] - y0);
   const double* ub = U + (int64_t)slot * G.bstride;
+  const BlockMeta& M = meta[slot];
   const int64_t vs = G.vstride;
   const int tid = threadIdx.x, tx = tid % TGX, ty = tid / TGX;
+  // cell (i,j,q) of this block, or -- direct halo -- of the same-level face neighbour it lies in
+  // (the plus-shaped stencil has at most one coordinate outside the block)
+  auto at = [&](int i, int j, int q) -> const double* {
+    int b = slot;
+    if (i < 0 && M.nb[0] >= 0) { b = M.nb[0]; i += G.n[0]; }
+    else if (i >= G.n[0] && M.nb[1] >= 0) { b = M.nb[1]; i -= G.n[0]; }
+    else if (j < 0 && M.nb[2] >= 0) { b = M.nb[2]; j += G.n[1]; }
+    else if (j >= G.n[1] && M.nb[3] >= 0) { b = M.nb[3]; j -= G.n[1]; }
+    else if (q < 0 && M.nb[4] >= 0) { b = M.nb[4]; q += G.n[2]; }
+    else if (q >= G.n[2] && M.nb[5] >= 0) { b = M.nb[5]; q -= G.n[2]; }
+    return U + (int64_t)b * G.bstride + ((int64_t)(q + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+  };
+  (void)ub;
   const bool own = tx < nxt && ty < nyt;
   double mx = 0.0;
   for (int q = -1; q <= G.n[2]; ++q) {
     double* P = sp[(q + 3) % 3];
-    // pressures of plane q over the tile and its plus-shaped halo: (TGY+2) x (TGX+2) minus corners
+    // pressures of plane q over the tile and its plus-shaped halo: (TGY+2) x (TGX+2) minus corners;
+    // the z ghost planes (q = -1, n3) only at the tile's own columns
+    const bool zghost = q < 0 || q >= G.n[2];
     for (int c = tid; c < TGP; c += TGT) {
       const int j = c / TGW - 1, i = c % TGW - 1;
       const bool xin = i >= 0 && i < nxt, yin = j >= 0 && j < nyt;
-      const bool need = (xin && j >= -1 && j <= nyt) || (yin && i >= -1 && i <= nxt);
-      if (need) {
-        const double* u = ub + ((int64_t)(q + G.g) * G.N[1] + (y0 + j + G.g)) * G.N[0] + (x0 + i + G.g);
-        P[c] = pressure_rn(u, vs, G.gm1);
-      }
+      const bool need = zghost ? (xin && yin) : ((xin && j >= -1 && j <= nyt) || (yin && i >= -1 && i <= nxt));
+      if (need) P[c] = pressure_rn(at(x0 + i, y0 + j, q), vs, G.gm1);
     }
     __syncthreads();
     const int c = q - 1;  // plane whose indicator is complete now
@@ -1689,12 +1703,13 @@ cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslo
   return cudaGetLastError();
 }
 
-cudaError_t launch_tag(const double* U, int nslots, unsigned long long* eps_bits, const Geom& G, cudaStream_t s) {
+cudaError_t launch_tag(const double* U, const BlockMeta* meta, int nslots, unsigned long long* eps_bits, const Geom& G,
+                       cudaStream_t s) {
   if (nslots <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(eps_bits, 0, sizeof(unsigned long long) * nslots, s);
   if (e != cudaSuccess) return e;
   const int tiles = ((G.n[0] + TGX - 1) / TGX) * ((G.n[1] + TGY - 1) / TGY);
-  tag_kernel<<<nslots * tiles, TGT, 0, s>>>(U, eps_bits, G);
+  tag_kernel<<<nslots * tiles, TGT, 0, s>>>(U, meta, eps_bits, G);
   return cudaGetLastError();
 }
 

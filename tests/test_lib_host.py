@@ -132,10 +132,15 @@ def test_direct_halo_cycle_plan(P):
     # uniform periodic single rank: the per-cycle exchange is empty (all faces read directly)
     info = P.Mesh(host_only=True, mesh_nx=(64, 64, 64), block_nx=(16, 16, 16)).plan_info()
     assert info["direct_halo"] and info["n_cyc_local_tasks"] == 0
-    # outflow: only physical-boundary tasks remain; multilevel: direct halo is off
-    info = P.Mesh(host_only=True, mesh_nx=(64, 64, 64), block_nx=(16, 16, 16), max_level=1, refinement=1,
-                  regions=[(1, 0.1, 0.3, 0.1, 0.3, 0.1, 0.3)]).plan_info()
-    assert not info["direct_halo"]
+    # multilevel: blocks without a coarser neighbour read their same-level local faces directly and
+    # drop edge / corner ghosts; blocks with coarse staging keep every entry.  The per-cycle plan is
+    # therefore a strict subset of the full one, and the direct halo can be switched off.
+    ml = dict(mesh_nx=(64, 64, 64), block_nx=(16, 16, 16), max_level=1, refinement=1,
+              regions=[(1, 0.1, 0.3, 0.1, 0.3, 0.1, 0.3)])
+    info = P.Mesh(host_only=True, **ml).plan_info()
+    assert info["direct_halo"] and 0 < info["n_cyc_local_tasks"] < info["n_local_tasks"]
+    off = P.Mesh(host_only=True, direct_halo=False, **ml).plan_info()
+    assert not off["direct_halo"] and off["n_cyc_local_tasks"] == off["n_local_tasks"] == info["n_local_tasks"]
     # multi-rank uniform, NCCL halo: the cycle plan keeps only remote faces, symmetric across ranks
     R = 4
     kw = dict(mesh_nx=(128, 64, 64), block_nx=(16, 16, 16), halo_transport=P.HALO_NCCL)
