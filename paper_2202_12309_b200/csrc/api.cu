@@ -642,7 +642,7 @@ static ph_status setup_device(ph_mesh* m) {
   if (!m->ho && !m->multilevel && m->cfg.refinement != PH_REF_ADAPTIVE && m->cfg.recon == PH_RECON_PLM_MINMOD &&
       G.n[0] % TX == 0 && G.n[1] % TY == 0 && !getenv("PH_NO_HBASE"))
     TRY(dalloc(m, (void**)&m->Hpool, (size_t)std::max<int64_t>(nloc, 1) * G.bstride * sizeof(double)));
-  m->partials_n = std::max<int64_t>({(int64_t)m->stage_ctas, nloc * G.n[2], 1});
+  m->partials_n = std::max<int64_t>({(int64_t)m->stage_ctas, nloc * G.n[2], nloc * tag_ctas_per_block(G), 1});
   TRY(dalloc(m, (void**)&m->partials, m->partials_n * 6 * sizeof(double)));
   CU(cudaMemsetAsync(m->partials, 0, m->partials_n * 6 * sizeof(double), m->stream));
   {
@@ -1098,6 +1098,7 @@ static ph_status one_cycle(ph_mesh* m) {
     TRY(run_stage(m, m->U1, m->U0, 0.5, 0.5, 0.5, fuse_reduce, 2));
   }
   TRY(exchange(m, m->U0, 1));
+  bool tag_partials = false;  // the tag pass also reduced dt / totals of the unchanged mesh
   if (adaptive) {
     // O5 step 6: tag after the cycle, remesh, exchange; dt and totals on the new mesh
     CycleState st;
@@ -1109,9 +1110,11 @@ static ph_status one_cycle(ph_mesh* m) {
       bool changed = false;
       TRY(tag_and_remesh(m, false, gate, true, &changed));
       if (changed) TRY(exchange(m, m->U0, 0));
+      tag_partials = !changed;
     }
   }
   if (fuse_reduce) TRY(reduce_finalize(m, nloc > 0 ? m->stage_ctas : 0, 1));
+  else if (tag_partials) TRY(reduce_finalize(m, nloc * tag_ctas_per_block(m->G), 1));
   else TRY(standalone_reduce(m, m->U0, 1));
   return PH_OK;
 }
@@ -1309,7 +1312,7 @@ static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, 
   const int R = m->nranks;
   const int64_t nglob = (int64_t)m->blocks.size();
   const int64_t maxloc = (nglob + R - 1) / R;
-  CU(launch_tag(m->U0, m->d_meta, nloc, m->d_eps, m->G, m->stream));
+  CU(launch_tag(m->U0, m->d_meta, nloc, m->d_eps, m->partials, m->d_err, m->G, m->stream));
   m->launches++;
   std::vector<unsigned long long> bits((size_t)maxloc * R, 0ull);
   if (R > 1) {

@@ -184,8 +184,11 @@ cudaError_t launch_finalize(const double* all, int nranks, CycleState* st, doubl
 cudaError_t launch_cycle_begin(CycleState* st, double tlim, int set_tlim, cudaStream_t s);
 cudaError_t launch_interior_copy(double* U, double* buf, int slot0, int nslots, int to_pool, const Geom& G,
                                  cudaStream_t s);
-cudaError_t launch_tag(const double* U, const BlockMeta* meta, int nslots, unsigned long long* eps_bits, const Geom& G,
-                       cudaStream_t s);
+// AMR indicator per block; with partials != null also the dt / totals partials of U (one row of 6
+// per CTA, tag_ctas_per_block(G) CTAs per block, same layout as reduce_kernel)
+cudaError_t launch_tag(const double* U, const BlockMeta* meta, int nslots, unsigned long long* eps_bits,
+                       double* partials, ErrWord* err, const Geom& G, cudaStream_t s);
+int tag_ctas_per_block(const Geom& G);
 cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, double* Unew, const double* rbuf,
                           double* sbuf, const Geom& G, cudaStream_t s);
 cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslots, const StageArgs& a, double* W,

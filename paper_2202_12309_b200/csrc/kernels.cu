@@ -1369,8 +1369,10 @@ __device__ __forceinline__ double pressure_rn(const double* u, int64_t vs, doubl
 // ring with a plus-shaped halo of 1 (x/y neighbours) -- the z neighbours come from the ring.
 constexpr int TGX = 32, TGY = 8, TGT = TGX * TGY, TGW = TGX + 2, TGP = (TGY + 2) * TGW;
 __global__ void __launch_bounds__(TGT) tag_kernel(const double* U, const BlockMeta* meta, unsigned long long* eps_bits,
-                                                  Geom G) {
+                                                  double* partials, ErrWord* err, Geom G) {
   __shared__ double sp[3][TGP];
+  __shared__ double red[TGT / 32][6];
+  double tmax = 0.0, ts[NVAR] = {0, 0, 0, 0, 0};  // dt / totals partials of this tile (a6, a10)
   const int ntx = (G.n[0] + TGX - 1) / TGX, nty = (G.n[1] + TGY - 1) / TGY;
   int b = blockIdx.x;
   const int txi = b % ntx;
@@ -1398,17 +1400,57 @@ __global__ void __launch_bounds__(TGT) tag_kernel(const double* U, const BlockMe
   (void)ub;
   const bool own = tx < nxt && ty < nyt;
   double mx = 0.0;
+  // plane loads are prefetched one plane ahead (2 cells per thread of the plus-shaped tile plane)
+  constexpr int NS = (TGP + TGT - 1) / TGT;
+  double uq[NS][NVAR];
+  auto need_cell = [&](int c, int q, int& i, int& j) -> bool {
+    j = c / TGW - 1;
+    i = c % TGW - 1;
+    if (c >= TGP) return false;
+    const bool xin = i >= 0 && i < nxt, yin = j >= 0 && j < nyt;
+    // the z ghost planes (q = -1, n3) only at the tile's own columns
+    return (q < 0 || q >= G.n[2]) ? (xin && yin) : ((xin && j >= -1 && j <= nyt) || (yin && i >= -1 && i <= nxt));
+  };
+  auto load_plane = [&](int q) {
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      int i, j;
+      if (need_cell(tid + s * TGT, q, i, j)) {
+        const double* u = at(x0 + i, y0 + j, q);
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) uq[s][v] = u[v * vs];
+      }
+    }
+  };
+  load_plane(-1);
   for (int q = -1; q <= G.n[2]; ++q) {
     double* P = sp[(q + 3) % 3];
-    // pressures of plane q over the tile and its plus-shaped halo: (TGY+2) x (TGX+2) minus corners;
-    // the z ghost planes (q = -1, n3) only at the tile's own columns
-    const bool zghost = q < 0 || q >= G.n[2];
-    for (int c = tid; c < TGP; c += TGT) {
-      const int j = c / TGW - 1, i = c % TGW - 1;
-      const bool xin = i >= 0 && i < nxt, yin = j >= 0 && j < nyt;
-      const bool need = zghost ? (xin && yin) : ((xin && j >= -1 && j <= nyt) || (yin && i >= -1 && i <= nxt));
-      if (need) P[c] = pressure_rn(at(x0 + i, y0 + j, q), vs, G.gm1);
+    // pressures of plane q over the tile and its plus-shaped halo, in the oracle's exact order
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      int i, j;
+      const int c = tid + s * TGT;
+      if (!need_cell(c, q, i, j)) continue;
+      const double* un = uq[s];
+      const double ir = __ddiv_rn(1.0, un[0]);
+      const double v1 = __dmul_rn(un[1], ir), v2 = __dmul_rn(un[2], ir), v3 = __dmul_rn(un[3], ir);
+      const double ke = __dmul_rn(0.5, __dadd_rn(__dadd_rn(__dmul_rn(un[1], v1), __dmul_rn(un[2], v2)), __dmul_rn(un[3], v3)));
+      P[c] = __dmul_rn(G.gm1, __dsub_rn(un[4], ke));
+      if (partials && q >= 0 && q < G.n[2] && i >= 0 && i < nxt && j >= 0 && j < nyt) {
+        // dt / totals of the tile's own cells (the standalone reduction's arithmetic)
+        const double fr = rcp_nr(un[0]);
+        const double w1 = un[1] * fr, w2 = un[2] * fr, w3 = un[3] * fr;
+        const double fke = 0.5 * ((un[1] * w1 + un[2] * w2) + un[3] * w3);
+        const double p = G.gm1 * (un[4] - fke);
+        if (!(un[0] > 0.0) || !(p > 0.0)) set_error(err, 0, M.gid, q, y0 + j, x0 + i);
+        const double cs = sound_speed(un[0], p, G.gamma);
+        const double s1 = (fabs(w1) + cs) * M.idx[0], s2 = (fabs(w2) + cs) * M.idx[1], s3 = (fabs(w3) + cs) * M.idx[2];
+        tmax = dmax(tmax, dmax(s1, dmax(s2, s3)));
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) ts[v] += un[v];
+      }
     }
+    if (q < G.n[2]) load_plane(q + 1);
     __syncthreads();
     const int c = q - 1;  // plane whose indicator is complete now
     if (c >= 0 && own) {
@@ -1426,7 +1468,32 @@ __global__ void __launch_bounds__(TGT) tag_kernel(const double* U, const BlockMe
   }
   for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
   if ((threadIdx.x & 31) == 0) atomicMax(eps_bits + slot, (unsigned long long)__double_as_longlong(mx));
+  if (partials) {  // deterministic: warp shuffles, then thread 0 in warp order
+    for (int off = 16; off > 0; off >>= 1) {
+      tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) ts[v] += __shfl_xor_sync(0xffffffffu, ts[v], off);
+    }
+    const int warp = tid / 32, lane = tid % 32;
+    if (lane == 0) {
+      red[warp][0] = tmax;
+      for (int v = 0; v < NVAR; ++v) red[warp][1 + v] = ts[v];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double m = 0.0, s[NVAR] = {0, 0, 0, 0, 0};
+      for (int w = 0; w < TGT / 32; ++w) {
+        m = fmax(m, red[w][0]);
+        for (int v = 0; v < NVAR; ++v) s[v] += red[w][1 + v];
+      }
+      double* o = partials + (int64_t)blockIdx.x * 6;
+      o[0] = m;
+      for (int v = 0; v < NVAR; ++v) o[1 + v] = s[v] * M.dV;
+    }
+  }
 }
+
+int tag_ctas_per_block(const Geom& G) { return ((G.n[0] + TGX - 1) / TGX) * ((G.n[1] + TGY - 1) / TGY); }
 
 // new pool <- old pool (see RemeshTask): same-level move, 8-child prolongation of a refined parent
 // using the parent's valid ghosts for the slopes (A11), pairwise restriction of derefined
@@ -1703,13 +1770,13 @@ cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslo
   return cudaGetLastError();
 }
 
-cudaError_t launch_tag(const double* U, const BlockMeta* meta, int nslots, unsigned long long* eps_bits, const Geom& G,
-                       cudaStream_t s) {
+cudaError_t launch_tag(const double* U, const BlockMeta* meta, int nslots, unsigned long long* eps_bits,
+                       double* partials, ErrWord* err, const Geom& G, cudaStream_t s) {
   if (nslots <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(eps_bits, 0, sizeof(unsigned long long) * nslots, s);
   if (e != cudaSuccess) return e;
   const int tiles = ((G.n[0] + TGX - 1) / TGX) * ((G.n[1] + TGY - 1) / TGY);
-  tag_kernel<<<nslots * tiles, TGT, 0, s>>>(U, meta, eps_bits, G);
+  tag_kernel<<<nslots * tiles, TGT, 0, s>>>(U, meta, eps_bits, partials, err, G);
   return cudaGetLastError();
 }
 
