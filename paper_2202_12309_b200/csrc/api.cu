@@ -1038,7 +1038,8 @@ static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a
   return PH_OK;
 }
 
-static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, bool move, bool* changed);
+static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, bool move, bool* changed,
+                                int deref_interval = 0);
 
 static ph_status one_cycle(ph_mesh* m) {
   CU(launch_cycle_begin(m->d_st, 0.0, 0, m->stream));
@@ -1100,18 +1101,13 @@ static ph_status one_cycle(ph_mesh* m) {
   TRY(exchange(m, m->U0, 1));
   bool tag_partials = false;  // the tag pass also reduced dt / totals of the unchanged mesh
   if (adaptive) {
-    // O5 step 6: tag after the cycle, remesh, exchange; dt and totals on the new mesh
-    CycleState st;
-    CU(cudaMemcpyAsync(&st, m->d_st, sizeof st, cudaMemcpyDeviceToHost, m->stream));
-    CU(cudaStreamSynchronize(m->stream));
-    if (st.active) {
-      const int iv = m->cfg.derefine_interval > 0 ? m->cfg.derefine_interval : 1;
-      const bool gate = ((st.cycle + 1) % iv) == 0;  // P:580, A16 (cycle after increment)
-      bool changed = false;
-      TRY(tag_and_remesh(m, false, gate, true, &changed));
-      if (changed) TRY(exchange(m, m->U0, 0));
-      tag_partials = !changed;
-    }
+    // O5 step 6: tag after the cycle, remesh, exchange; dt and totals on the new mesh.  The cycle
+    // state (active, cycle count for the derefinement gate) is read back in the tag pass's sync.
+    const int iv = m->cfg.derefine_interval > 0 ? m->cfg.derefine_interval : 1;
+    bool changed = false;
+    TRY(tag_and_remesh(m, false, false, true, &changed, iv));
+    if (changed) TRY(exchange(m, m->U0, 0));
+    tag_partials = !changed;
   }
   if (fuse_reduce) TRY(reduce_finalize(m, nloc > 0 ? m->stage_ctas : 0, 1));
   else if (tag_partials) TRY(reduce_finalize(m, nloc * tag_ctas_per_block(m->G), 1));
@@ -1306,7 +1302,11 @@ static ph_status remesh(ph_mesh* m, const std::unordered_set<LocKey>& leaves, bo
 
 /* Tag every local block (eps_B, A14), gather the indicators of all ranks, normalise the flags
  * (O9) identically on every rank and install the new mesh if it changed. */
-static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, bool move, bool* changed) {
+/* deref_interval > 0: per-cycle call; the cycle state is read in the same sync as the indicators,
+ * inactive cycles (t >= tlim) change nothing, and derefinement is allowed when the cycle count after
+ * this cycle's increment is a multiple of the interval (A16). */
+static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, bool move, bool* changed,
+                                int deref_interval) {
   *changed = false;
   const int nloc = (int)m->local_gids.size();
   const int R = m->nranks;
@@ -1322,7 +1322,13 @@ static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, 
   } else if (nloc) {
     CU(cudaMemcpyAsync(bits.data(), m->d_eps, nloc * sizeof(unsigned long long), cudaMemcpyDeviceToHost, m->stream));
   }
+  CycleState st{};
+  if (deref_interval > 0) CU(cudaMemcpyAsync(&st, m->d_st, sizeof st, cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
+  if (deref_interval > 0) {
+    if (!st.active) return PH_OK;
+    allow_deref = ((st.cycle + 1) % deref_interval) == 0;
+  }
   std::vector<Loc> locs;
   std::vector<int8_t> flags;
   for (int r = 0; r < R; ++r) {
@@ -1341,8 +1347,10 @@ static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, 
     }
   }
   if (!refine_only) m->last_flags = flags;
+  // nothing can change without a refinement request, or a derefinement request on a gate cycle
   bool any = false;
-  for (int8_t f : flags) any = any || f != 0;
+  const bool deref_ok = allow_deref && !refine_only;
+  for (int8_t f : flags) any = any || f > 0 || (f < 0 && deref_ok);
   if (!any) return PH_OK;
   std::unordered_set<LocKey> nl = normalize_flags(*m->tree, locs, flags, allow_deref && !refine_only);
   if (nl == m->tree->leaves()) return PH_OK;
