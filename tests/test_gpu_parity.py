@@ -96,6 +96,16 @@ def test_limiters_and_vl2(oracle_mod, P, recon, integ):
     _check_run(o, g)
 
 
+@pytest.mark.parametrize("integ", [0, 1])
+def test_full_tile_stage2_base(oracle_mod, P, integ):
+    """32^3 blocks take the full-tile path where stage 1 also writes the stage-2 base H = a0 U^n + b1 U^1
+    (RK2: 1/2, 1/2; VL2: 1, 0) and stage 2 reads H instead of U^n and U^1 at the cell"""
+    o, g = _run_both(oracle_mod, P, P.BLAST, [10.0, 0.1, 0.2, 0.1, -0.05, 0.0], 8, integrator=integ,
+                     mesh_nx=(64, 64, 32), block_nx=(32, 32, 32), xmin=(-.5,) * 3, xmax=(.5,) * 3,
+                     bc_inner=(P.REFLECT, P.PERIODIC, P.OUTFLOW), bc_outer=(P.REFLECT, P.PERIODIC, P.OUTFLOW))
+    _check_run(o, g)
+
+
 def test_static_two_level_blast_with_flux_correction(oracle_mod, P):
     kw = dict(mesh_nx=(32, 32, 32), block_nx=(8, 8, 8), xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=1,
               refinement=P.REF_STATIC, regions=[(1, -0.15, 0.15, -0.15, 0.15, -0.15, 0.15)])
