@@ -616,8 +616,10 @@ static ph_status setup_device(ph_mesh* m) {
   if (m->sbuf_n) TRY(dalloc(m, (void**)&m->sbuf, m->sbuf_n * sizeof(double)));
   if (m->rbuf_n) TRY(dalloc(m, (void**)&m->rbuf, m->rbuf_n * sizeof(double)));
   // stage launch geometry
-  m->ntx = (G.n[0] + TX - 1) / TX;
-  m->nty = (G.n[1] + TY - 1) / TY;
+  int tile_x = TX, tile_y = TY;
+  const bool full_tile = stage_tile(G, m->cfg.recon, m->fbuf != nullptr, &tile_x, &tile_y);
+  m->ntx = (G.n[0] + tile_x - 1) / tile_x;
+  m->nty = (G.n[1] + tile_y - 1) / tile_y;
   int64_t base = std::max<int64_t>(nloc, 1) * m->ntx * m->nty;
   int nkc = 1;
   while (base * nkc < 1184 && G.n[2] / (nkc * 2) >= 4) nkc *= 2;
@@ -639,8 +641,7 @@ static ph_status setup_device(ph_mesh* m) {
   // stage-2 base pool: on the uniform full-tile minmod path (the kernels' H template), not under
   // flux correction (it would also have to correct H) nor AMR
   m->Hpool = nullptr;
-  if (!m->ho && !m->multilevel && m->cfg.refinement != PH_REF_ADAPTIVE && m->cfg.recon == PH_RECON_PLM_MINMOD &&
-      G.n[0] % TX == 0 && G.n[1] % TY == 0 && !getenv("PH_NO_HBASE"))
+  if (!m->ho && !m->multilevel && m->cfg.refinement != PH_REF_ADAPTIVE && full_tile && !getenv("PH_NO_HBASE"))
     TRY(dalloc(m, (void**)&m->Hpool, (size_t)std::max<int64_t>(nloc, 1) * G.bstride * sizeof(double)));
   m->partials_n = std::max<int64_t>({(int64_t)m->stage_ctas, nloc * G.n[2], nloc * tag_ctas_per_block(G), 1});
   TRY(dalloc(m, (void**)&m->partials, m->partials_n * 6 * sizeof(double)));

@@ -194,5 +194,7 @@ cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, d
 cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslots, const StageArgs& a, double* W,
                                    double* Fx, double* Fy, double* Fz, const Geom& G, cudaStream_t s);
 size_t stage_smem_bytes(bool use_u0);
+// stage-kernel tile (tx x ty columns) for this block extent; true = full-tile (minmod, uniform) path
+bool stage_tile(const Geom& G, int recon, bool ml, int* tx, int* ty);
 
 }  // namespace ph

@@ -334,20 +334,18 @@ __device__ __forceinline__ double cfl_term_rn(const double* W, const BlockMeta& 
 #endif
 constexpr int TX = TILE_X, TY = TILE_Y, NCELL = TX * TY, NT = PH_STAGE_NT;
 static_assert(NT >= NCELL && NT % 32 == 0, "stage kernel: one thread per tile column at least");
-constexpr int SWX = TX + 4, SWY = TY + 4;
-constexpr int VS = SWY * SWX;           // var stride in a ring slot
 
 // One face: PLM states from the 4 stencil points p0..p3 (cells c-2 .. c+1 along the normal) of
 // the smem primitives, permuted so that w = (rho, u_normal, v_t1, v_t2, p), then HLLE.  F is
 // returned in natural component order.  CN/C1/C2: variable index of normal, t1, t2.
-template <int RECON, int CN, int C1, int C2>
+template <int RECON, int CN, int C1, int C2, int VSv>
 __device__ __forceinline__ void face_flux(const double* p0, const double* p1, const double* p2, const double* p3,
                                           const Geom& G, double* F) {
   constexpr int cv[NVAR] = {0, CN, C1, C2, 4};
   double wl[NVAR], wr[NVAR], Fn[NVAR];
 #pragma unroll
   for (int s = 0; s < NVAR; ++s) {
-    const int o = cv[s] * VS;
+    const int o = cv[s] * VSv;
     plm_face<RECON>(p0[o], p1[o], p2[o], p3[o], wl[s], wr[s]);
   }
   hlle(wl, wr, G, Fn);
@@ -357,17 +355,21 @@ __device__ __forceinline__ void face_flux(const double* p0, const double* p1, co
   F[C2] = Fn[3];
   F[4] = Fn[4];
 }
-constexpr int SLOT = NVAR * VS;         // doubles per ring slot
-constexpr int FXS = TY * (TX + 1);      // var stride of sFx
-constexpr int FYS = (TY + 1) * TX;      // var stride of sFy
-constexpr int FZS = NCELL;              // var stride of sFz
 
-template <int RECON, bool REDUCE, bool USE_U0, bool ML, bool FULL, bool HB>
+// threads of a tile: one per column (the 32x8 tile may add warps via PH_STAGE_NT, an experiment knob)
+template <int TXv, int TYv>
+__host__ __device__ constexpr int tile_threads() { return (TXv == TILE_X && TYv == TILE_Y) ? NT : TXv * TYv; }
+
+template <int RECON, bool REDUCE, bool USE_U0, bool ML, bool FULL, bool HB, int TXv = TILE_X, int TYv = TILE_Y>
 #ifdef PH_STAGE_MAXREG
 __global__ void __maxnreg__(PH_STAGE_MAXREG) stage_kernel(StageArgs A, Geom G) {
 #else
-__global__ void __launch_bounds__(NT, PH_STAGE_MINB) stage_kernel(StageArgs A, Geom G) {
+__global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage_kernel(StageArgs A, Geom G) {
 #endif
+  // tile geometry (the 32x8 default or 16x16 for 16-wide blocks), shadowing the 32x8 constants
+  constexpr int TX = TXv, TY = TYv, NCELL = TX * TY, NT = tile_threads<TXv, TYv>();
+  constexpr int SWX = TX + 4, SWY = TY + 4, VS = SWY * SWX, SLOT = NVAR * VS;
+  constexpr int FXS = TY * (TX + 1), FYS = (TY + 1) * TX, FZS = NCELL;
   extern __shared__ double smem[];
   double* sW = smem;                       // [3][5][SWY][SWX]: planes q-2, q-1, q
   double* sFx = sW + 3 * SLOT;             // [5][TY][TX+1]
@@ -554,7 +556,7 @@ __global__ void __launch_bounds__(NT, PH_STAGE_MINB) stage_kernel(StageArgs A, G
         if (FULL || (j < nyt && fi <= nxt)) {
           const double* p = Wc + (j + 2) * SWX + fi;
           double F[NVAR];
-          face_flux<RECON, 1, 2, 3>(p, p + 1, p + 2, p + 3, G, F);
+          face_flux<RECON, 1, 2, 3, VS>(p, p + 1, p + 2, p + 3, G, F);
           double* d = sFx + j * (TX + 1) + fi;
           d[0] = F[0]; d[FXS] = F[1]; d[2 * FXS] = F[2]; d[3 * FXS] = F[3]; d[4 * FXS] = F[4];
           if (ML) {
@@ -578,7 +580,7 @@ __global__ void __launch_bounds__(NT, PH_STAGE_MINB) stage_kernel(StageArgs A, G
         if (FULL || (jf <= nyt && i < nxt)) {
           const double* p = Wc + jf * SWX + (i + 2);
           double F[NVAR];
-          face_flux<RECON, 2, 3, 1>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
+          face_flux<RECON, 2, 3, 1, VS>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
           double* d = sFy + jf * TX + i;
           d[0] = F[0]; d[FYS] = F[1]; d[2 * FYS] = F[2]; d[3 * FYS] = F[3]; d[4 * FYS] = F[4];
           if (ML) {
@@ -744,9 +746,34 @@ __global__ void __launch_bounds__(NT, PH_STAGE_MINB) stage_kernel(StageArgs A, G
   }
 }
 
-size_t stage_smem_bytes(bool use_u0) {
+template <int TXv, int TYv>
+size_t stage_smem_bytes_t(bool use_u0) {
+  constexpr int TX = TXv, TY = TYv, NCELL = TX * TY, NT = tile_threads<TXv, TYv>();
+  constexpr int SLOT = NVAR * (TX + 4) * (TY + 4), FXS = TY * (TX + 1), FYS = (TY + 1) * TX, FZS = NCELL;
   return sizeof(double) * (3 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS + ((use_u0 && PH_U0_SMEM) ? NVAR * NCELL : 0) +
                            (PH_WARP_RED ? 6 * (NT / 32) : 0));
+}
+size_t stage_smem_bytes(bool use_u0) { return stage_smem_bytes_t<TILE_X, TILE_Y>(use_u0); }
+
+// Tile of the stage kernel for blocks of extent n: the full-tile (no bounds checks) minmod path on
+// uniform levels uses 32x8 when n1 is a multiple of 32, else 16x16 when n1 and n2 are multiples of 16
+// (e.g. 16^3 blocks, which would leave half of a 32-wide tile idle); everything else runs 32x8 tiles
+// with bounds checks.  Returns whether the full-tile path applies.
+bool stage_tile(const Geom& G, int recon, bool ml, int* tx, int* ty) {
+  const bool mm = recon == 0 && !ml;
+  if (mm && G.n[0] % TILE_X == 0 && G.n[1] % TILE_Y == 0) {
+    *tx = TILE_X;
+    *ty = TILE_Y;
+    return true;
+  }
+  if (mm && G.n[0] % 16 == 0 && G.n[1] % 16 == 0) {
+    *tx = 16;
+    *ty = 16;
+    return true;
+  }
+  *tx = TILE_X;
+  *ty = TILE_Y;
+  return false;
 }
 
 // ------------------------------------------------------------------------------ exchange kernel
@@ -1381,7 +1408,6 @@ __global__ void __launch_bounds__(TGT) tag_kernel(const double* U, const BlockMe
   const int slot = b / nty;
   const int x0 = txi * TGX, y0 = tyi * TGY;
   const int nxt = min(TGX, G.n[0] - x0), nyt = min(TGY, G.n[1] - y0);
-  const double* ub = U + (int64_t)slot * G.bstride;
   const BlockMeta& M = meta[slot];
   const int64_t vs = G.vstride;
   const int tid = threadIdx.x, tx = tid % TGX, ty = tid / TGX;
@@ -1397,7 +1423,6 @@ __global__ void __launch_bounds__(TGT) tag_kernel(const double* U, const BlockMe
     else if (q >= G.n[2] && M.nb[5] >= 0) { b = M.nb[5]; q -= G.n[2]; }
     return U + (int64_t)b * G.bstride + ((int64_t)(q + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
   };
-  (void)ub;
   const bool own = tx < nxt && ty < nyt;
   double mx = 0.0;
   // plane loads are prefetched one plane ahead (2 cells per thread of the plus-shaped tile plane)
@@ -1558,39 +1583,44 @@ __global__ void remesh_kernel(const RemeshTask* tasks, const double* Uold, doubl
 // ------------------------------------------------------------------------------ launchers
 #define PH_CHECK_LAUNCH() cudaGetLastError()
 
-template <int R, bool RD, bool U0, bool ML, bool FULL, bool HB = false>
+template <int R, bool RD, bool U0, bool ML, bool FULL, bool HB = false, int TXv = TILE_X, int TYv = TILE_Y>
 static cudaError_t launch_stage_t(int nblk_cta, const StageArgs& a, const Geom& G, cudaStream_t s) {
-  const size_t sm = stage_smem_bytes(U0);
+  const size_t sm = stage_smem_bytes_t<TXv, TYv>(U0);
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB>,
+    cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     if (getenv("PH_DEBUG_ATTR")) {
       cudaFuncAttributes fa;
-      cudaFuncGetAttributes(&fa, stage_kernel<R, RD, U0, ML, FULL, HB>);
+      cudaFuncGetAttributes(&fa, stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv>);
       fprintf(stderr, "stage_kernel<%d,%d,%d,%d,%d>: regs %d maxThreads %d static smem %zu local %zu dyn %zu (max dyn %d) NT %d\n",
               R, (int)RD, (int)U0, (int)ML, (int)FULL, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
               fa.localSizeBytes, sm, fa.maxDynamicSharedSizeBytes, NT);
     }
     // shared-memory carveout hint (percent of the maximum); the rest of the 256 KB is L1
     if (const char* cv = getenv("PH_CARVEOUT")) {
-      e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB>, cudaFuncAttributePreferredSharedMemoryCarveout,
+      e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                atoi(cv));
       if (e != cudaSuccess) return e;
     }
     attr = true;
   }
-  stage_kernel<R, RD, U0, ML, FULL, HB><<<nblk_cta, NT, sm, s>>>(a, G);
+  stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv><<<nblk_cta, tile_threads<TXv, TYv>(), sm, s>>>(a, G);
   return cudaGetLastError();
 }
 
 template <int R, bool RD, bool U0>
 static cudaError_t launch_stage_ml(bool ml, int n, const StageArgs& a, const Geom& G, cudaStream_t s) {
   // full-tile fast path (block extents multiples of the tile): minmod, uniform-level meshes
-  const bool full = (R == 0) && !ml && (G.n[0] % TX == 0) && (G.n[1] % TY == 0);
+  int tx, ty;
+  const bool full = stage_tile(G, R, ml, &tx, &ty);
+  if (a.H && !full) return cudaErrorInvalidValue;  // the host enables H only where the full-tile path runs
+  if (full && tx == 16) {
+    if (a.H) return launch_stage_t<0, RD, U0, false, true, true, 16, 16>(n, a, G, s);
+    return launch_stage_t<0, RD, U0, false, true, false, 16, 16>(n, a, G, s);
+  }
   if (full && a.H) return launch_stage_t<0, RD, U0, false, true, true>(n, a, G, s);
-  if (a.H) return cudaErrorInvalidValue;  // the host enables H only where the full-tile path runs
   if (full) return launch_stage_t<0, RD, U0, false, true>(n, a, G, s);
   return ml ? launch_stage_t<R, RD, U0, true, false>(n, a, G, s) : launch_stage_t<R, RD, U0, false, false>(n, a, G, s);
 }
