@@ -41,6 +41,12 @@ __device__ __forceinline__ double minmod_i(double a, double b) {
 #ifndef PH_WARP_RED
 #define PH_WARP_RED 0
 #endif
+// full-tile path: the tile-boundary faces (x face 0 of every row, y face row 0) of plane c+1 are
+// computed during plane c's 4th face round by warps that would otherwise wait at the barrier, into a
+// small side buffer; plane c+1 then needs 3 rounds.  Planes alternate 4 / 3 rounds instead of 4 / 4.
+#ifndef PH_EXTRA_PRE
+#define PH_EXTRA_PRE 1
+#endif
 // timing-only decomposition knobs (wrong results; never set in a product build)
 #ifndef PH_TIMING_NO_REDUCE
 #define PH_TIMING_NO_REDUCE 0
@@ -377,9 +383,13 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
   double* sFz = sFy + NVAR * FYS;          // [2][5][TY][TX]
   double* sU0 = sFz + 2 * NVAR * FZS;      // [5][TY][TX]: U^n of the cells being finished (stage 2)
   double* sRed = sU0 + ((USE_U0 && PH_U0_SMEM) ? NVAR * NCELL : 0);  // [NT/32][6] warp accumulators
+  double* exFx = sRed + (PH_WARP_RED ? 6 * (NT / 32) : 0);  // [5][TY]: next plane's x faces fi = 0
+  double* exFy = exFx + NVAR * TY;                          // [5][TX]: next plane's y faces jf = 0
+  constexpr bool PRE = PH_EXTRA_PRE && FULL && !ML;
 
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
+  const int warp_id = tid >> 5, lane = tid & 31;
   int bid = blockIdx.x;
   const int kc = bid % A.nkc;
   bid /= A.nkc;
@@ -549,7 +559,51 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
       if (USE_U0 && PH_U0_SMEM) asm volatile("cp.async.commit_group;" ::: "memory");
     }
     // x faces of plane c: 33 per row, item t -> (row t/33, face t%33); rounds 0,1 (warp 0 only)
-    if (xy) {
+    const bool reduced = PRE && ((c - k0) & 1);  // boundary faces of plane c precomputed last iteration
+    if (xy && reduced) {
+      // interior faces only: x faces 1..TX of every row, y face rows 1..TY, one round each
+#pragma unroll 1
+      for (int t = tid; t < TX * TY; t += NT) {
+        const int j = t / TX, fi = t - j * TX + 1;
+        const double* p = Wc + (j + 2) * SWX + fi;
+        double F[NVAR];
+        face_flux<RECON, 1, 2, 3, VS>(p, p + 1, p + 2, p + 3, G, F);
+        double* d = sFx + j * (TX + 1) + fi;
+        d[0] = F[0]; d[FXS] = F[1]; d[2 * FXS] = F[2]; d[3 * FXS] = F[3]; d[4 * FXS] = F[4];
+      }
+#pragma unroll 1
+      for (int t = tid; t < TX * TY; t += NT) {
+        const int jf = t / TX + 1, i = t - (jf - 1) * TX;
+        const double* p = Wc + jf * SWX + (i + 2);
+        double F[NVAR];
+        face_flux<RECON, 2, 3, 1, VS>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
+        double* d = sFy + jf * TX + i;
+        d[0] = F[0]; d[FYS] = F[1]; d[2 * FYS] = F[2]; d[3 * FYS] = F[3]; d[4 * FYS] = F[4];
+      }
+      for (int t = tid; t < NVAR * (TX + TY); t += NT) {  // the precomputed boundary faces
+        const int v = t / (TX + TY), e = t - v * (TX + TY);
+        if (e < TY) sFx[v * FXS + e * (TX + 1)] = exFx[v * TY + e];
+        else sFy[v * FYS + (e - TY)] = exFy[v * TX + (e - TY)];
+      }
+    } else if (xy) {
+      if (PRE && c + 1 < k1) {
+        // boundary faces of plane c+1 (its primitives are in the ring already) on warps 1 and 2,
+        // which otherwise idle through this plane's 4th round
+        const double* Wn = sW + ((c + 4) % 3) * SLOT;
+        if (warp_id == 1 && lane < TY) {
+          const double* p = Wn + (lane + 2) * SWX;
+          double F[NVAR];
+          face_flux<RECON, 1, 2, 3, VS>(p, p + 1, p + 2, p + 3, G, F);
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) exFx[v * TY + lane] = F[v];
+        } else if (warp_id == 2 && lane < TX) {
+          const double* p = Wn + (lane + 2);
+          double F[NVAR];
+          face_flux<RECON, 2, 3, 1, VS>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) exFy[v * TX + lane] = F[v];
+        }
+      }
 #pragma unroll 1
       for (int t = tid; t < (TX + 1) * TY; t += NT) {
         const int j = t / (TX + 1), fi = t - j * (TX + 1);
@@ -751,7 +805,7 @@ size_t stage_smem_bytes_t(bool use_u0) {
   constexpr int TX = TXv, TY = TYv, NCELL = TX * TY, NT = tile_threads<TXv, TYv>();
   constexpr int SLOT = NVAR * (TX + 4) * (TY + 4), FXS = TY * (TX + 1), FYS = (TY + 1) * TX, FZS = NCELL;
   return sizeof(double) * (3 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS + ((use_u0 && PH_U0_SMEM) ? NVAR * NCELL : 0) +
-                           (PH_WARP_RED ? 6 * (NT / 32) : 0));
+                           (PH_WARP_RED ? 6 * (NT / 32) : 0) + NVAR * (TX + TY));
 }
 size_t stage_smem_bytes(bool use_u0) { return stage_smem_bytes_t<TILE_X, TILE_Y>(use_u0); }
 
