@@ -47,6 +47,10 @@ __device__ __forceinline__ double minmod_i(double a, double b) {
 #ifndef PH_EXTRA_PRE
 #define PH_EXTRA_PRE 1
 #endif
+// how many following planes' boundary faces a full plane precomputes (1: planes 4/3 rounds, 2: 4/3/3)
+#ifndef PH_EXTRA_AHEAD
+#define PH_EXTRA_AHEAD 2
+#endif
 // timing-only decomposition knobs (wrong results; never set in a product build)
 #ifndef PH_TIMING_NO_REDUCE
 #define PH_TIMING_NO_REDUCE 0
@@ -383,8 +387,9 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
   double* sFz = sFy + NVAR * FYS;          // [2][5][TY][TX]
   double* sU0 = sFz + 2 * NVAR * FZS;      // [5][TY][TX]: U^n of the cells being finished (stage 2)
   double* sRed = sU0 + ((USE_U0 && PH_U0_SMEM) ? NVAR * NCELL : 0);  // [NT/32][6] warp accumulators
-  double* exFx = sRed + (PH_WARP_RED ? 6 * (NT / 32) : 0);  // [5][TY]: next plane's x faces fi = 0
-  double* exFy = exFx + NVAR * TY;                          // [5][TX]: next plane's y faces jf = 0
+  // [PH_EXTRA_AHEAD][5][TY + TX]: following planes' x faces fi = 0 (first TY) and y faces jf = 0
+  double* exF = sRed + (PH_WARP_RED ? 6 * (NT / 32) : 0);
+  constexpr int EXS = NVAR * (TX + TY);
   constexpr bool PRE = PH_EXTRA_PRE && FULL && !ML;
 
   const int tid = threadIdx.x;
@@ -559,7 +564,8 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
       if (USE_U0 && PH_U0_SMEM) asm volatile("cp.async.commit_group;" ::: "memory");
     }
     // x faces of plane c: 33 per row, item t -> (row t/33, face t%33); rounds 0,1 (warp 0 only)
-    const bool reduced = PRE && ((c - k0) & 1);  // boundary faces of plane c precomputed last iteration
+    const int phase = (c - k0) % (PH_EXTRA_AHEAD + 1);  // 0: full plane; else boundary faces precomputed
+    const bool reduced = PRE && phase != 0;
     if (xy && reduced) {
       // interior faces only: x faces 1..TX of every row, y face rows 1..TY, one round each
 #pragma unroll 1
@@ -580,28 +586,33 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
         double* d = sFy + jf * TX + i;
         d[0] = F[0]; d[FYS] = F[1]; d[2 * FYS] = F[2]; d[3 * FYS] = F[3]; d[4 * FYS] = F[4];
       }
+      const double* ex = exF + (phase - 1) * EXS;
       for (int t = tid; t < NVAR * (TX + TY); t += NT) {  // the precomputed boundary faces
         const int v = t / (TX + TY), e = t - v * (TX + TY);
-        if (e < TY) sFx[v * FXS + e * (TX + 1)] = exFx[v * TY + e];
-        else sFy[v * FYS + (e - TY)] = exFy[v * TX + (e - TY)];
+        if (e < TY) sFx[v * FXS + e * (TX + 1)] = ex[t];
+        else sFy[v * FYS + (e - TY)] = ex[t];
       }
     } else if (xy) {
-      if (PRE && c + 1 < k1) {
-        // boundary faces of plane c+1 (its primitives are in the ring already) on warps 1 and 2,
-        // which otherwise idle through this plane's 4th round
-        const double* Wn = sW + ((c + 4) % 3) * SLOT;
-        if (warp_id == 1 && lane < TY) {
-          const double* p = Wn + (lane + 2) * SWX;
-          double F[NVAR];
-          face_flux<RECON, 1, 2, 3, VS>(p, p + 1, p + 2, p + 3, G, F);
+      if (PRE) {
+        // boundary faces of planes c+1 .. c+AHEAD (their primitives are in the ring already) on
+        // warps 1-2 and 3,5, which otherwise idle through this plane's 4th round
+        const int a = (warp_id == 1 || warp_id == 2) ? 1 : ((warp_id == 3 || warp_id == 5) ? 2 : 0);
+        if (a != 0 && a <= PH_EXTRA_AHEAD && c + a < k1) {
+          const double* Wn = sW + ((c + a + 3) % 3) * SLOT;
+          double* ex = exF + (a - 1) * EXS;
+          if ((warp_id == 1 || warp_id == 3) && lane < TY) {
+            const double* p = Wn + (lane + 2) * SWX;
+            double F[NVAR];
+            face_flux<RECON, 1, 2, 3, VS>(p, p + 1, p + 2, p + 3, G, F);
 #pragma unroll
-          for (int v = 0; v < NVAR; ++v) exFx[v * TY + lane] = F[v];
-        } else if (warp_id == 2 && lane < TX) {
-          const double* p = Wn + (lane + 2);
-          double F[NVAR];
-          face_flux<RECON, 2, 3, 1, VS>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
+            for (int v = 0; v < NVAR; ++v) ex[v * (TX + TY) + lane] = F[v];
+          } else if ((warp_id == 2 || warp_id == 5) && lane < TX) {
+            const double* p = Wn + (lane + 2);
+            double F[NVAR];
+            face_flux<RECON, 2, 3, 1, VS>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
 #pragma unroll
-          for (int v = 0; v < NVAR; ++v) exFy[v * TX + lane] = F[v];
+            for (int v = 0; v < NVAR; ++v) ex[v * (TX + TY) + TY + lane] = F[v];
+          }
         }
       }
 #pragma unroll 1
@@ -805,7 +816,7 @@ size_t stage_smem_bytes_t(bool use_u0) {
   constexpr int TX = TXv, TY = TYv, NCELL = TX * TY, NT = tile_threads<TXv, TYv>();
   constexpr int SLOT = NVAR * (TX + 4) * (TY + 4), FXS = TY * (TX + 1), FYS = (TY + 1) * TX, FZS = NCELL;
   return sizeof(double) * (3 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS + ((use_u0 && PH_U0_SMEM) ? NVAR * NCELL : 0) +
-                           (PH_WARP_RED ? 6 * (NT / 32) : 0) + NVAR * (TX + TY));
+                           (PH_WARP_RED ? 6 * (NT / 32) : 0) + PH_EXTRA_AHEAD * NVAR * (TX + TY));
 }
 size_t stage_smem_bytes(bool use_u0) { return stage_smem_bytes_t<TILE_X, TILE_Y>(use_u0); }
 
