@@ -621,8 +621,10 @@ static ph_status setup_device(ph_mesh* m) {
   m->ntx = (G.n[0] + tile_x - 1) / tile_x;
   m->nty = (G.n[1] + tile_y - 1) / tile_y;
   int64_t base = std::max<int64_t>(nloc, 1) * m->ntx * m->nty;
+  // split the k-march of small meshes until ~8 CTAs per SM exist, down to min_kc planes per CTA
+  const int min_kc = getenv("PH_MIN_KC") ? std::max(1, atoi(getenv("PH_MIN_KC"))) : 1;
   int nkc = 1;
-  while (base * nkc < 1184 && G.n[2] / (nkc * 2) >= 4) nkc *= 2;
+  while (base * nkc < 1184 && G.n[2] / (nkc * 2) >= min_kc) nkc *= 2;
   m->KC = (G.n[2] + nkc - 1) / nkc;
   m->nkc = (G.n[2] + m->KC - 1) / m->KC;
   m->pack_size = (m->cfg.pack_size > 0) ? (int)std::min<int64_t>(m->cfg.pack_size, nloc) : (int)nloc;
