@@ -28,7 +28,7 @@ def _port():
 
 CASES = [(c, "auto") for c in ("smr2", "smr3_walls", "amr2", "wenoz")]
 # uniform meshes: both halo transports (NCCL pack/send/unpack, and peer memory read in place)
-CASES += [(c, h) for c in ("blast", "sod_walls", "wave64") for h in ("nccl", "peer")]
+CASES += [(c, h) for c in ("blast", "sod_walls", "wave64", "tiny") for h in ("nccl", "peer")]
 
 
 @pytest.mark.parametrize("case,halo", CASES)

@@ -31,6 +31,9 @@ CASES = {
     # NEXT 3: WENO-Z with nghost 3 (generic high-order path) across GPUs
     "wenoz": dict(kw=dict(mesh_nx=(64, 32, 32), block_nx=(16, 16, 16), xmin=(-.5,) * 3, xmax=(.5,) * 3, recon=4,
                           nghost=3), problem=2, params=[10.0, 0.1, 0.15], cycles=8),
+    # fewer blocks than ranks: some ranks own no block at all (empty partitions, A19/O2)
+    "tiny": dict(kw=dict(mesh_nx=(64, 32, 32), block_nx=(32, 32, 32), xmin=(-.5,) * 3, xmax=(.5,) * 3),
+                 problem=2, params=[10.0, 0.1, 0.2], cycles=6),
     # AMR: tagging gathered across ranks, remesh with block migration between GPUs
     "amr2": dict(kw=dict(mesh_nx=(32, 32, 32), block_nx=(8, 8, 8), xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=2,
                          refinement=2, refine_tol=0.1, derefine_tol=0.025, derefine_interval=2),
