@@ -30,12 +30,12 @@ PER_GPU_ROOT = {"2b": (8, 8, 8), "4": (4, 4, 4)}
 SCALE_AXES = [(1, 1, 1), (2, 1, 1), (2, 2, 1), (2, 2, 2), (4, 2, 2), (4, 4, 2), (4, 4, 4), (8, 4, 4)]
 
 
-def workload(cfg, ngpu, n=64):
+def workload(cfg, ngpu, n=64, strong=False):
     root = PER_GPU_ROOT[cfg]
     k = {1: 0, 2: 1, 4: 2, 8: 3}.get(ngpu)
     if k is None:
         raise SystemExit(f"--gpus {ngpu}: use 1, 2, 4 or 8")
-    ax = SCALE_AXES[k]
+    ax = SCALE_AXES[0 if strong else k]  # strong scaling: the 1-GPU mesh on every N
     groot = tuple(root[d] * ax[d] for d in range(3))
     mesh = tuple(n * r for r in groot)
     # unit cell width in every direction: domain extents proportional to the mesh
@@ -169,7 +169,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
-    W = workload(args.config, world)
+    W = workload(args.config, world, strong=args.scaling == "strong")
     transport = {"auto": P.HALO_AUTO, "nccl": P.HALO_NCCL, "peer": P.HALO_PEER}[args.halo]
     mesh = P.Mesh(device=local, rank=rank, nranks=world, stream=stream, halo_transport=transport, **W)
     halo = "local direct halo" if world == 1 else (
@@ -266,6 +266,14 @@ def run_ours(args):
         except Exception:
             traffic = None
     b_ghost = (6 * r - 1) * 40.0
+    size = "512^3" if args.config == "2b" else "256^3"
+    base = (f"(BASELINE configs[{1 if args.config == '2b' else 3}]"
+            f"{', reading 2b' if args.config == '2b' else ''}), global mesh {W['mesh_nx']}, "
+            f"{nglob} blocks, all local blocks per launch, PLM-minmod + HLLE + RK2, CFL 0.3")
+    if args.scaling == "strong":
+        workload_desc = f"blast 3D, fixed {size} global mesh in 64^3 blocks split over {world} GPU(s), strong scaling " + base
+    else:
+        workload_desc = f"blast 3D, {size} cells per GPU in 64^3 blocks " + base
     # co-limiter (SURVEY §8(d) "report both"): the fp64 pipe.  Instructions per cell-stage from the
     # committed ncu capture of this kernel; peak = 148 SMs x 64 fp64 lanes/clk x 1965 MHz (B200 unit
     # counts and max clock).
@@ -284,12 +292,9 @@ def run_ours(args):
     line = {
         "metric": "zone-cycles/s", "value": value, "unit": "zone-cycles/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"blast 3D, {'512^3' if args.config == '2b' else '256^3'} cells per GPU in 64^3 blocks "
-                               f"(BASELINE configs[{1 if args.config == '2b' else 3}]"
-                               f"{', reading 2b' if args.config == '2b' else ''}), global mesh {W['mesh_nx']}, "
-                               f"{nglob} blocks, all local blocks per launch, PLM-minmod + HLLE + RK2, CFL 0.3",
+        "config": {"workload": workload_desc,
                    "global_blocks": nglob, "block": n, "nghost": 2,
                    "l2": "inputs larger than L2 (state %.1f GB per GPU vs 126 MB L2)" % (2 * nloc * 5 * (n + 4) ** 3 * 8 / 1e9),
                    "parallelism": f"morton-partition dp{world}", "halo": halo},
@@ -329,6 +334,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="2b", choices=["2b", "4"])
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: fixed work per GPU (default); strong: the 1-GPU mesh split over N GPUs")
     ap.add_argument("--halo", default="auto", choices=["auto", "nccl", "peer"],
                     help="multi-GPU halo transport (auto: peer memory when every rank can map its peers)")
     ap.add_argument("--no-cpu", action="store_true")
