@@ -105,10 +105,7 @@ struct CycleState {
   long long hist_count;
 };
 
-#ifndef PH_TILE_Y
-#define PH_TILE_Y 8
-#endif
-constexpr int TILE_X = 32, TILE_Y = PH_TILE_Y;  // stage-kernel tile (i, j)
+constexpr int TILE_X = 32, TILE_Y = 8;  // default stage-kernel tile (i, j); 16x16 for 16-wide blocks
 
 struct StageArgs {
   const double* Uin;   // pool with valid ghosts (stage input)
@@ -193,7 +190,7 @@ cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, d
                           double* sbuf, const Geom& G, cudaStream_t s);
 cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslots, const StageArgs& a, double* W,
                                    double* Fx, double* Fy, double* Fz, const Geom& G, cudaStream_t s);
-size_t stage_smem_bytes(bool use_u0);
+size_t stage_smem_bytes();
 // stage-kernel tile (tx x ty columns) for this block extent; true = full-tile (minmod, uniform) path
 bool stage_tile(const Geom& G, int recon, bool ml, int* tx, int* ty);
 

@@ -23,55 +23,12 @@ __device__ __forceinline__ double minmod_i(double a, double b) {
   return ((ha ^ hb) >= 0) ? m : 0.0;
 }
 
-#ifndef PH_PREFETCH_UIN
-#define PH_PREFETCH_UIN 1
-#endif
-#ifndef PH_PREFETCH_U0
-#define PH_PREFETCH_U0 1
-#endif
-#ifndef PH_MINMOD_HALF
-#define PH_MINMOD_HALF 1
-#endif
-// stage 2: stage the finish operand U^n in shared memory with cp.async instead of holding it in
-// registers across the face phase.  Off: removes the 32 B spill but the extra 10 KB of smem per CTA
-// costs L1 and is 2.4 % slower on 2b (profiles/r01_ab_finish_prefetch.md)
-// stage 2: reduce the CFL max and the 5 totals per plane with warp shuffles into per-warp smem
-// accumulators (fixed order: plane, then warp) instead of 6 per-thread accumulators live for the
-// whole k-march -- frees 12 registers in the reducing kernel
-#ifndef PH_WARP_RED
-#define PH_WARP_RED 0
-#endif
-// full-tile path: the tile-boundary faces (x face 0 of every row, y face row 0) of plane c+1 are
-// computed during plane c's 4th face round by warps that would otherwise wait at the barrier, into a
-// small side buffer; plane c+1 then needs 3 rounds.  Planes alternate 4 / 3 rounds instead of 4 / 4.
-#ifndef PH_EXTRA_PRE
-#define PH_EXTRA_PRE 1
-#endif
-// how many following planes' boundary faces a full plane precomputes (1: planes 4/3 rounds, 2: 4/3/3)
-#ifndef PH_EXTRA_AHEAD
-#define PH_EXTRA_AHEAD 2
-#endif
-// timing-only decomposition knobs (wrong results; never set in a product build)
-#ifndef PH_TIMING_NO_REDUCE
-#define PH_TIMING_NO_REDUCE 0
-#endif
-#ifndef PH_TIMING_NO_U0
-#define PH_TIMING_NO_U0 0
-#endif
-// plane loads through L1 (ld.global.nc) or L2 only (ld.global.cg): no reuse in L1, .cg is 0.6 % faster
-#ifndef PH_LDCG
-#define PH_LDCG 1
-#endif
-__device__ __forceinline__ double ld_plane(const double* p) {
-#if PH_LDCG
-  return __ldcg(p);
-#else
-  return __ldg(p);
-#endif
-}
-#ifndef PH_U0_SMEM
-#define PH_U0_SMEM 0
-#endif
+// full-tile path: the tile-boundary faces (x face 0 of every row, y face row 0) of planes c+1 and
+// c+2 are computed during plane c's 4th face round by warps that would otherwise wait at the
+// barrier, into a small side buffer; those planes then need 3 face rounds (4/3/3 instead of 4/4/4).
+constexpr int EXTRA_AHEAD = 2;
+// plane loads bypass L1 (ld.global.cg): there is no reuse in L1 (+0.6 % over ld.global.nc)
+__device__ __forceinline__ double ld_plane(const double* p) { return __ldcg(p); }
 __device__ __forceinline__ double minmod_pick(double a, double b) { return (fabs(a) < fabs(b)) ? a : b; }
 __device__ __forceinline__ double minmod_half(double a, double b) {
   return ((__double2hiint(a) ^ __double2hiint(b)) >= 0) ? 0.5 : 0.0;
@@ -92,7 +49,6 @@ __device__ __forceinline__ double slope(double dl, double dr) {
 template <int RECON>
 __device__ __forceinline__ void plm_face(double q0, double q1, double q2, double q3, double& wl, double& wr) {
   double d0 = q1 - q0, d1 = q2 - q1, d2 = q3 - q2;
-#if PH_MINMOD_HALF
   if (RECON == 0) {
     // minmod with the sign test folded into the coefficient: h = same sign ? 0.5 : 0 (one select
     // on the high word), state = q + h * (smaller-magnitude difference); equals q + 0.5*minmod
@@ -100,7 +56,6 @@ __device__ __forceinline__ void plm_face(double q0, double q1, double q2, double
     wr = fma(-minmod_half(d1, d2), minmod_pick(d1, d2), q2);
     return;
   }
-#endif
   double s1 = slope<RECON>(d0, d1);
   double s2 = slope<RECON>(d1, d2);
   wl = fma(0.5, s1, q1);   // == q1 + 0.5*s1 exactly (0.5*s1 is exact)
@@ -133,25 +88,10 @@ __device__ __forceinline__ double sound_speed(double rho, double p, double gamma
 }
 
 // min / max as plain compare-selects (DSETP + 2 FSEL).  fmin/fmax carry IEEE NaN semantics that
-// cost a SEL, a predicated LOP3 and register moves per call; a NaN state is already flagged by
-// the cons->prim positivity check, so only finite operands matter here.
-#ifndef PH_FAST_MINMAX
-#define PH_FAST_MINMAX 1
-#endif
-__device__ __forceinline__ double dmin(double a, double b) {
-#if PH_FAST_MINMAX
-  return a < b ? a : b;
-#else
-  return fmin(a, b);
-#endif
-}
-__device__ __forceinline__ double dmax(double a, double b) {
-#if PH_FAST_MINMAX
-  return a > b ? a : b;
-#else
-  return fmax(a, b);
-#endif
-}
+// cost a SEL, a predicated LOP3 and register moves per call (+1.3 % on 2b without them); a NaN state
+// is already flagged by the cons->prim positivity check, so only finite operands matter here.
+__device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 
 // HLLE, Davis speeds, clamped branch-free form (a4; A4, A5).  w = (rho, u_n, v_t1, v_t2, p).
 __device__ __forceinline__ void hlle(const double* wl, const double* wr, const Geom& G, double* F) {
@@ -323,27 +263,15 @@ __device__ __forceinline__ double cfl_term_rn(const double* W, const BlockMeta& 
 
 
 // ------------------------------------------------------------------------------ stage kernel
-// One CTA = a TX x TY tile of (i,j) columns of one block, marching up a k-range of KC planes.
-// Plane q is converted to primitives (a2) into slot q%4 of a 4-plane smem ring (plus-shaped
-// x/y halo).  Iteration q then computes, as ONE flat work list balanced over all 256 threads,
-// the x and y faces of plane q-2 and the z faces between planes q-2 and q-1 (a3 PLM + a4 HLLE,
-// one shared code path per face), and finishes the cells of plane q-2: flux divergence and the
-// RK stage combine (a5).  The final stage also reduces the CFL term and the totals (a6, a10).
-#ifndef PH_PREFETCH
-#define PH_PREFETCH 0
-#endif
-#ifndef PH_PREFETCH_L1
-#define PH_PREFETCH_L1 1
-#endif
-// threads per CTA (>= cells per tile; extra warps take x/y face items only) and CTAs per SM
-#ifndef PH_STAGE_NT
-#define PH_STAGE_NT (TILE_X * TILE_Y)
-#endif
-#ifndef PH_STAGE_MINB
-#define PH_STAGE_MINB 2
-#endif
-constexpr int TX = TILE_X, TY = TILE_Y, NCELL = TX * TY, NT = PH_STAGE_NT;
-static_assert(NT >= NCELL && NT % 32 == 0, "stage kernel: one thread per tile column at least");
+// One CTA = a TX x TY tile of (i,j) columns of one block, marching up a k-range of KC planes, one
+// thread per column, 2 CTAs per SM.  Plane q is converted to primitives (a2) into slot q%3 of a
+// 3-plane smem ring (plus-shaped x/y halo, read from the face neighbours directly when they are
+// local and same-level).  Iteration q then computes the x and y faces of plane c = q-2 as flat work
+// lists over all threads and the z face between planes c and c+1 of each column (its z states
+// carried in registers) -- a3 PLM + a4 HLLE, one code path per face -- and finishes the cells of
+// plane c: flux divergence and the RK stage combine (a5).  The final stage also reduces the CFL
+// term and the totals (a6, a10).
+constexpr int TX = TILE_X, TY = TILE_Y, NCELL = TX * TY, NT = NCELL;
 
 // One face: PLM states from the 4 stencil points p0..p3 (cells c-2 .. c+1 along the normal) of
 // the smem primitives, permuted so that w = (rho, u_normal, v_t1, v_t2, p), then HLLE.  F is
@@ -366,18 +294,10 @@ __device__ __forceinline__ void face_flux(const double* p0, const double* p1, co
   F[4] = Fn[4];
 }
 
-// threads of a tile: one per column (the 32x8 tile may add warps via PH_STAGE_NT, an experiment knob)
-template <int TXv, int TYv>
-__host__ __device__ constexpr int tile_threads() { return (TXv == TILE_X && TYv == TILE_Y) ? NT : TXv * TYv; }
-
 template <int RECON, bool REDUCE, bool USE_U0, bool ML, bool FULL, bool HB, int TXv = TILE_X, int TYv = TILE_Y>
-#ifdef PH_STAGE_MAXREG
-__global__ void __maxnreg__(PH_STAGE_MAXREG) stage_kernel(StageArgs A, Geom G) {
-#else
-__global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage_kernel(StageArgs A, Geom G) {
-#endif
-  // tile geometry (the 32x8 default or 16x16 for 16-wide blocks), shadowing the 32x8 constants
-  constexpr int TX = TXv, TY = TYv, NCELL = TX * TY, NT = tile_threads<TXv, TYv>();
+__global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G) {
+  // tile geometry (32x8, or 16x16 for 16-wide blocks), shadowing the 32x8 constants
+  constexpr int TX = TXv, TY = TYv, NCELL = TX * TY, NT = NCELL;
   constexpr int SWX = TX + 4, SWY = TY + 4, VS = SWY * SWX, SLOT = NVAR * VS;
   constexpr int FXS = TY * (TX + 1), FYS = (TY + 1) * TX, FZS = NCELL;
   extern __shared__ double smem[];
@@ -385,12 +305,9 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
   double* sFx = sW + 3 * SLOT;             // [5][TY][TX+1]
   double* sFy = sFx + NVAR * FXS;          // [5][TY+1][TX]
   double* sFz = sFy + NVAR * FYS;          // [2][5][TY][TX]
-  double* sU0 = sFz + 2 * NVAR * FZS;      // [5][TY][TX]: U^n of the cells being finished (stage 2)
-  double* sRed = sU0 + ((USE_U0 && PH_U0_SMEM) ? NVAR * NCELL : 0);  // [NT/32][6] warp accumulators
-  // [PH_EXTRA_AHEAD][5][TY + TX]: following planes' x faces fi = 0 (first TY) and y faces jf = 0
-  double* exF = sRed + (PH_WARP_RED ? 6 * (NT / 32) : 0);
+  double* exF = sFz + 2 * NVAR * FZS;      // [EXTRA_AHEAD][5][TY + TX]: later planes' x faces fi = 0, y faces jf = 0
   constexpr int EXS = NVAR * (TX + TY);
-  constexpr bool PRE = PH_EXTRA_PRE && FULL && !ML;
+  constexpr bool PRE = FULL && !ML;        // boundary-face precompute on the regular full-tile path
 
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
@@ -413,7 +330,7 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
   const double* Ub = A.Uin + (int64_t)slot * G.bstride;
   const double dt = A.st->dt_used;
   const double idx1 = M.idx[0], idx2 = M.idx[1], idx3 = M.idx[2];
-  const bool own = (NT == NCELL || tid < NCELL) && (FULL || ((tx < nxt) && (ty < nyt)));
+  const bool own = FULL || ((tx < nxt) && (ty < nyt));
 
   // ---- load-slot geometry: the plus-shaped halo plane is 2 cells per thread ----
   int sl_i[2], sl_j[2];
@@ -467,24 +384,6 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
     const bool halo = (q < k0) || (q >= k1);
     return halo ? (s == 0 && own) : sl_ok[s];
   };
-  // The next plane is only *prefetched* (no destination register, so no scoreboard is held across
-  // the face phase); the real loads at store time then hit in cache.
-  auto prefetch_plane = [&](int q) {
-#pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      if (slot_ok(q, s)) {
-        const double* p = slot_ptr(q, s);
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) {
-#if PH_PREFETCH_L1
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(p + v * G.vstride));
-#else
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(p + v * G.vstride));
-#endif
-        }
-      }
-    }
-  };
   auto issue_load = [&](int q) {
 #pragma unroll
     for (int s = 0; s < 2; ++s) {
@@ -520,21 +419,12 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
   };
 
   double tmax = 0.0, tsum[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};
-  if (REDUCE && PH_WARP_RED && (tid & 31) == 0)
-    for (int v = 0; v < 6; ++v) sRed[(tid >> 5) * 6 + v] = 0.0;  // first read after >= 1 barrier
   double topz[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};  // z top state of plane q-2 (my column)
   const int qbeg = k0 - 2, qend = k1 + 2;
-#if PH_PREFETCH
-  for (int q = qbeg; q < qend; ++q) {
-    issue_load(q);
-    store_prims(q);
-    if (q + 1 < qend) prefetch_plane(q + 1);
-#else
   issue_load(qbeg);
   for (int q = qbeg; q < qend; ++q) {
     store_prims(q);
-    if (q + 1 < qend) issue_load(q + 1);
-#endif
+    if (q + 1 < qend) issue_load(q + 1);  // the next plane's loads fly during this plane's faces
     __syncthreads();
     const int c = q - 2;                 // plane whose x/y faces and cells are done now
     const int fz = q - 1;                // z face between planes q-2 and q-1
@@ -542,29 +432,23 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
     const bool zf = (fz >= k0) && (fz <= k1);
     const double* Wc = sW + ((c + 3) % 3) * SLOT;
     // prefetch the finish-phase operands of my cell so their latency hides behind the faces
+    // (without it the kernel is 7 % slower): U_in and U^n, or on the H path only H
     double uin[NVAR], u0v[NVAR];
     const int64_t cell = (int64_t)slot * G.bstride + (int64_t)(c + g) * plane +
                          (int64_t)(y0 + ty + g) * G.N[0] + (x0 + tx + g);
     if (xy && own) {
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
-        if (HB && USE_U0) {  // stage 2 of the H path: the base H is the only cell operand
+        if (HB && USE_U0) {
           uin[v] = ld_plane(A.H + cell + v * G.vstride);
-          continue;
-        }
-        if (PH_PREFETCH_UIN) uin[v] = ld_plane(A.Uin + cell + v * G.vstride);
-        if (USE_U0 && PH_TIMING_NO_U0) {
-        } else if (USE_U0 && PH_U0_SMEM) {
-          const unsigned sa = (unsigned)__cvta_generic_to_shared(sU0 + v * NCELL + tid);
-          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(A.U0 + cell + v * G.vstride) : "memory");
-        } else if (USE_U0 && PH_PREFETCH_U0) {
-          u0v[v] = A.U0[cell + v * G.vstride];
+        } else {
+          uin[v] = ld_plane(A.Uin + cell + v * G.vstride);
+          if (USE_U0) u0v[v] = A.U0[cell + v * G.vstride];
         }
       }
-      if (USE_U0 && PH_U0_SMEM) asm volatile("cp.async.commit_group;" ::: "memory");
     }
     // x faces of plane c: 33 per row, item t -> (row t/33, face t%33); rounds 0,1 (warp 0 only)
-    const int phase = (c - k0) % (PH_EXTRA_AHEAD + 1);  // 0: full plane; else boundary faces precomputed
+    const int phase = (c - k0) % (EXTRA_AHEAD + 1);  // 0: full plane; else boundary faces precomputed
     const bool reduced = PRE && phase != 0;
     if (xy && reduced) {
       // interior faces only: x faces 1..TX of every row, y face rows 1..TY, one round each
@@ -597,7 +481,7 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
         // boundary faces of planes c+1 .. c+AHEAD (their primitives are in the ring already) on
         // warps 1-2 and 3,5, which otherwise idle through this plane's 4th round
         const int a = (warp_id == 1 || warp_id == 2) ? 1 : ((warp_id == 3 || warp_id == 5) ? 2 : 0);
-        if (a != 0 && a <= PH_EXTRA_AHEAD && c + a < k1) {
+        if (a != 0 && a <= EXTRA_AHEAD && c + a < k1) {
           const double* Wn = sW + ((c + a + 3) % 3) * SLOT;
           double* ex = exF + (a - 1) * EXS;
           if ((warp_id == 1 || warp_id == 3) && lane < TY) {
@@ -672,7 +556,6 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
         const double a = p0[v * VS];
-#if PH_MINMOD_HALF
         if (RECON == 0) {
           const double dl = a - pm[v * VS], dr = pp[v * VS] - a;
           const double h = minmod_half(dl, dr), mp = minmod_pick(dl, dr);
@@ -680,7 +563,6 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
           top[v] = fma(h, mp, a);
           continue;
         }
-#endif
         const double s = slope<RECON>(a - pm[v * VS], pp[v * VS] - a);
         bot[v] = fma(-0.5, s, a);
         top[v] = fma(0.5, s, a);
@@ -712,7 +594,6 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
       const double* fzl = sFz + (c & 1) * NVAR * FZS + tid;        // face c   (lower)
       const double* fzu = sFz + ((c + 1) & 1) * NVAR * FZS + tid;  // face c+1 (upper)
       double un[NVAR];
-      if (USE_U0 && PH_U0_SMEM) asm volatile("cp.async.wait_all;" ::: "memory");  // my own copies only
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
         double d1 = (sFx[v * FXS + ty * (TX + 1) + tx + 1] - sFx[v * FXS + ty * (TX + 1) + tx]) * idx1;
@@ -723,66 +604,27 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
         if (HB && USE_U0) {
           out = fma(A.cdt * dt, L, uin[v]);  // H + cdt dt L
         } else {
-          const double ui = PH_PREFETCH_UIN ? uin[v] : __ldg(A.Uin + cell + v * G.vstride);
-          out = fma(A.b1, ui, (A.cdt * dt) * L);
-          if (USE_U0 && !PH_TIMING_NO_U0)
-            out = fma(A.a0, PH_U0_SMEM ? sU0[v * NCELL + tid] : (PH_PREFETCH_U0 ? u0v[v] : A.U0[cell + v * G.vstride]), out);
-          if (HB && !USE_U0) A.H[cell + v * G.vstride] = fma(A.hb1, out, A.ha0 * ui);  // stage 1: write H
+          out = fma(A.b1, uin[v], (A.cdt * dt) * L);
+          if (USE_U0) out = fma(A.a0, u0v[v], out);
+          if (HB && !USE_U0) A.H[cell + v * G.vstride] = fma(A.hb1, out, A.ha0 * uin[v]);  // stage 1: write H
         }
         un[v] = out;
         A.Uout[cell + v * G.vstride] = out;
       }
-      if (REDUCE && !PH_TIMING_NO_REDUCE) {
+      if (REDUCE) {
         double ir = rcp_nr(un[0]);
         double v1 = un[1] * ir, v2 = un[2] * ir, v3 = un[3] * ir;
         double ke = 0.5 * ((un[1] * v1 + un[2] * v2) + un[3] * v3);
         double p = G.gm1 * (un[4] - ke);
         double cs = sound_speed(un[0], p, G.gamma);
         double s1 = (fabs(v1) + cs) * idx1, s2 = (fabs(v2) + cs) * idx2, s3 = (fabs(v3) + cs) * idx3;
-        if (PH_WARP_RED) {
-          tmax = dmax(s1, dmax(s2, s3));  // this cell only; reduced over the warp below
+        tmax = dmax(tmax, dmax(s1, dmax(s2, s3)));
 #pragma unroll
-          for (int v = 0; v < NVAR; ++v) tsum[v] = un[v];
-        } else {
-          tmax = dmax(tmax, dmax(s1, dmax(s2, s3)));
-#pragma unroll
-          for (int v = 0; v < NVAR; ++v) tsum[v] += un[v];
-        }
+        for (int v = 0; v < NVAR; ++v) tsum[v] += un[v];
       }
-    }
-    if (REDUCE && PH_WARP_RED && xy) {
-      // plane c of this warp: shuffle tree, then lane 0 adds to the warp's accumulators
-#pragma unroll
-      for (int off = 16; off > 0; off >>= 1) {
-        tmax = dmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) tsum[v] += __shfl_xor_sync(0xffffffffu, tsum[v], off);
-      }
-      if ((tid & 31) == 0) {
-        double* r = sRed + (tid >> 5) * 6;
-        r[0] = dmax(r[0], tmax);
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) r[1 + v] += tsum[v];
-      }
-      tmax = 0.0;
-#pragma unroll
-      for (int v = 0; v < NVAR; ++v) tsum[v] = 0.0;
     }
   }
-  if (REDUCE && PH_WARP_RED) {
-    __syncthreads();
-    if (tid == 0) {
-      double m = PH_TIMING_NO_REDUCE ? 1e5 : 0.0, s[NVAR] = {0, 0, 0, 0, 0};
-      for (int w = 0; w < NT / 32; ++w) {
-        m = fmax(m, sRed[w * 6]);
-        for (int v = 0; v < NVAR; ++v) s[v] += sRed[w * 6 + 1 + v];
-      }
-      double* o = A.partials + (int64_t)(A.cta_base + blockIdx.x) * 6;
-      o[0] = m;
-      for (int v = 0; v < NVAR; ++v) o[1 + v] = s[v] * M.dV;
-    }
-  } else if (REDUCE) {
-    if (PH_TIMING_NO_REDUCE) tmax = 1e5;  // timing-only: keep dt finite and small
+  if (REDUCE) {
     // deterministic CTA reduction: warp shuffles then thread 0 in fixed warp order
     __syncthreads();
     double* red = smem;
@@ -812,13 +654,12 @@ __global__ void __launch_bounds__(tile_threads<TXv, TYv>(), PH_STAGE_MINB) stage
 }
 
 template <int TXv, int TYv>
-size_t stage_smem_bytes_t(bool use_u0) {
-  constexpr int TX = TXv, TY = TYv, NCELL = TX * TY, NT = tile_threads<TXv, TYv>();
+size_t stage_smem_bytes_t() {
+  constexpr int TX = TXv, TY = TYv, NCELL = TX * TY;
   constexpr int SLOT = NVAR * (TX + 4) * (TY + 4), FXS = TY * (TX + 1), FYS = (TY + 1) * TX, FZS = NCELL;
-  return sizeof(double) * (3 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS + ((use_u0 && PH_U0_SMEM) ? NVAR * NCELL : 0) +
-                           (PH_WARP_RED ? 6 * (NT / 32) : 0) + PH_EXTRA_AHEAD * NVAR * (TX + TY));
+  return sizeof(double) * (3 * SLOT + NVAR * FXS + NVAR * FYS + 2 * NVAR * FZS + EXTRA_AHEAD * NVAR * (TX + TY));
 }
-size_t stage_smem_bytes(bool use_u0) { return stage_smem_bytes_t<TILE_X, TILE_Y>(use_u0); }
+size_t stage_smem_bytes() { return stage_smem_bytes_t<TILE_X, TILE_Y>(); }
 
 // Tile of the stage kernel for blocks of extent n: the full-tile (no bounds checks) minmod path on
 // uniform levels uses 32x8 when n1 is a multiple of 32, else 16x16 when n1 and n2 are multiples of 16
@@ -1650,7 +1491,7 @@ __global__ void remesh_kernel(const RemeshTask* tasks, const double* Uold, doubl
 
 template <int R, bool RD, bool U0, bool ML, bool FULL, bool HB = false, int TXv = TILE_X, int TYv = TILE_Y>
 static cudaError_t launch_stage_t(int nblk_cta, const StageArgs& a, const Geom& G, cudaStream_t s) {
-  const size_t sm = stage_smem_bytes_t<TXv, TYv>(U0);
+  const size_t sm = stage_smem_bytes_t<TXv, TYv>();
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv>,
@@ -1671,7 +1512,7 @@ static cudaError_t launch_stage_t(int nblk_cta, const StageArgs& a, const Geom& 
     }
     attr = true;
   }
-  stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv><<<nblk_cta, tile_threads<TXv, TYv>(), sm, s>>>(a, G);
+  stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv><<<nblk_cta, TXv * TYv, sm, s>>>(a, G);
   return cudaGetLastError();
 }
 
