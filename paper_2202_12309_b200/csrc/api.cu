@@ -351,13 +351,34 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
     int bits = bc_bits(m, b);
     if (b.has_coarser) {
       int cs = cslot[gid];
-      XTask t{};
-      t.kind = T_CRESTRICT;
-      t.dst_slot = cs;
-      t.src_slot = (int)b.local;
-      for (int d = 0; d < 3; ++d) { t.lo[d] = 0; t.ext[d] = m->G.nc[d]; t.so[d] = 0; }
-      t.ncell = t.ext[0] * t.ext[1] * t.ext[2];
-      add_chunks(P.b1, t);
+      // own interior into the staging.  Phase C (prolongation) reads the staging at and next to its
+      // ghost layer, and physical BCs on the staging mirror cg interior layers, so the outer cg coarse
+      // layers of the interior suffice: a non-overlapping shell (x slabs whole, y slabs without the x
+      // slabs, z slabs inside both); the whole interior when the shell would cover it anyway.  This
+      // phase is HBM-bound (it reads the block's fine interior), so the shell saves its bytes.
+      const int* nc = m->G.nc;
+      const int T = m->G.cg;
+      auto shell = [&](int lo0, int e0, int lo1, int e1, int lo2, int e2) {
+        XTask t{};
+        t.kind = T_CRESTRICT;
+        t.dst_slot = cs;
+        t.src_slot = (int)b.local;
+        t.lo[0] = lo0; t.ext[0] = e0;
+        t.lo[1] = lo1; t.ext[1] = e1;
+        t.lo[2] = lo2; t.ext[2] = e2;
+        t.ncell = e0 * e1 * e2;
+        if (t.ncell > 0) add_chunks(P.b1, t);
+      };
+      if (getenv("PH_FULL_STAGING") || nc[0] <= 2 * T || nc[1] <= 2 * T || nc[2] <= 2 * T) {
+        shell(0, nc[0], 0, nc[1], 0, nc[2]);
+      } else {
+        shell(0, T, 0, nc[1], 0, nc[2]);
+        shell(nc[0] - T, T, 0, nc[1], 0, nc[2]);
+        shell(T, nc[0] - 2 * T, 0, T, 0, nc[2]);
+        shell(T, nc[0] - 2 * T, nc[1] - T, T, 0, nc[2]);
+        shell(T, nc[0] - 2 * T, T, nc[1] - 2 * T, 0, T);
+        shell(T, nc[0] - 2 * T, T, nc[1] - 2 * T, nc[2] - T, T);
+      }
       for (int q = 0; q < 27; ++q) {
         if (q == 13 || kind[q] == -2 || kind[q] == -1) continue;
         int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
