@@ -45,6 +45,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--case", default="blast")
     ap.add_argument("--halo", default="auto", choices=["auto", "nccl", "peer"])
+    ap.add_argument("--cycles", type=int, default=0, help="override the case's cycle count (soak runs)")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -53,7 +54,9 @@ def main():
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    C = CASES[a.case]
+    C = dict(CASES[a.case])
+    if a.cycles > 0:
+        C["cycles"] = a.cycles
     transport = {"auto": P.HALO_AUTO, "nccl": P.HALO_NCCL, "peer": P.HALO_PEER}[a.halo]
     m = P.Mesh(device=local, rank=rank, nranks=world, halo_transport=transport, **C["kw"])
     m.set_problem(C["problem"], C["params"])
