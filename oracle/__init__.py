@@ -8,7 +8,7 @@ is built from ``oracle/oracle.cpp`` alone (plain scalar C++, ``-O2
 -ffp-contract=off``).
 
 Parity status per function ("Oracle pins"):
-  cons<->prim, PLM, HLLE, restriction, prolongation, Morton, partition, tree/2:1,
+  cons<->prim, PLM, HLLE (Davis and Einfeldt), restriction, prolongation, Morton, partition, tree/2:1,
   neighbours, exchange, flux correction, dt, totals, RK2  -> pinned (tests/test_oracle_*.py)
   AMR refinement criterion (A14), derefinement gate (A16), staging geometry (A12),
   VL2, van Leer / MC limiters                              -> parity unpinned by the paper
@@ -30,6 +30,7 @@ MINMOD, VANLEER, MC, PPM, WENOZ = 0, 1, 2, 3, 4
 RK2, VL2 = 0, 1
 LINEAR_WAVE, SOD, BLAST, KH = 0, 1, 2, 3
 REF_NONE, REF_STATIC, REF_ADAPTIVE = 0, 1, 2
+DAVIS, EINFELDT = 0, 1
 
 
 def build(force: bool = False) -> str:
@@ -58,6 +59,7 @@ class _Cfg(C.Structure):
         ("derefine_interval", C.c_int32),
         ("nregions", C.c_int32), ("regions", C.POINTER(C.c_double)),
         ("nranks", C.c_int32), ("nthreads", C.c_int32),
+        ("wavespeed", C.c_int32),
     ]
 
 
@@ -90,6 +92,8 @@ def lib():
         L.orc_recon5.restype = None
         L.orc_hlle.argtypes = [dp, dp, C.c_double, dp]
         L.orc_hlle.restype = None
+        L.orc_hlle_ws.argtypes = [dp, dp, C.c_double, C.c_int32, dp]
+        L.orc_hlle_ws.restype = None
         L.orc_flux_phys.argtypes = [dp, C.c_double, dp]
         L.orc_flux_phys.restype = None
         L.orc_restrict8.argtypes = [dp]
@@ -164,11 +168,14 @@ def recon5(q, recon):
     return a.value, b.value
 
 
-def hlle(WL, WR, gamma):
+def hlle(WL, WR, gamma, wavespeed=DAVIS):
     WL = np.ascontiguousarray(WL, dtype=np.float64)
     WR = np.ascontiguousarray(WR, dtype=np.float64)
     F = np.zeros(5)
-    lib().orc_hlle(_dp(WL), _dp(WR), gamma, _dp(F))
+    if wavespeed == DAVIS:
+        lib().orc_hlle(_dp(WL), _dp(WR), gamma, _dp(F))
+    else:
+        lib().orc_hlle_ws(_dp(WL), _dp(WR), gamma, wavespeed, _dp(F))
     return F
 
 
@@ -215,7 +222,7 @@ DEFAULTS = dict(
     bc_inner=(PERIODIC,) * 3, bc_outer=(PERIODIC,) * 3,
     gamma=5.0 / 3.0, cfl=0.3, recon=MINMOD, integrator=RK2,
     refinement=REF_NONE, refine_tol=0.1, derefine_tol=0.025, derefine_interval=8,
-    regions=(), nranks=1, nthreads=0,
+    regions=(), nranks=1, nthreads=0, wavespeed=DAVIS,
 )
 
 
@@ -224,7 +231,7 @@ class Mesh:
 
     def __init__(self, **kw):
         c = dict(DEFAULTS)
-        unknown = set(kw) - set(c) - {"pack_size", "wavespeed"}
+        unknown = set(kw) - set(c) - {"pack_size"}
         if unknown:
             raise TypeError(f"unknown config keys {unknown}")
         c.update({k: v for k, v in kw.items() if k in c})
@@ -252,6 +259,7 @@ class Mesh:
         cfg.regions = _dp(regs) if regs.size else None
         cfg.nranks = c["nranks"]
         cfg.nthreads = c["nthreads"]
+        cfg.wavespeed = c["wavespeed"]
         self._cfg = cfg
         h = C.c_void_p()
         _check(lib().orc_mesh_create(C.byref(cfg), C.byref(h)))

@@ -186,19 +186,37 @@ void phys(const double* W, double gamma, double* U, double* F) {
   F[0] = mu; F[1] = mu * u + p; F[2] = mu * v; F[3] = mu * w; F[4] = (E + p) * u;
 }
 
-/* a4: HLLE with Davis wave speeds in the clamped branch-free form (A4, A5) */
-void hlle(const double* WL, const double* WR, double gamma, double* F) {
+/* a4: HLLE in the clamped branch-free form (A4, A5) with Davis wave speeds, or Einfeldt's:
+ * the Roe averages (weights sqrt(rho)) of velocity and total enthalpy H = (E + p) / rho give
+ * c~^2 = (gamma - 1)(H~ - |v~|^2 / 2), and u~ -+ c~ join the min / max. */
+void hlle(const double* WL, const double* WR, double gamma, double* F, int ws = ORC_WS_DAVIS) {
   double cl = std::sqrt(gamma * WL[4] / WL[0]);
   double cr = std::sqrt(gamma * WR[4] / WR[0]);
-  double a = WL[1] - cl, b = WR[1] - cr;
-  double sl = a < b ? a : b;
-  a = WL[1] + cl; b = WR[1] + cr;
-  double sr = a > b ? a : b;
-  double bp = sr > 0.0 ? sr : 0.0;
-  double bm = sl < 0.0 ? sl : 0.0;
   double UL[5], FL[5], UR[5], FR[5];
   phys(WL, gamma, UL, FL);
   phys(WR, gamma, UR, FR);
+  // Davis: S_L = min(u_L - c_L, u_R - c_R), S_R = max(u_L + c_L, u_R + c_R)
+  double a = WL[1] - cl, b = WR[1] - cr;
+  double sl = a < b ? a : b;
+  a = WL[1] + cl;
+  b = WR[1] + cr;
+  double sr = a > b ? a : b;
+  if (ws == ORC_WS_EINFELDT) {
+    // Einfeldt: S_L = min(u_L - c_L, u~ - c~), S_R = max(u_R + c_R, u~ + c~)
+    const double rl = std::sqrt(WL[0]), rr = std::sqrt(WR[0]);
+    const double u = (rl * WL[1] + rr * WR[1]) / (rl + rr);
+    const double v = (rl * WL[2] + rr * WR[2]) / (rl + rr);
+    const double w = (rl * WL[3] + rr * WR[3]) / (rl + rr);
+    const double hl = (UL[4] + WL[4]) / WL[0], hr = (UR[4] + WR[4]) / WR[0];
+    const double h = (rl * hl + rr * hr) / (rl + rr);
+    const double c = std::sqrt((gamma - 1.0) * (h - 0.5 * (u * u + (v * v + w * w))));
+    a = WL[1] - cl;
+    sl = a < u - c ? a : u - c;
+    b = WR[1] + cr;
+    sr = b > u + c ? b : u + c;
+  }
+  double bp = sr > 0.0 ? sr : 0.0;
+  double bm = sl < 0.0 ? sl : 0.0;
   double inv = 1.0 / (bp - bm);
   double bb = bp * bm;
   for (int n = 0; n < 5; ++n) F[n] = ((bp * FL[n] - bm * FR[n]) + bb * (UR[n] - UL[n])) * inv;
@@ -797,7 +815,7 @@ int compute_fluxes(const orc_mesh* m, const Block& b, const std::vector<double>&
           double wl[5] = {WL[0], WL[1 + d], WL[1 + t1], WL[1 + t2], WL[4]};
           double wr[5] = {WR[0], WR[1 + d], WR[1 + t1], WR[1 + t2], WR[4]};
           double fn[5];
-          hlle(wl, wr, gamma, fn);
+          hlle(wl, wr, gamma, fn, m->cfg.wavespeed);
           double fo[5];
           fo[0] = fn[0];
           fo[1 + d] = fn[1];
@@ -1127,6 +1145,9 @@ void orc_plm(double qm, double q0, double qp, int32_t recon, double* ql, double*
 }
 void orc_recon5(const double q[5], int32_t recon, double* ql, double* qr) { recon5(q, recon, ql, qr); }
 void orc_hlle(const double WL[5], const double WR[5], double gamma, double F[5]) { hlle(WL, WR, gamma, F); }
+void orc_hlle_ws(const double WL[5], const double WR[5], double gamma, int32_t wavespeed, double F[5]) {
+  hlle(WL, WR, gamma, F, wavespeed);
+}
 void orc_flux_phys(const double W[5], double gamma, double F[5]) {
   double U[5];
   phys(W, gamma, U, F);
@@ -1148,6 +1169,10 @@ int orc_mesh_create(const orc_config* cfg, orc_mesh** out) {
   if (cfg->recon >= ORC_RECON_PPM && cfg->nghost != 3) return fail(ORC_ERR_CONFIG, "PPM / WENO-Z need nghost = 3 (A8)");
   if (cfg->nghost == 3 && cfg->max_level > 0)
     return fail(ORC_ERR_CONFIG, "nghost = 3 is supported on uniform meshes only (reading A39)");
+  if (cfg->wavespeed != ORC_WS_DAVIS && cfg->wavespeed != ORC_WS_EINFELDT)
+    return fail(ORC_ERR_CONFIG, "unknown wave-speed estimate");
+  if (cfg->wavespeed == ORC_WS_EINFELDT && cfg->recon >= ORC_RECON_PPM)
+    return fail(ORC_ERR_CONFIG, "Einfeldt wave speeds are implemented for PLM (PPM / WENO-Z use Davis)");
   if (!(cfg->gamma > 1.0)) return fail(ORC_ERR_CONFIG, "gamma must exceed 1");
   if (!(cfg->cfl > 0.0)) return fail(ORC_ERR_CONFIG, "cfl must be positive");
   if (cfg->max_level < 0 || cfg->max_level > 10) return fail(ORC_ERR_CONFIG, "max_level out of range");

@@ -28,6 +28,10 @@ enum { ORC_RECON_MINMOD = 0, ORC_RECON_VANLEER = 1, ORC_RECON_MC = 2, ORC_RECON_
 enum { ORC_INT_RK2 = 0, ORC_INT_VL2 = 1 };
 enum { ORC_PROB_LINEAR_WAVE = 0, ORC_PROB_SOD = 1, ORC_PROB_BLAST = 2, ORC_PROB_KH = 3 };
 enum { ORC_REF_NONE = 0, ORC_REF_STATIC = 1, ORC_REF_ADAPTIVE = 2 };
+/* HLLE wave-speed estimates (A4): Davis min/max of the face states' u -+ c (default), or Einfeldt
+ * (1988): the Roe-averaged speeds u~ -+ c~ also enter the min/max (S_L = min(u_L - c_L, u~ - c~),
+ * S_R = max(u_R + c_R, u~ + c~)). */
+enum { ORC_WS_DAVIS = 0, ORC_WS_EINFELDT = 1 };
 
 typedef struct {
   int64_t mesh_nx[3];      /* root-grid cells per dim */
@@ -45,6 +49,7 @@ typedef struct {
   const double* regions;
   int32_t nranks;          /* simulated ranks: only the partition depends on it */
   int32_t nthreads;        /* OpenMP threads over blocks (0 = default) */
+  int32_t wavespeed;       /* ORC_WS_* (PLM meshes; PPM / WENO-Z use Davis) */
 } orc_config;
 
 typedef struct { int64_t gid; int32_t level, rank; int64_t lx[3]; double xmin[3], xmax[3]; } orc_block;
@@ -88,6 +93,7 @@ void orc_plm(double qm, double q0, double qp, int32_t recon, double* q_left_face
 void orc_recon5(const double q[5], int32_t recon, double* q_left_face, double* q_right_face);
 /* HLLE in the face-normal frame: W = (rho, u_normal, v_t1, v_t2, p) */
 void orc_hlle(const double WL[5], const double WR[5], double gamma, double F[5]);
+void orc_hlle_ws(const double WL[5], const double WR[5], double gamma, int32_t wavespeed, double F[5]);
 void orc_flux_phys(const double W[5], double gamma, double F[5]);
 double orc_restrict8(const double v[8]); /* v in (k,j,i) child order */
 /* prolongation of one coarse value with neighbours cm[d] = C_{-d}, cp[d] = C_{+d}; out[8] in (k,j,i) child order */

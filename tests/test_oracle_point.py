@@ -142,6 +142,59 @@ def test_hlle_mirror_antisymmetry_bitwise(oracle_mod):
         assert np.array_equal(G, F * np.array([-1, 1, -1, -1, -1.0]))
 
 
+def _normal_shock(M, gamma, V):
+    """states on either side of a shock of Mach number M (textbook Rankine-Hugoniot relations, e.g.
+    Toro eqs. 3.50-3.51) in a frame where the shock moves with speed V; the upstream gas (rho 1, p 1)
+    comes from the left, so the shock is a left-facing (u - c family) wave"""
+    c1 = np.sqrt(gamma)
+    u1 = M * c1                                   # upstream speed relative to the shock
+    r = (gamma + 1) * M * M / ((gamma - 1) * M * M + 2)
+    p2 = 1.0 + 2 * gamma / (gamma + 1) * (M * M - 1)
+    u2 = u1 / r
+    WL = np.array([1.0, u1 + V, 0.2, -0.1, 1.0])
+    WR = np.array([r, u2 + V, 0.2, -0.1, p2])
+    return WL, WR
+
+
+@pytest.mark.parametrize("M", [1.5, 3.0, 10.0])
+@pytest.mark.parametrize("V", [-0.4, 0.0, 0.6])
+def test_hlle_einfeldt_exact_at_an_isolated_shock(oracle_mod, M, V):
+    """Roe's property: across a single shock the Roe-averaged speed u~ - c~ equals the shock speed, so
+    the Einfeldt HLLE flux is the exact Godunov flux (F_R for a left-moving shock, F_L otherwise) --
+    any slip in the sqrt(rho) weights, the enthalpy average or c~ breaks this.  Davis' speeds do not
+    have the property (the flux carries numerical dissipation)."""
+    g = 1.4
+    WL, WR = _normal_shock(M, g, V)
+    FL, UL = _phys_flux(WL, g)
+    FR, UR = _phys_flux(WR, g)
+    np.testing.assert_allclose(FR - FL, V * (UR - UL), rtol=1e-12, atol=1e-12)  # R-H check of the fixture
+    exact = FR if V < 0 else FL
+    F = oracle_mod.hlle(WL, WR, g, oracle_mod.EINFELDT)
+    scale = np.abs(exact).max()
+    assert np.abs(F - exact).max() <= 1e-13 * scale, (F, exact)
+    D = oracle_mod.hlle(WL, WR, g, oracle_mod.DAVIS)
+    if V <= 0:
+        assert np.abs(D - exact).max() > 1e-6 * scale
+
+
+def test_hlle_einfeldt_consistency_and_mirror(oracle_mod):
+    rng = np.random.default_rng(4)
+    mir = np.array([1, -1, 1, 1, 1.0])
+    for _ in range(500):
+        W = np.array([rng.uniform(0.1, 5), *rng.normal(0, 2, 3), rng.uniform(0.1, 5)])
+        F = oracle_mod.hlle(W, W, 1.4, oracle_mod.EINFELDT)
+        Fx, _ = _phys_flux(W, 1.4)
+        assert np.all(np.abs(F - Fx) <= 1.6e-15 * (np.abs(Fx).max() + W[4]))
+        WL = np.array([rng.uniform(0.1, 5), *rng.normal(0, 1, 3), rng.uniform(0.1, 5)])
+        WR = np.array([rng.uniform(0.1, 5), *rng.normal(0, 1, 3), rng.uniform(0.1, 5)])
+        F = oracle_mod.hlle(WL, WR, 1.4, oracle_mod.EINFELDT)
+        G = oracle_mod.hlle(WR * mir, WL * mir, 1.4, oracle_mod.EINFELDT)
+        np.testing.assert_allclose(G, F * np.array([-1, 1, -1, -1, -1.0]), rtol=1e-13, atol=1e-14)
+        # the Einfeldt interval contains the Davis one: never less dissipative than Davis' bounds allow
+        D = oracle_mod.hlle(WL, WR, 1.4, oracle_mod.DAVIS)
+        assert np.all(np.isfinite(F)) and np.all(np.isfinite(D))
+
+
 # ------------------------------------------------------------------ restriction / prolongation (A10, A11)
 def test_restrict_examples(oracle_mod):
     ex = gold("spec_examples.json")["restrict_pair"]
