@@ -1,5 +1,5 @@
 /*
- * ph.h -- C ABI of the B200-native Parthenon-hydro hot path (ABI version 2).
+ * ph.h -- C ABI of the B200-native Parthenon-hydro hot path (ABI version 3).
  *
  * What it computes (PAPER.md = arXiv 2202.12309, cited P:line):
  *   the per-cycle update of the Parthenon-hydro miniapp (§4.1: "a two-stage
@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define PH_ABI_VERSION 2
+#define PH_ABI_VERSION 3
 
 typedef struct ph_mesh ph_mesh; /* opaque; owned by the caller until ph_mesh_destroy */
 
@@ -59,6 +59,10 @@ typedef enum {
   PH_RECON_PPM = 3, PH_RECON_WENOZ = 4                                   /* NEXT 3 (A37, A38); nghost 3 */
 } ph_recon;
 typedef enum { PH_INT_RK2 = 0, PH_INT_VL2 = 1 } ph_integrator;                      /* A1 */
+/* HLLE wave-speed estimates (A4): Davis S_L = min(u_L - c_L, u_R - c_R), S_R = max(u_L + c_L, u_R + c_R)
+ * (default), or Einfeldt (1988) S_L = min(u_L - c_L, u~ - c~), S_R = max(u_R + c_R, u~ + c~) with Roe
+ * averages (sqrt(rho) weights) of velocity and total enthalpy.  Einfeldt: PLM reconstructions only. */
+typedef enum { PH_WS_DAVIS = 0, PH_WS_EINFELDT = 1 } ph_wavespeed;
 typedef enum { PH_PROB_LINEAR_WAVE = 0, PH_PROB_SOD = 1, PH_PROB_BLAST = 2, PH_PROB_KH = 3 } ph_problem;
 typedef enum { PH_REF_NONE = 0, PH_REF_STATIC = 1, PH_REF_ADAPTIVE = 2 } ph_refinement;
 /* How the per-cycle halo of a uniform multi-GPU mesh travels between GPUs.  Either way blocks with
@@ -103,6 +107,7 @@ typedef struct {
                                        non-adaptive, nghost-2 meshes with nranks > 1; its receive
                                        buffers come from cudaMalloc (CUDA IPC), not dev_alloc.
                                        The full exchange (ph_refresh, ph_exchange) stays on NCCL. */
+  int32_t wavespeed;                /* ph_wavespeed (ABI 3); 0 = Davis */
 } ph_config;
 
 /* One leaf block.  gid = position in Z-order (A19); rank from the contiguous Morton partition. */

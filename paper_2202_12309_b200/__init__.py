@@ -7,4 +7,4 @@ There is no CPU fallback: if ``libph.so`` is missing the import fails loudly.
 """
 from .ph import Mesh, PhError, lib, PERIODIC, OUTFLOW, REFLECT, MINMOD, VANLEER, MC, PPM, WENOZ, RK2, VL2  # noqa: F401
 from .ph import LINEAR_WAVE, SOD, BLAST, KH, REF_NONE, REF_STATIC, REF_ADAPTIVE  # noqa: F401
-from .ph import HALO_AUTO, HALO_NCCL, HALO_PEER  # noqa: F401
+from .ph import HALO_AUTO, HALO_NCCL, HALO_PEER, DAVIS, EINFELDT  # noqa: F401

@@ -1411,6 +1411,10 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
     return fail(PH_ERR_INVALID_ARG, "bad rank / nranks");
   if (cfg->recon < 0 || cfg->recon > 4 || cfg->integrator < 0 || cfg->integrator > 1)
     return fail(PH_ERR_CONFIG, "unknown recon / integrator");
+  if (cfg->wavespeed != PH_WS_DAVIS && cfg->wavespeed != PH_WS_EINFELDT)
+    return fail(PH_ERR_CONFIG, "unknown wave-speed estimate");
+  if (cfg->wavespeed == PH_WS_EINFELDT && cfg->recon >= PH_RECON_PPM)
+    return fail(PH_ERR_CONFIG, "Einfeldt wave speeds are implemented for PLM (PPM / WENO-Z use Davis)");
   if (cfg->max_level < 0 || cfg->max_level > 10) return fail(PH_ERR_CONFIG, "max_level out of range");
   MeshCfg mc{};
   for (int d = 0; d < 3; ++d) {
@@ -1464,6 +1468,7 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
   G.gm1 = cfg->gamma - 1.0;
   G.inv_gm1 = 1.0 / (cfg->gamma - 1.0);
   G.cfl = cfg->cfl;
+  G.wavespeed = cfg->wavespeed;
   try {
     m->tree = new Tree(mc);
     if (cfg->refinement != PH_REF_NONE && cfg->max_level > 0) m->tree->refine_regions(m->regions);

@@ -24,6 +24,7 @@ struct Geom {
   double gamma, gm1, inv_gm1;
   double cfl;
   int exact;       // 1: high-order path computes in the oracle's exact operation order (NEXT 3)
+  int wavespeed;   // HLLE wave speeds: 0 Davis, 1 Einfeldt (A4)
 };
 
 // Per local block slot.

@@ -93,20 +93,37 @@ __device__ __forceinline__ double sound_speed(double rho, double p, double gamma
 __device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
 __device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
 
-// HLLE, Davis speeds, clamped branch-free form (a4; A4, A5).  w = (rho, u_n, v_t1, v_t2, p).
+// HLLE in the clamped branch-free form (a4; A4, A5).  w = (rho, u_n, v_t1, v_t2, p).  Wave speeds:
+// Davis (EIN = false), or Einfeldt (EIN = true): the Roe averages (sqrt(rho) weights) of velocity
+// and total enthalpy H = (E + p) / rho give c~^2 = (gamma - 1)(H~ - |v~|^2 / 2), and
+// S_L = min(u_L - c_L, u~ - c~), S_R = max(u_R + c_R, u~ + c~).
+template <bool EIN = false>
 __device__ __forceinline__ void hlle(const double* wl, const double* wr, const Geom& G, double* F) {
   double cl = sound_speed(wl[0], wl[4], G.gamma);
   double cr = sound_speed(wr[0], wr[4], G.gamma);
-  double sl = dmin(wl[1] - cl, wr[1] - cr);
-  double sr = dmax(wl[1] + cl, wr[1] + cr);
-  double bp = dmax(sr, 0.0);
-  double bm = dmin(sl, 0.0);
-  double inv = rcp_nr(bp - bm);
-  double bb = bp * bm;
   double mul = wl[0] * wl[1];
   double El = wl[4] * G.inv_gm1 + (0.5 * wl[0]) * (wl[1] * wl[1] + (wl[2] * wl[2] + wl[3] * wl[3]));
   double mur = wr[0] * wr[1];
   double Er = wr[4] * G.inv_gm1 + (0.5 * wr[0]) * (wr[1] * wr[1] + (wr[2] * wr[2] + wr[3] * wr[3]));
+  double sl, sr;
+  if (EIN) {
+    const double rl = wl[0] * rsqrt_nr(wl[0]), rr = wr[0] * rsqrt_nr(wr[0]);  // sqrt(rho)
+    const double is = rcp_nr(rl + rr);
+    const double u = (rl * wl[1] + rr * wr[1]) * is, v = (rl * wl[2] + rr * wr[2]) * is,
+                 w = (rl * wl[3] + rr * wr[3]) * is;
+    const double h = (rl * ((El + wl[4]) * rcp_nr(wl[0])) + rr * ((Er + wr[4]) * rcp_nr(wr[0]))) * is;
+    const double c2 = G.gm1 * (h - 0.5 * (u * u + (v * v + w * w)));
+    const double c = c2 * rsqrt_nr(c2);
+    sl = dmin(wl[1] - cl, u - c);
+    sr = dmax(wr[1] + cr, u + c);
+  } else {
+    sl = dmin(wl[1] - cl, wr[1] - cr);
+    sr = dmax(wl[1] + cl, wr[1] + cr);
+  }
+  double bp = dmax(sr, 0.0);
+  double bm = dmin(sl, 0.0);
+  double inv = rcp_nr(bp - bm);
+  double bb = bp * bm;
   // F = ((bp FL - bm FR) + bb (UR - UL)) * inv
   F[0] = ((bp * mul - bm * mur) + bb * (wr[0] - wl[0])) * inv;
   F[1] = ((bp * (mul * wl[1] + wl[4]) - bm * (mur * wr[1] + wr[4])) + bb * (mur - mul)) * inv;
@@ -276,7 +293,7 @@ constexpr int TX = TILE_X, TY = TILE_Y, NCELL = TX * TY, NT = NCELL;
 // One face: PLM states from the 4 stencil points p0..p3 (cells c-2 .. c+1 along the normal) of
 // the smem primitives, permuted so that w = (rho, u_normal, v_t1, v_t2, p), then HLLE.  F is
 // returned in natural component order.  CN/C1/C2: variable index of normal, t1, t2.
-template <int RECON, int CN, int C1, int C2, int VSv>
+template <int RECON, int CN, int C1, int C2, int VSv, bool EIN = false>
 __device__ __forceinline__ void face_flux(const double* p0, const double* p1, const double* p2, const double* p3,
                                           const Geom& G, double* F) {
   constexpr int cv[NVAR] = {0, CN, C1, C2, 4};
@@ -286,7 +303,7 @@ __device__ __forceinline__ void face_flux(const double* p0, const double* p1, co
     const int o = cv[s] * VSv;
     plm_face<RECON>(p0[o], p1[o], p2[o], p3[o], wl[s], wr[s]);
   }
-  hlle(wl, wr, G, Fn);
+  hlle<EIN>(wl, wr, G, Fn);
   F[0] = Fn[0];
   F[CN] = Fn[1];
   F[C1] = Fn[2];
@@ -294,7 +311,8 @@ __device__ __forceinline__ void face_flux(const double* p0, const double* p1, co
   F[4] = Fn[4];
 }
 
-template <int RECON, bool REDUCE, bool USE_U0, bool ML, bool FULL, bool HB, int TXv = TILE_X, int TYv = TILE_Y>
+template <int RECON, bool REDUCE, bool USE_U0, bool ML, bool FULL, bool HB, int TXv = TILE_X, int TYv = TILE_Y,
+          bool EIN = false>
 __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G) {
   // tile geometry (32x8, or 16x16 for 16-wide blocks), shadowing the 32x8 constants
   constexpr int TX = TXv, TY = TYv, NCELL = TX * TY, NT = NCELL;
@@ -457,7 +475,7 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
         const int j = t / TX, fi = t - j * TX + 1;
         const double* p = Wc + (j + 2) * SWX + fi;
         double F[NVAR];
-        face_flux<RECON, 1, 2, 3, VS>(p, p + 1, p + 2, p + 3, G, F);
+        face_flux<RECON, 1, 2, 3, VS, EIN>(p, p + 1, p + 2, p + 3, G, F);
         double* d = sFx + j * (TX + 1) + fi;
         d[0] = F[0]; d[FXS] = F[1]; d[2 * FXS] = F[2]; d[3 * FXS] = F[3]; d[4 * FXS] = F[4];
       }
@@ -466,7 +484,7 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
         const int jf = t / TX + 1, i = t - (jf - 1) * TX;
         const double* p = Wc + jf * SWX + (i + 2);
         double F[NVAR];
-        face_flux<RECON, 2, 3, 1, VS>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
+        face_flux<RECON, 2, 3, 1, VS, EIN>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
         double* d = sFy + jf * TX + i;
         d[0] = F[0]; d[FYS] = F[1]; d[2 * FYS] = F[2]; d[3 * FYS] = F[3]; d[4 * FYS] = F[4];
       }
@@ -487,13 +505,13 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
           if ((warp_id == 1 || warp_id == 3) && lane < TY) {
             const double* p = Wn + (lane + 2) * SWX;
             double F[NVAR];
-            face_flux<RECON, 1, 2, 3, VS>(p, p + 1, p + 2, p + 3, G, F);
+            face_flux<RECON, 1, 2, 3, VS, EIN>(p, p + 1, p + 2, p + 3, G, F);
 #pragma unroll
             for (int v = 0; v < NVAR; ++v) ex[v * (TX + TY) + lane] = F[v];
           } else if ((warp_id == 2 || warp_id == 5) && lane < TX) {
             const double* p = Wn + (lane + 2);
             double F[NVAR];
-            face_flux<RECON, 2, 3, 1, VS>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
+            face_flux<RECON, 2, 3, 1, VS, EIN>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
 #pragma unroll
             for (int v = 0; v < NVAR; ++v) ex[v * (TX + TY) + TY + lane] = F[v];
           }
@@ -505,7 +523,7 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
         if (FULL || (j < nyt && fi <= nxt)) {
           const double* p = Wc + (j + 2) * SWX + fi;
           double F[NVAR];
-          face_flux<RECON, 1, 2, 3, VS>(p, p + 1, p + 2, p + 3, G, F);
+          face_flux<RECON, 1, 2, 3, VS, EIN>(p, p + 1, p + 2, p + 3, G, F);
           double* d = sFx + j * (TX + 1) + fi;
           d[0] = F[0]; d[FXS] = F[1]; d[2 * FXS] = F[2]; d[3 * FXS] = F[3]; d[4 * FXS] = F[4];
           if (ML) {
@@ -529,7 +547,7 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
         if (FULL || (jf <= nyt && i < nxt)) {
           const double* p = Wc + jf * SWX + (i + 2);
           double F[NVAR];
-          face_flux<RECON, 2, 3, 1, VS>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
+          face_flux<RECON, 2, 3, 1, VS, EIN>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
           double* d = sFy + jf * TX + i;
           d[0] = F[0]; d[FYS] = F[1]; d[2 * FYS] = F[2]; d[3 * FYS] = F[3]; d[4 * FYS] = F[4];
           if (ML) {
@@ -571,7 +589,7 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
         const double wl[NVAR] = {topz[0], topz[3], topz[1], topz[2], topz[4]};  // normal = x3
         const double wr[NVAR] = {bot[0], bot[3], bot[1], bot[2], bot[4]};
         double Fn[NVAR];
-        hlle(wl, wr, G, Fn);
+        hlle<EIN>(wl, wr, G, Fn);
         const double F[NVAR] = {Fn[0], Fn[2], Fn[3], Fn[1], Fn[4]};
         double* d = sFz + (fz & 1) * NVAR * FZS + tid;
         d[0] = F[0]; d[FZS] = F[1]; d[2 * FZS] = F[2]; d[3 * FZS] = F[3]; d[4 * FZS] = F[4];
@@ -666,7 +684,7 @@ size_t stage_smem_bytes() { return stage_smem_bytes_t<TILE_X, TILE_Y>(); }
 // (e.g. 16^3 blocks, which would leave half of a 32-wide tile idle); everything else runs 32x8 tiles
 // with bounds checks.  Returns whether the full-tile path applies.
 bool stage_tile(const Geom& G, int recon, bool ml, int* tx, int* ty) {
-  const bool mm = recon == 0 && !ml;
+  const bool mm = recon == 0 && !ml && G.wavespeed == 0;  // the Einfeldt variant runs bounds-checked tiles
   if (mm && G.n[0] % TILE_X == 0 && G.n[1] % TILE_Y == 0) {
     *tx = TILE_X;
     *ty = TILE_Y;
@@ -1489,30 +1507,31 @@ __global__ void remesh_kernel(const RemeshTask* tasks, const double* Uold, doubl
 // ------------------------------------------------------------------------------ launchers
 #define PH_CHECK_LAUNCH() cudaGetLastError()
 
-template <int R, bool RD, bool U0, bool ML, bool FULL, bool HB = false, int TXv = TILE_X, int TYv = TILE_Y>
+template <int R, bool RD, bool U0, bool ML, bool FULL, bool HB = false, int TXv = TILE_X, int TYv = TILE_Y,
+          bool EIN = false>
 static cudaError_t launch_stage_t(int nblk_cta, const StageArgs& a, const Geom& G, cudaStream_t s) {
   const size_t sm = stage_smem_bytes_t<TXv, TYv>();
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv>,
+    cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv, EIN>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     if (getenv("PH_DEBUG_ATTR")) {
       cudaFuncAttributes fa;
-      cudaFuncGetAttributes(&fa, stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv>);
+      cudaFuncGetAttributes(&fa, stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv, EIN>);
       fprintf(stderr, "stage_kernel<%d,%d,%d,%d,%d>: regs %d maxThreads %d static smem %zu local %zu dyn %zu (max dyn %d) NT %d\n",
               R, (int)RD, (int)U0, (int)ML, (int)FULL, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
               fa.localSizeBytes, sm, fa.maxDynamicSharedSizeBytes, NT);
     }
     // shared-memory carveout hint (percent of the maximum); the rest of the 256 KB is L1
     if (const char* cv = getenv("PH_CARVEOUT")) {
-      e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv>, cudaFuncAttributePreferredSharedMemoryCarveout,
+      e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv, EIN>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                atoi(cv));
       if (e != cudaSuccess) return e;
     }
     attr = true;
   }
-  stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv><<<nblk_cta, TXv * TYv, sm, s>>>(a, G);
+  stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv, EIN><<<nblk_cta, TXv * TYv, sm, s>>>(a, G);
   return cudaGetLastError();
 }
 
@@ -1528,6 +1547,9 @@ static cudaError_t launch_stage_ml(bool ml, int n, const StageArgs& a, const Geo
   }
   if (full && a.H) return launch_stage_t<0, RD, U0, false, true, true>(n, a, G, s);
   if (full) return launch_stage_t<0, RD, U0, false, true>(n, a, G, s);
+  if (G.wavespeed)  // Einfeldt wave speeds (A4 variant)
+    return ml ? launch_stage_t<R, RD, U0, true, false, false, TILE_X, TILE_Y, true>(n, a, G, s)
+              : launch_stage_t<R, RD, U0, false, false, false, TILE_X, TILE_Y, true>(n, a, G, s);
   return ml ? launch_stage_t<R, RD, U0, true, false>(n, a, G, s) : launch_stage_t<R, RD, U0, false, false>(n, a, G, s);
 }
 

@@ -18,7 +18,8 @@ MINMOD, VANLEER, MC, PPM, WENOZ = 0, 1, 2, 3, 4
 RK2, VL2 = 0, 1
 LINEAR_WAVE, SOD, BLAST, KH = 0, 1, 2, 3
 REF_NONE, REF_STATIC, REF_ADAPTIVE = 0, 1, 2
-ABI_VERSION = 2
+ABI_VERSION = 3
+DAVIS, EINFELDT = 0, 1
 HALO_AUTO, HALO_NCCL, HALO_PEER = 0, 1, 2
 
 _ALLOC = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p)
@@ -42,7 +43,7 @@ class _Cfg(C.Structure):
         ("no_direct_halo", C.c_int32),
         ("stream", C.c_void_p), ("nccl_id", C.c_void_p),
         ("dev_alloc", _ALLOC), ("dev_free", _FREE), ("alloc_ctx", C.c_void_p),
-        ("halo_transport", C.c_int32),
+        ("halo_transport", C.c_int32), ("wavespeed", C.c_int32),
     ]
 
 
@@ -146,7 +147,7 @@ DEFAULTS = dict(
     bc_inner=(PERIODIC,) * 3, bc_outer=(PERIODIC,) * 3,
     gamma=5.0 / 3.0, cfl=0.3, recon=MINMOD, integrator=RK2,
     refine_tol=0.1, derefine_tol=0.025, derefine_interval=8, regions=(), pack_size=0,
-    direct_halo=True, halo_transport=HALO_AUTO,
+    direct_halo=True, halo_transport=HALO_AUTO, wavespeed=DAVIS,
 )
 
 
@@ -188,6 +189,7 @@ class Mesh:
         cfg.host_only = 1 if host_only else 0
         cfg.no_direct_halo = 0 if c["direct_halo"] else 1
         cfg.halo_transport = c["halo_transport"]
+        cfg.wavespeed = c["wavespeed"]
         self._keep = []
         if not host_only:
             import torch

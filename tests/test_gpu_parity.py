@@ -106,6 +106,23 @@ def test_full_tile_stage2_base(oracle_mod, P, integ):
     _check_run(o, g)
 
 
+@pytest.mark.parametrize("case", ["blast", "sod_walls", "two_level"])
+def test_einfeldt_wave_speeds(oracle_mod, P, case):
+    """HLLE with Einfeldt (Roe-averaged) wave speeds (A4 variant, ph_config.wavespeed) vs the oracle"""
+    u = dict(xmin=(-.5,) * 3, xmax=(.5,) * 3, wavespeed=P.EINFELDT)
+    if case == "blast":
+        o, g = _run_both(oracle_mod, P, P.BLAST, [10.0, 0.1, 0.2], 8, mesh_nx=(64, 64, 32), block_nx=(32, 32, 32), **u)
+    elif case == "sod_walls":
+        o, g = _run_both(oracle_mod, P, P.SOD, [0.5], 10, mesh_nx=(128, 16, 16), block_nx=(32, 16, 16), gamma=1.4,
+                         wavespeed=P.EINFELDT, bc_inner=(P.OUTFLOW, P.REFLECT, 0), bc_outer=(P.REFLECT, P.OUTFLOW, 0))
+    else:
+        o, g = _run_both(oracle_mod, P, P.BLAST, [10.0, 0.1, 0.12], 10, mesh_nx=(32, 32, 32), block_nx=(8, 8, 8),
+                         max_level=1, refinement=P.REF_STATIC, regions=[(1, -0.15, 0.15, -0.15, 0.15, -0.15, 0.15)], **u)
+    _check_run(o, g)
+    with pytest.raises(P.PhError):  # PPM / WENO-Z keep Davis speeds
+        P.Mesh(mesh_nx=(32,) * 3, block_nx=(16,) * 3, nghost=3, recon=P.PPM, wavespeed=P.EINFELDT)
+
+
 def test_static_two_level_blast_with_flux_correction(oracle_mod, P):
     kw = dict(mesh_nx=(32, 32, 32), block_nx=(8, 8, 8), xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=1,
               refinement=P.REF_STATIC, regions=[(1, -0.15, 0.15, -0.15, 0.15, -0.15, 0.15)])
