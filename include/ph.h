@@ -9,7 +9,7 @@
  *   boundaries (§3.7), flux correction, the CFL dt min-reduction as a
  *   global reduction (§3.10), Z-order (Morton) distribution of blocks over GPUs
  *    and remeshing with load balancing (§3.8).
- *   Readings where the paper is silent are SURVEY.md §8(c) A1-A30, listed in DESIGN.md.
+ *   Readings where the paper is silent are SURVEY.md §8(c) A1-A30 plus DESIGN.md A5'-A41.
  *
  * Conventions
  *   - Every function returns ph_status; PH_OK == 0.  No C++ exception crosses this boundary.
@@ -24,7 +24,12 @@
  *   - Multi-GPU (cfg->nranks > 1): one process per GPU; every rank calls every function
  *     collectively with identical arguments (except gid / buffers).  NCCL is bootstrapped from
  *     a 128-byte ncclUniqueId that rank 0 obtains with ph_nccl_unique_id and the caller
- *     broadcasts (the Python binding uses torch.distributed).
+ *     broadcasts (the Python binding uses torch.distributed).  On uniform meshes the per-cycle
+ *     halo travels by peer-memory puts over NVLink (CUDA IPC; cfg->halo_transport) or NCCL;
+ *     blocks with remote faces are updated first, interior blocks meanwhile on a second stream.
+ *     The dt / totals reduction is an allgather in rank order, so N GPUs reproduce 1 GPU bitwise.
+ *   - ph_get_state_full after ph_step returns valid ghosts on one rank (a full exchange is run when
+ *     the direct halo left local face ghosts stale); on several ranks call ph_exchange first.
  *   - Host state layout: [5][n3][n2][n1], interior cells only, i fastest, variables
  *     (rho, m1, m2, m3, E) -- conserved variables of the Euler equations.
  *   - Calls on one handle must be serialised by the caller.
@@ -96,8 +101,9 @@ typedef struct {
   int32_t device;                   /* CUDA device ordinal */
   int32_t host_only;                /* 1: build the mesh/partition/exchange plan only (no GPU) */
   int32_t no_direct_halo;           /* 1: materialise every ghost each exchange (the paper's scheme);
-                                       0 (default): on uniform meshes the stage kernel reads local
-                                       same-level face neighbours' interiors directly */
+                                       0 (default): the stage kernel of every block without coarse
+                                       staging reads its local same-level face neighbours' interiors
+                                       directly (all blocks of a uniform mesh) */
   void* stream;                     /* cudaStream_t to enqueue on (borrowed); NULL = legacy default */
   const void* nccl_id;              /* 128-byte ncclUniqueId (nranks > 1), else NULL */
   void* (*dev_alloc)(size_t bytes, void* ctx); /* optional device allocator (torch caching allocator) */
@@ -143,12 +149,14 @@ typedef struct {
   int64_t recv_doubles_from[64];
   uint64_t send_hash_to[64];    /* order-sensitive hash of the (dst gid, entry) sequence */
   uint64_t recv_hash_from[64];
-  /* the per-cycle exchange (direct halo: only remote faces and physical BCs on uniform meshes) */
+  /* the per-cycle exchange (direct halo: blocks without coarse staging drop local same-level face
+     copies and edge / corner entries; on uniform meshes only remote faces and physical BCs remain) */
   int64_t cyc_send_doubles_to[64];
   int64_t cyc_recv_doubles_from[64];
   uint64_t cyc_send_hash_to[64];
   uint64_t cyc_recv_hash_from[64];
-  int32_t direct_halo;          /* 1 if stage kernels read local same-level face neighbours directly */
+  int32_t direct_halo;          /* 1 if stage kernels of blocks without coarse staging read local
+                                   same-level face neighbours directly (uniform and multilevel meshes) */
   int64_t n_cyc_local_tasks;
   int32_t peer_halo;            /* 1 if the per-cycle halo travels by peer-memory puts (ABI 2) */
 } ph_plan_info;
