@@ -147,6 +147,7 @@ struct ph_mesh {
   unsigned long long* my_flags = nullptr;           // [64] in my region, written by peers
   unsigned long long* d_ctr = nullptr;              // [2] signal / wait epoch counters (device)
   unsigned long long send_mask = 0, recv_mask = 0;  // peers I put to / receive from per exchange
+  bool fused_put = false;  // the boundary blocks' stage kernel stores the faces itself (no put kernel)
   // boundary-first schedule of the multi-GPU cycle: B (high priority) runs boundary blocks and the
   // halo, I runs interior blocks concurrently
   cudaStream_t bstream = nullptr, istream = nullptr;
@@ -577,6 +578,8 @@ static ph_status build_plan(ph_mesh* m) {
     for (int f = 0; f < 6; ++f) {
       M.fslot[f] = fslot[b.gid][f];
       M.nb[f] = -1;
+      M.prank[f] = -1;
+      M.poff[f] = 0;
     }
     if (m->direct_halo && !b.has_coarser) {
       for (auto& e : b.nbrs) {
@@ -782,6 +785,29 @@ static ph_status setup_peer(ph_mesh* m, bool* ok_out) {
     t.bc = p;
     t.buf = t.buf - PL.send_off[p] + all[p].recv_off[me];
   }
+  // fused put (PH_FUSED_PUT=1): on the full-tile path the boundary blocks' stage kernel stores its g
+  // boundary layers itself, as cells are finished, instead of a separate put kernel.  Correct (bitwise
+  // vs 1 GPU) but slower at N = 4 (2b -3.5 %, config 4 -7 %, profiles/r01_multi_gpu_halo.md): the
+  // x-face layers are 16 B per row, so those remote stores are fine-grained and add to the stage
+  // kernel's store pressure, while the put kernel writes the packed faces as 256-B warp stores.
+  // Each per-cycle pack task is one face of one block (uniform mesh: faces only), whose source shift
+  // so names the face -- so[d] = +n: the sender's +d layers, -n: its -d layers.
+  int tx = 0, ty = 0;
+  m->fused_put = getenv("PH_FUSED_PUT") && atoi(getenv("PH_FUSED_PUT")) != 0 &&
+                 stage_tile(m->G, m->cfg.recon, false, &tx, &ty);
+  for (const XTask& t : PL.pack.tasks) {
+    int d = 0;
+    while (d < 2 && t.so[d] == 0) ++d;
+    if (t.kind != T_COPY || t.so[d] == 0 || t.ext[d] != m->G.g) m->fused_put = false;  // not a plain face
+    if (!m->fused_put) break;
+    BlockMeta& M = m->meta[t.src_slot];
+    const int f = 2 * d + (t.so[d] > 0 ? 1 : 0);
+    M.prank[f] = t.bc;
+    M.poff[f] = t.buf;
+  }
+  if (!m->fused_put)
+    for (BlockMeta& M : m->meta)
+      for (int f = 0; f < 6; ++f) M.prank[f] = -1;
   *ok_out = true;
   return PH_OK;
 }
@@ -845,7 +871,7 @@ static ph_status exchange_begin(ph_mesh* m, double* U, int which) {
   a.rbuf = m->rbuf;
   const bool put = m->peer && which == 1;  // peer transport: pack straight into the peers' receive halves
   if (put) a.peer_rbuf = m->d_prbuf[U == m->U1 ? 0 : 1];
-  if (PL.pack.nchunks()) {
+  if (PL.pack.nchunks() && !(put && m->fused_put)) {  // fused: the boundary stage kernel stored them
     a.tasks = PL.pack.d_tasks;
     a.chunks = PL.pack.d_chunks;
     CU(launch_xfill(PL.pack.nchunks(), a, m->G, m->stream));
@@ -941,7 +967,7 @@ static ph_status standalone_reduce(ph_mesh* m, double* U, int mode) {
 
 /* one stage over all local blocks, pack by pack (a2-a5) */
 static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a0, double b1, double cdt,
-                           bool reduce, int stage, int s0 = 0, int s1 = -1, bool post = true) {
+                           bool reduce, int stage, int s0 = 0, int s1 = -1, bool post = true, bool put = false) {
   const int nloc = (int)m->local_gids.size();
   if (s1 < 0) s1 = nloc;
   if (m->ho) {
@@ -1012,6 +1038,7 @@ static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a
     A.KC = m->KC;
     A.cta_base = p0 * per_blk;
     A.stage = stage;
+    if (put && m->fused_put) A.peer_rbuf = m->d_prbuf[Uout == m->U1 ? 0 : 1];
     if (m->Hpool) {
       const bool vl2 = m->cfg.integrator == PH_INT_VL2;
       A.H = m->Hpool;
@@ -1090,7 +1117,7 @@ static ph_status one_cycle(ph_mesh* m) {
     CU(cudaStreamWaitEvent(m->bstream, m->ev_a, 0));
     CU(cudaStreamWaitEvent(m->istream, m->ev_a, 0));
     m->stream = m->bstream;
-    TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, c1, false, 1, m->n_int, nloc));
+    TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, c1, false, 1, m->n_int, nloc, true, true));
     CU(cudaEventRecord(m->ev_b1, m->bstream));
     TRY(exchange_begin(m, m->U1, 1));
     m->stream = m->istream;
@@ -1099,7 +1126,7 @@ static ph_status one_cycle(ph_mesh* m) {
     m->stream = m->bstream;
     TRY(exchange_end(m, m->U1, 1));
     CU(cudaStreamWaitEvent(m->bstream, m->ev_i1, 0));
-    TRY(run_stage(m, m->U1, m->U0, a2, b2, c2, true, 2, m->n_int, nloc));
+    TRY(run_stage(m, m->U1, m->U0, a2, b2, c2, true, 2, m->n_int, nloc, true, true));
     TRY(exchange_begin(m, m->U0, 1));
     TRY(exchange_end(m, m->U0, 1));
     CU(cudaEventRecord(m->ev_b2, m->bstream));

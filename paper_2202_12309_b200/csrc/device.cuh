@@ -38,6 +38,8 @@ struct BlockMeta {
   int cslot;         // coarse staging slot, -1 if none
   int fslot[6];      // face-flux slot for faces -x,+x,-y,+y,-z,+z (coarse-fine faces), else -1
   int nb[6];         // direct halo: slot of the local same-level face neighbour, else -1 (use ghosts)
+  int prank[6];      // fused peer put: rank receiving this face's g boundary layers, else -1
+  long long poff[6]; // ... and the offset (doubles) of its [v][box] task in that rank's receive half
 };
 
 // Ghost-exchange task (fill-in-one).  One task fills one destination box.
@@ -126,6 +128,9 @@ struct StageArgs {
   // H = ha0 U^n + hb1 U^1, and stage 2 reads H instead of U^n and U^1 at the cell (null = off)
   double* H;
   double ha0, hb1;
+  // fused peer put (boundary blocks, peer transport): finished cells within g layers of a remote face
+  // are also stored into that peer's receive half (M.prank / M.poff); null = off
+  double* const* peer_rbuf;
 };
 
 struct XArgs {

@@ -314,7 +314,7 @@ __device__ __forceinline__ void face_flux(const double* p0, const double* p1, co
 }
 
 template <int RECON, bool REDUCE, bool USE_U0, bool ML, bool FULL, bool HB, int TXv = TILE_X, int TYv = TILE_Y,
-          bool EIN = false>
+          bool EIN = false, bool PUT = false>
 __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G) {
   // tile geometry (32x8, or 16x16 for 16-wide blocks), shadowing the 32x8 constants
   constexpr int TX = TXv, TY = TYv, NCELL = TX * TY, NT = NCELL;
@@ -630,6 +630,26 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
         }
         un[v] = out;
         st_cell(A.Uout + cell + v * G.vstride, out);
+      }
+      if (PUT) {
+        // fused halo put: a cell within g layers of a face whose neighbour lives on another GPU is
+        // stored, as it is finished, straight into that GPU's receive buffer over NVLink -- at the
+        // place its unpack reads: the face box (g layers x n x n), [v][cell], cell (k, j, i)-major
+        const int cc[3] = {x0 + tx, y0 + ty, c};
+#pragma unroll
+        for (int f = 0; f < 6; ++f) {
+          const int pr = M.prank[f];
+          if (pr < 0) continue;
+          const int d = f >> 1;
+          const int l = (f & 1) ? cc[d] - (G.n[d] - g) : cc[d];  // layer within the face box
+          if (l < 0 || l >= g) continue;
+          const int e0 = d == 0 ? g : G.n[0], e1 = d == 1 ? g : G.n[1], e2 = d == 2 ? g : G.n[2];
+          const int i2 = d == 0 ? l : cc[0], j2 = d == 1 ? l : cc[1], k2 = d == 2 ? l : cc[2];
+          const int64_t nbox = (int64_t)e0 * e1 * e2;
+          double* dst = A.peer_rbuf[pr] + M.poff[f] + ((int64_t)k2 * e1 + j2) * e0 + i2;
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) dst[v * nbox] = un[v];
+        }
       }
       if (REDUCE) {
         double ir = rcp_nr(un[0]);
@@ -1510,30 +1530,30 @@ __global__ void remesh_kernel(const RemeshTask* tasks, const double* Uold, doubl
 #define PH_CHECK_LAUNCH() cudaGetLastError()
 
 template <int R, bool RD, bool U0, bool ML, bool FULL, bool HB = false, int TXv = TILE_X, int TYv = TILE_Y,
-          bool EIN = false>
+          bool EIN = false, bool PUT = false>
 static cudaError_t launch_stage_t(int nblk_cta, const StageArgs& a, const Geom& G, cudaStream_t s) {
   const size_t sm = stage_smem_bytes_t<TXv, TYv>();
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv, EIN>,
+    cudaError_t e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv, EIN, PUT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     if (getenv("PH_DEBUG_ATTR")) {
       cudaFuncAttributes fa;
-      cudaFuncGetAttributes(&fa, stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv, EIN>);
+      cudaFuncGetAttributes(&fa, stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv, EIN, PUT>);
       fprintf(stderr, "stage_kernel<%d,%d,%d,%d,%d>: regs %d maxThreads %d static smem %zu local %zu dyn %zu (max dyn %d) NT %d\n",
               R, (int)RD, (int)U0, (int)ML, (int)FULL, fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
               fa.localSizeBytes, sm, fa.maxDynamicSharedSizeBytes, NT);
     }
     // shared-memory carveout hint (percent of the maximum); the rest of the 256 KB is L1
     if (const char* cv = getenv("PH_CARVEOUT")) {
-      e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv, EIN>, cudaFuncAttributePreferredSharedMemoryCarveout,
+      e = cudaFuncSetAttribute(stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv, EIN, PUT>, cudaFuncAttributePreferredSharedMemoryCarveout,
                                atoi(cv));
       if (e != cudaSuccess) return e;
     }
     attr = true;
   }
-  stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv, EIN><<<nblk_cta, TXv * TYv, sm, s>>>(a, G);
+  stage_kernel<R, RD, U0, ML, FULL, HB, TXv, TYv, EIN, PUT><<<nblk_cta, TXv * TYv, sm, s>>>(a, G);
   return cudaGetLastError();
 }
 
@@ -1543,10 +1563,17 @@ static cudaError_t launch_stage_ml(bool ml, int n, const StageArgs& a, const Geo
   int tx, ty;
   const bool full = stage_tile(G, R, ml, &tx, &ty);
   if (a.H && !full) return cudaErrorInvalidValue;  // the host enables H only where the full-tile path runs
+  if (a.peer_rbuf && !full) return cudaErrorInvalidValue;  // the host fuses the put only on full tiles
   if (full && tx == 16) {
+    if (a.peer_rbuf)
+      return a.H ? launch_stage_t<0, RD, U0, false, true, true, 16, 16, false, true>(n, a, G, s)
+                 : launch_stage_t<0, RD, U0, false, true, false, 16, 16, false, true>(n, a, G, s);
     if (a.H) return launch_stage_t<0, RD, U0, false, true, true, 16, 16>(n, a, G, s);
     return launch_stage_t<0, RD, U0, false, true, false, 16, 16>(n, a, G, s);
   }
+  if (full && a.peer_rbuf)
+    return a.H ? launch_stage_t<0, RD, U0, false, true, true, TILE_X, TILE_Y, false, true>(n, a, G, s)
+               : launch_stage_t<0, RD, U0, false, true, false, TILE_X, TILE_Y, false, true>(n, a, G, s);
   if (full && a.H) return launch_stage_t<0, RD, U0, false, true, true>(n, a, G, s);
   if (full) return launch_stage_t<0, RD, U0, false, true>(n, a, G, s);
   if (G.wavespeed)  // Einfeldt wave speeds (A4 variant)

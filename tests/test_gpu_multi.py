@@ -29,6 +29,8 @@ def _port():
 CASES = [(c, "auto") for c in ("smr2", "smr3_walls", "amr2", "wenoz")]
 # uniform meshes: both halo transports (NCCL pack/send/unpack, and peer memory read in place)
 CASES += [(c, h) for c in ("blast", "sod_walls", "wave64", "tiny") for h in ("nccl", "peer")]
+# the fused put: the boundary blocks' stage kernel stores its faces into the peers' buffers itself
+CASES += [("blast", "peer-fused"), ("sod_walls", "peer-fused")]
 
 
 @pytest.mark.parametrize("case,halo", CASES)
@@ -39,8 +41,9 @@ def test_multi_gpu_matches_oracle_and_single_gpu(case, halo, world):
     for attempt in range(4):  # the free-port probe can race with another rendezvous: retry
         cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
                "--master-addr", "127.0.0.1", "--master-port", str(_port()),
-               os.path.join(ROOT, "tools", "multi_check.py"), "--case", case, "--halo", halo]
-        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+               os.path.join(ROOT, "tools", "multi_check.py"), "--case", case, "--halo", halo.split("-")[0]]
+        env = dict(os.environ, PH_FUSED_PUT="1") if halo.endswith("-fused") else None
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
         if "EADDRINUSE" not in r.stderr:
             break
     line = [l for l in r.stdout.splitlines() if l.startswith("MULTI_CHECK")]
