@@ -1576,6 +1576,10 @@ static cudaError_t launch_stage_ml(bool ml, int n, const StageArgs& a, const Geo
                : launch_stage_t<0, RD, U0, false, true, false, TILE_X, TILE_Y, false, true>(n, a, G, s);
   if (full && a.H) return launch_stage_t<0, RD, U0, false, true, true>(n, a, G, s);
   if (full) return launch_stage_t<0, RD, U0, false, true>(n, a, G, s);
+  // multilevel meshes whose blocks tile exactly: the bounds-check-free variant (no boundary-face
+  // precompute and no H there: coarse-fine faces store fluxes for the reflux)
+  if (ml && R == 0 && !G.wavespeed && G.n[0] % TILE_X == 0 && G.n[1] % TILE_Y == 0 && !getenv("PH_NO_ML_FULL"))
+    return launch_stage_t<0, RD, U0, true, true>(n, a, G, s);
   if (G.wavespeed)  // Einfeldt wave speeds (A4 variant)
     return ml ? launch_stage_t<R, RD, U0, true, false, false, TILE_X, TILE_Y, true>(n, a, G, s)
               : launch_stage_t<R, RD, U0, false, false, false, TILE_X, TILE_Y, true>(n, a, G, s);
