@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
   double* sFz = sFy + NVAR * FYS;          // [2][5][TY][TX]
   double* exF = sFz + 2 * NVAR * FZS;      // [EXTRA_AHEAD][5][TY + TX]: later planes' x faces fi = 0, y faces jf = 0
   constexpr int EXS = NVAR * (TX + TY);
-  constexpr bool PRE = FULL && !ML;        // boundary-face precompute on the regular full-tile path
+  constexpr bool PRE = FULL;               // boundary-face precompute on the regular full-tile path
 
   const int tid = threadIdx.x;
   const int tx = tid % TX, ty = tid / TX;
@@ -470,6 +470,27 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
     // x faces of plane c: 33 per row, item t -> (row t/33, face t%33); rounds 0,1 (warp 0 only)
     const int phase = (c - k0) % (EXTRA_AHEAD + 1);  // 0: full plane; else boundary faces precomputed
     const bool reduced = PRE && phase != 0;
+    // multilevel: x / y face fluxes on a coarse-fine block face also go to the face-flux slots (a8)
+    auto ml_x = [&](int pl, int fi, int j, const double* F) {
+      const int gi = x0 + fi;
+      const int fs = (gi == 0) ? M.fslot[0] : ((gi == G.n[0]) ? M.fslot[1] : -1);
+      if (fs >= 0) {
+        const int64_t fstr = (int64_t)G.n[1] * G.n[2];
+        double* o = A.fbuf + (int64_t)fs * G.fstride + (int64_t)pl * G.n[1] + (y0 + j);
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) o[v * fstr] = F[v];
+      }
+    };
+    auto ml_y = [&](int pl, int jf, int i, const double* F) {
+      const int gj = y0 + jf;
+      const int fs = (gj == 0) ? M.fslot[2] : ((gj == G.n[1]) ? M.fslot[3] : -1);
+      if (fs >= 0) {
+        const int64_t fstr = (int64_t)G.n[0] * G.n[2];
+        double* o = A.fbuf + (int64_t)fs * G.fstride + (int64_t)pl * G.n[0] + (x0 + i);
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) o[v * fstr] = F[v];
+      }
+    };
     if (xy && reduced) {
       // interior faces only: x faces 1..TX of every row, y face rows 1..TY, one round each
 #pragma unroll 1
@@ -480,6 +501,7 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
         face_flux<RECON, 1, 2, 3, VS, EIN>(p, p + 1, p + 2, p + 3, G, F);
         double* d = sFx + j * (TX + 1) + fi;
         d[0] = F[0]; d[FXS] = F[1]; d[2 * FXS] = F[2]; d[3 * FXS] = F[3]; d[4 * FXS] = F[4];
+        if (ML) ml_x(c, fi, j, F);
       }
 #pragma unroll 1
       for (int t = tid; t < TX * TY; t += NT) {
@@ -489,6 +511,7 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
         face_flux<RECON, 2, 3, 1, VS, EIN>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
         double* d = sFy + jf * TX + i;
         d[0] = F[0]; d[FYS] = F[1]; d[2 * FYS] = F[2]; d[3 * FYS] = F[3]; d[4 * FYS] = F[4];
+        if (ML) ml_y(c, jf, i, F);
       }
       const double* ex = exF + (phase - 1) * EXS;
       for (int t = tid; t < NVAR * (TX + TY); t += NT) {  // the precomputed boundary faces
@@ -510,12 +533,14 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
             face_flux<RECON, 1, 2, 3, VS, EIN>(p, p + 1, p + 2, p + 3, G, F);
 #pragma unroll
             for (int v = 0; v < NVAR; ++v) ex[v * (TX + TY) + lane] = F[v];
+            if (ML) ml_x(c + a, 0, lane, F);
           } else if ((warp_id == 2 || warp_id == 5) && lane < TX) {
             const double* p = Wn + (lane + 2);
             double F[NVAR];
             face_flux<RECON, 2, 3, 1, VS, EIN>(p, p + SWX, p + 2 * SWX, p + 3 * SWX, G, F);
 #pragma unroll
             for (int v = 0; v < NVAR; ++v) ex[v * (TX + TY) + TY + lane] = F[v];
+            if (ML) ml_y(c + a, 0, lane, F);
           }
         }
       }
