@@ -278,7 +278,7 @@ def run_ours(args):
     # committed ncu capture of this kernel; peak = 148 SMs x 64 fp64 lanes/clk x 1965 MHz (B200 unit
     # counts and max clock).
     fp64 = None
-    pp = os.path.join(ROOT, "profiles", "r01_stage_2b_v10.json")
+    pp = os.path.join(ROOT, "profiles", "r01_stage_2b_v11.json")
     if os.path.exists(pp) and stage_n:
         try:
             per_cell = float(json.load(open(pp))["fp64_inst_per_cell"])
@@ -286,7 +286,7 @@ def run_ours(args):
             fpk = 148 * 64 * 1965e6
             fp64 = {"bound": "alu", "achieved": ach, "peak": fpk, "unit": "fp64-pipe thread instr/s",
                     "frac": ach / fpk, "inst_per_cell_stage": per_cell,
-                    "source": "inst count: ncu profiles/r01_stage_2b_v10.json; peak: 148 SM x 64 lanes x 1.965 GHz"}
+                    "source": "inst count: ncu profiles/r01_stage_2b_v11.json; peak: 148 SM x 64 lanes x 1.965 GHz"}
         except Exception:
             fp64 = None
     line = {
