@@ -253,7 +253,9 @@ def run_ours(args):
     nloc_cells = nloc * n ** 3
     # algorithmic bytes per stage launch: read U with halo (r*40 B/cell), write 40 B/cell,
     # stage 2 also reads U^n at the cell (40 B/cell): averaged over the two stages
-    stage_bytes = nloc_cells * (r * 40.0 + 60.0)
+    # per launch: the timed cycles' total algorithmic bytes over the stage launches (N > 1 splits each
+    # stage into a boundary and an interior launch; N = 1: one launch of all local blocks)
+    stage_bytes = nloc_cells * (r * 40.0 + 60.0) * 2 * args.steps / max(stage_n, 1)
     stage_avg_ms = stage_ms / max(stage_n, 1)
     achieved = stage_bytes / (stage_avg_ms * 1e-3) / 1e9 if stage_n else None
     traffic = None
