@@ -284,7 +284,7 @@ def run_ours(args):
     if os.path.exists(pp) and stage_n:
         try:
             per_cell = float(json.load(open(pp))["fp64_inst_per_cell"])
-            ach = per_cell * nloc_cells / (stage_avg_ms * 1e-3)
+            ach = per_cell * nloc_cells * 2 * args.steps / (stage_ms * 1e-3)  # all timed stage launches
             fpk = 148 * 64 * 1965e6
             fp64 = {"bound": "alu", "achieved": ach, "peak": fpk, "unit": "fp64-pipe thread instr/s",
                     "frac": ach / fpk, "inst_per_cell_stage": per_cell,
