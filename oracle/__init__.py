@@ -9,9 +9,9 @@ is built from ``oracle/oracle.cpp`` alone (plain scalar C++, ``-O2
 
 Parity status per function ("Oracle pins"):
   cons<->prim, PLM, HLLE (Davis and Einfeldt), restriction, prolongation, Morton, partition, tree/2:1,
-  neighbours, exchange, flux correction, dt, totals, RK2  -> pinned (tests/test_oracle_*.py)
+  neighbours, exchange, flux correction, dt, totals, RK2, VL2  -> pinned (tests/test_oracle_*.py)
   AMR refinement criterion (A14), derefinement gate (A16), staging geometry (A12),
-  VL2, van Leer / MC limiters                              -> parity unpinned by the paper
+  van Leer / MC limiters                                   -> parity unpinned by the paper
 """
 from __future__ import annotations
 

@@ -167,6 +167,33 @@ def test_linear_wave_oblique_3d_second_order(oracle_mod):
     assert r[0] >= 2.1 and r[1] >= 2.4 and r[1] > r[0], (e, r)
 
 
+def test_linear_wave_vl2_second_order_and_close_to_rk2(oracle_mod):
+    """VL2 (NEXT 2): second order in space and time on the aligned wave; with the same PLM in both
+    stages its error is within a few percent of RK2's (the SURVEY prototype: 0.5 %)"""
+    def l1(N, integ):
+        m = oracle_mod.Mesh(mesh_nx=(N, 4, 4), block_nx=(N // 2, 4, 4), integrator=integ)
+        m.set_problem(oracle_mod.LINEAR_WAVE, [1e-6, 1, 0, 0])
+        m.step(100000, 1.0)
+        x = (np.arange(N) + 0.5) / N
+        rho = np.concatenate([m.get_state(b)[0, 0, 0] for b in range(2)])
+        return np.abs(rho - (1 + 1e-6 * np.sin(2 * np.pi * x))).mean()
+    e = [l1(N, oracle_mod.VL2) for N in (32, 64, 128)]
+    assert e[0] / e[1] >= 2.9 and e[1] / e[2] >= 3.3, e
+    r = l1(128, oracle_mod.RK2)
+    assert abs(e[2] - r) <= 0.05 * r, (e[2], r)
+
+
+def test_vl2_conserves_to_roundoff(oracle_mod):
+    m = oracle_mod.Mesh(mesh_nx=(32, 32, 32), block_nx=(16, 16, 16), xmin=(-.5,) * 3, xmax=(.5,) * 3,
+                        integrator=oracle_mod.VL2)
+    m.set_problem(oracle_mod.BLAST, [10.0, 0.1, 0.15])
+    t0 = m.totals()
+    m.step(30)
+    t1 = m.totals()
+    assert abs(t1[0] - t0[0]) <= 1e-13 * t0[0] and abs(t1[4] - t0[4]) <= 1e-13 * t0[4]
+    assert np.all(np.abs(t1[1:4] - t0[1:4]) <= 1e-13 * t0[4])
+
+
 def test_linear_wave_vanleer_converges_faster(oracle_mod):
     e = [_wave_l1(oracle_mod, N, (1, 0, 0), True, recon=oracle_mod.VANLEER) for N in (32, 64, 128)]
     assert e[1] / e[2] >= 3.6, e
@@ -202,11 +229,13 @@ def test_tlim_caps_last_step(oracle_mod):
     assert h[-1, 1] <= h[-2, 1]
 
 
-def test_stage_two_is_heun_on_a_linear_problem(oracle_mod):
-    """RK2 (A1) on a linear advection-like small-amplitude wave: halving dt at fixed mesh cuts
-    the time error by ~4 (second order in time), which forward Euler twice would not."""
+@pytest.mark.parametrize("integ", [0, 1])
+def test_stage_two_is_second_order_in_time(oracle_mod, integ):
+    """RK2 (Heun, A1) and VL2 (midpoint predictor-corrector, NEXT 2) on a small-amplitude wave:
+    halving dt at a fixed mesh cuts the time error by ~4 (second order in time); a first-order
+    integrator (forward Euler, or VL2 with a wrong predictor weight) would give ~2."""
     def run(cfl):
-        m = oracle_mod.Mesh(mesh_nx=(32, 4, 4), block_nx=(16, 4, 4), cfl=cfl)
+        m = oracle_mod.Mesh(mesh_nx=(32, 4, 4), block_nx=(16, 4, 4), cfl=cfl, integrator=integ)
         m.set_problem(oracle_mod.LINEAR_WAVE, [1e-6, 1, 0, 0])
         m.step(100000, 0.25)
         return np.concatenate([m.get_state(b)[0, 0, 0] for b in range(2)])
