@@ -11,7 +11,7 @@ Parity status per function ("Oracle pins"):
   cons<->prim, PLM, HLLE (Davis and Einfeldt), restriction, prolongation, Morton, partition, tree/2:1,
   neighbours, exchange, flux correction, dt, totals, RK2, VL2  -> pinned (tests/test_oracle_*.py)
   AMR refinement criterion (A14), derefinement gate (A16), staging geometry (A12),
-  van Leer / MC limiters                                   -> parity unpinned by the paper
+  (van Leer / MC: closed forms + convergence pins)        -> parity unpinned by the paper
 """
 from __future__ import annotations
 

@@ -199,6 +199,14 @@ def test_linear_wave_vanleer_converges_faster(oracle_mod):
     assert e[1] / e[2] >= 3.6, e
 
 
+def test_linear_wave_mc_second_order_and_below_minmod(oracle_mod):
+    """MC (the least clipping of the three limiters) is second order and, on a smooth wave, more
+    accurate than minmod at every resolution"""
+    e = [_wave_l1(oracle_mod, N, (1, 0, 0), True, recon=oracle_mod.MC) for N in (32, 64, 128)]
+    m = [_wave_l1(oracle_mod, N, (1, 0, 0), True) for N in (32, 64, 128)]
+    assert e[1] / e[2] >= 3.3 and all(a < b for a, b in zip(e, m)), (e, m)
+
+
 # ---------------------------------------------------------------- dt (O6) and totals (O10)
 def test_dt_worked_example(oracle_mod):
     ex = json.load(open(os.path.join(GOLD, "spec_examples.json")))["dt"]     # S:780
