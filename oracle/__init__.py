@@ -8,10 +8,11 @@ is built from ``oracle/oracle.cpp`` alone (plain scalar C++, ``-O2
 -ffp-contract=off``).
 
 Parity status per function ("Oracle pins"):
-  cons<->prim, PLM, HLLE (Davis and Einfeldt), restriction, prolongation, Morton, partition, tree/2:1,
-  neighbours, exchange, flux correction, dt, totals, RK2, VL2  -> pinned (tests/test_oracle_*.py)
-  AMR refinement criterion (A14), derefinement gate (A16), staging geometry (A12),
-  (van Leer / MC: closed forms + convergence pins)        -> parity unpinned by the paper
+  cons<->prim, PLM (minmod, van Leer, MC), HLLE (Davis and Einfeldt), restriction, prolongation,
+  Morton, partition, tree/2:1, neighbours, exchange, flux correction, dt, totals, RK2, VL2
+                                                           -> pinned (tests/test_oracle_*.py)
+  AMR refinement criterion (A14), derefinement gate (A16), staging geometry (A12)
+                                                           -> parity unpinned by the paper
 """
 from __future__ import annotations
 
