@@ -11,8 +11,8 @@ Parity status per function ("Oracle pins"):
   cons<->prim, PLM (minmod, van Leer, MC), HLLE (Davis and Einfeldt), restriction, prolongation,
   Morton, partition, tree/2:1, neighbours, exchange, flux correction, dt, totals, RK2, VL2
                                                            -> pinned (tests/test_oracle_*.py)
-  AMR refinement criterion (A14), derefinement gate (A16), staging geometry (A12)
-                                                           -> parity unpinned by the paper
+  AMR refinement criterion (A14: closed form on a linear pressure)  -> pinned
+  derefinement gate (A16), staging geometry (A12)          -> parity unpinned by the paper
 """
 from __future__ import annotations
 

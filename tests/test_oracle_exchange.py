@@ -205,3 +205,36 @@ def test_derefinement_gate(oracle_mod):
         S = m.get_state(b)
         for v in range(5):
             assert np.all(S[v] == U[v])
+
+
+@pytest.mark.parametrize("axis", [0, 1])
+def test_refinement_indicator_closed_form_on_a_linear_pressure(oracle_mod, axis):
+    """A14: eps_B = max over the block of |grad p| / p with central differences (half the difference of
+    the two neighbours, no dx).  On p = p0 + delta * i_global (rho = 1, v = 0) the difference is exact,
+    so block b's indicator is delta / p at its first cell with two interior-or-neighbour sides -- the
+    domain-boundary cell (outflow ghost = edge value) sees only delta / 2.  A dropped 1/2, a missing
+    component or dividing by the wrong pressure fails this."""
+    g, p0, d = 1.4, 1.0, 0.01
+    shape = [8, 8, 8]
+    shape[axis] = 24
+    bc = [0, 0, 0]
+    bc[axis] = oracle_mod.OUTFLOW
+    m = oracle_mod.Mesh(mesh_nx=tuple(shape), block_nx=(8, 8, 8), max_level=1, refinement=oracle_mod.REF_ADAPTIVE,
+                        refine_tol=1e9, derefine_tol=0.0, gamma=g, bc_inner=tuple(bc), bc_outer=tuple(bc))
+    for b in m.blocks():
+        lo = b["lx"][axis] * 8
+        i = np.arange(8) + lo
+        p = p0 + d * i
+        U = np.zeros((5, 8, 8, 8))
+        U[0] = 1.0
+        shp = [1, 1, 1]
+        shp[2 - axis] = 8
+        U[4] = (p / (g - 1)).reshape(shp)
+        m.set_state(b["gid"], U)
+    m.exchange()
+    m.tag_and_remesh()
+    eps = m.indicators()
+    first = {0: 1, 1: 8, 2: 16}  # first cell (global index) with a full central difference per block
+    for b in m.blocks():
+        want = d / (p0 + d * first[b["lx"][axis]])
+        assert abs(eps[b["gid"]] - want) <= 1e-13 * want, (b, eps[b["gid"]], want)
