@@ -195,6 +195,13 @@ ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info /
  * Times the full path incl. host<->device copies (bench e2e leg). */
 ph_status ph_step_host(ph_mesh* m, const double* host_in, double* host_out, int64_t nelem,
                        int32_t ncycles, double tlim);
+/* The same, enqueued on cfg->stream without waiting (host buffers must be pinned and stay valid until
+ * ph_sync; AMR meshes still synchronise inside their tag passes).  Two meshes on two streams can
+ * overlap one problem's device->host copy with the next one's host->device copy. */
+ph_status ph_step_host_async(ph_mesh* m, const double* host_in, double* host_out, int64_t nelem,
+                             int32_t ncycles, double tlim);
+/* Wait for everything enqueued on the mesh's stream; reports latched device errors (PH_ERR_PHYSICS). */
+ph_status ph_sync(ph_mesh* m);
 
 /* ---- queries ------------------------------------------------------------------------------ */
 ph_status ph_num_blocks(const ph_mesh* m, int64_t* nglobal, int64_t* nlocal);

@@ -1827,6 +1827,17 @@ ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) 
 
 ph_status ph_step_host(ph_mesh* m, const double* host_in, double* host_out, int64_t nelem, int32_t ncycles,
                        double tlim) {
+  TRY(ph_step_host_async(m, host_in, host_out, nelem, ncycles, tlim));
+  return check_err(m);
+}
+
+ph_status ph_sync(ph_mesh* m) {
+  TRY(need_device(m));
+  return check_err(m);
+}
+
+ph_status ph_step_host_async(ph_mesh* m, const double* host_in, double* host_out, int64_t nelem, int32_t ncycles,
+                             double tlim) {
   TRY(need_device(m));
   const Geom& G = m->G;
   int64_t nloc = (int64_t)m->local_gids.size();
@@ -1846,7 +1857,7 @@ ph_status ph_step_host(ph_mesh* m, const double* host_in, double* host_out, int6
     m->launches++;
   }
   if (ni) CU(cudaMemcpyAsync(host_out, m->stage_buf, ni * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
-  return check_err(m);
+  return PH_OK;
 }
 
 ph_status ph_num_blocks(const ph_mesh* m, int64_t* nglobal, int64_t* nlocal) {

@@ -74,7 +74,7 @@ EXPORTS = ["ph_nccl_unique_id", "ph_mesh_create", "ph_mesh_destroy", "ph_set_pro
            "ph_refresh", "ph_get_state", "ph_get_state_full", "ph_set_state_full", "ph_exchange", "ph_step",
            "ph_step_host", "ph_num_blocks", "ph_get_blocks", "ph_get_neighbors", "ph_get_refine_flags",
            "ph_get_history", "ph_get_time", "ph_totals", "ph_get_plan_info", "ph_launch_count",
-           "ph_kernel_timing", "ph_last_error"]
+           "ph_kernel_timing", "ph_last_error", "ph_step_host_async", "ph_sync"]
 
 _lib = None
 _LIVE = __import__("weakref").WeakSet()
@@ -112,6 +112,8 @@ def lib():
         L.ph_exchange.argtypes = [vp]
         L.ph_step.argtypes = [vp, C.c_int32, C.c_double, C.POINTER(PhStepInfo)]
         L.ph_step_host.argtypes = [vp, vp, vp, C.c_int64, C.c_int32, C.c_double]
+        L.ph_step_host_async.argtypes = [vp, vp, vp, C.c_int64, C.c_int32, C.c_double]
+        L.ph_sync.argtypes = [vp]
         L.ph_num_blocks.argtypes = [vp, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         L.ph_get_blocks.argtypes = [vp, C.POINTER(PhBlock), C.c_int64, C.POINTER(C.c_int64)]
         L.ph_get_neighbors.argtypes = [vp, C.c_int64, C.POINTER(PhNeighbor), C.c_int32, C.POINTER(C.c_int32)]
@@ -312,6 +314,17 @@ class Mesh:
             return x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data
         n = host_in.numel() if hasattr(host_in, "numel") else host_in.size
         _check(lib().ph_step_host(self._h, C.c_void_p(ptr(host_in)), C.c_void_p(ptr(host_out)), n, ncycles, tlim))
+
+    def step_host_async(self, host_in, host_out, ncycles, tlim=0.0):
+        """Enqueue step_host on the mesh's stream and return (pinned buffers; call sync())."""
+        def ptr(x):
+            return x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data
+        n = host_in.numel() if hasattr(host_in, "numel") else host_in.size
+        _check(lib().ph_step_host_async(self._h, C.c_void_p(ptr(host_in)), C.c_void_p(ptr(host_out)), n, ncycles,
+                                        tlim))
+
+    def sync(self):
+        _check(lib().ph_sync(self._h))
 
     def time(self):
         t, dt, cyc = C.c_double(), C.c_double(), C.c_int64()

@@ -196,6 +196,18 @@ def test_step_host_matches_step(P):
     h.step_host(hin, hout, 3)
     torch.cuda.synchronize()
     assert np.array_equal(hout.numpy(), ref)
+    # asynchronous problems alternating over two meshes on two streams give the same answers
+    a, b = P.Mesh(**kw), P.Mesh(stream=torch.cuda.Stream(), **kw)
+    outs = [torch.empty_like(hin).pin_memory() for _ in range(4)]
+    for s in range(4):
+        M = (a, b)[s % 2]
+        if s >= 2:
+            M.sync()
+        M.step_host_async(hin, outs[s], 3)
+    a.sync()
+    b.sync()
+    for o in outs:
+        assert np.array_equal(o.numpy(), ref)
 
 
 def test_negative_pressure_is_reported(P):
