@@ -356,7 +356,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=2)
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: W >= 3 warm-up steps required by the timing rules; using 3", file=sys.stderr)
