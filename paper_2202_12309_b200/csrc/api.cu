@@ -1,5 +1,7 @@
 // api.cu -- C ABI (include/ph.h): mesh/plan construction, device block pool, the per-cycle
-// schedule (O5) and NCCL plumbing.  Hot work runs in kernels.cu.
+// schedule (O5: one CUDA graph per cycle; boundary-first two-stream cycle on several GPUs), the halo
+// transports (peer-memory puts over CUDA IPC, or NCCL), AMR remesh and migration.  Hot work runs in
+// kernels.cu.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
