@@ -1366,7 +1366,7 @@ __device__ __forceinline__ double pressure_rn(const double* u, int64_t vs, doubl
 // columns marching up the block; the pressure of every cell is computed once into a 3-plane smem
 // ring with a plus-shaped halo of 1 (x/y neighbours) -- the z neighbours come from the ring.
 constexpr int TGX = 32, TGY = 8, TGT = TGX * TGY, TGW = TGX + 2, TGP = (TGY + 2) * TGW;
-__global__ void __launch_bounds__(TGT) tag_kernel(const double* U, const BlockMeta* meta, unsigned long long* eps_bits,
+__global__ void __launch_bounds__(TGT, 4) tag_kernel(const double* U, const BlockMeta* meta, unsigned long long* eps_bits,
                                                   double* partials, ErrWord* err, Geom G) {
   __shared__ double sp[3][TGP];
   __shared__ double red[TGT / 32][6];
