@@ -117,6 +117,8 @@ struct ph_mesh {
   int64_t graph_launches = 0;  // a direct-halo cycle ran since the last full exchange
   bool direct_halo = false;  // uniform mesh: stage kernels read local same-level face neighbours directly
   std::vector<RefluxTask> reflux[3];
+  std::vector<int2> rfx_faces;  // (slot, face) pairs receiving flux correction (static multilevel dt)
+  int2* d_rfx_faces = nullptr;
   RefluxTask* d_reflux[3] = {nullptr, nullptr, nullptr};
   // cross-rank flux correction: fine-side packs and per-peer layout
   std::vector<FluxPackTask> fpack;
@@ -583,6 +585,7 @@ static ph_status build_plan(ph_mesh* m) {
       M.prank[f] = -1;
       M.poff[f] = 0;
     }
+    M.rfx = 0;
     if (m->direct_halo && !b.has_coarser) {
       for (auto& e : b.nbrs) {
         int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
@@ -592,6 +595,13 @@ static ph_status build_plan(ph_mesh* m) {
       }
     }
   }
+  // faces receiving flux correction (coarse side): their first cell layer is reduced after the reflux
+  m->rfx_faces.clear();
+  for (int d = 0; d < 3; ++d)
+    for (const RefluxTask& rt : m->reflux[d]) m->meta[rt.cslot].rfx |= 1 << (2 * rt.dir + (rt.side > 0 ? 1 : 0));
+  for (int64_t s = 0; s < nloc; ++s)
+    for (int f = 0; f < 6; ++f)
+      if ((m->meta[s].rfx >> f) & 1) m->rfx_faces.push_back(make_int2((int)s, f));
   // stage launch order: with the multi-GPU direct halo, blocks that have no remote or physical
   // face come first so their stage can run while the halo exchange is in flight
   m->overlap = m->direct_halo && m->nranks > 1 && !m->multilevel && m->cfg.refinement != PH_REF_ADAPTIVE;
@@ -671,7 +681,9 @@ static ph_status setup_device(ph_mesh* m) {
   m->Hpool = nullptr;
   if (!m->ho && !m->multilevel && m->cfg.refinement != PH_REF_ADAPTIVE && full_tile && !getenv("PH_NO_HBASE"))
     TRY(dalloc(m, (void**)&m->Hpool, (size_t)std::max<int64_t>(nloc, 1) * G.bstride * sizeof(double)));
-  m->partials_n = std::max<int64_t>({(int64_t)m->stage_ctas, nloc * G.n[2], nloc * tag_ctas_per_block(G), 1});
+  m->partials_n = std::max<int64_t>({(int64_t)m->stage_ctas + (int64_t)m->rfx_faces.size(), nloc * G.n[2],
+                                      nloc * tag_ctas_per_block(G), 1});
+  TRY(upload(m, &m->d_rfx_faces, m->rfx_faces));
   TRY(dalloc(m, (void**)&m->partials, m->partials_n * 6 * sizeof(double)));
   CU(cudaMemsetAsync(m->partials, 0, m->partials_n * 6 * sizeof(double), m->stream));
   {
@@ -1142,14 +1154,23 @@ static ph_status one_cycle(ph_mesh* m) {
     TRY(reduce_finalize(m, nloc > 0 ? m->stage_ctas : 0, 1));
     return PH_OK;
   }
+  // static multilevel: stage 2 reduces dt / totals of all cells but the flux-corrected layers, which
+  // are reduced after the reflux (no standalone pass over the whole pool)
+  const bool ml_fuse = m->multilevel && !adaptive && !m->ho && !getenv("PH_NO_ML_FUSE");
+  const bool red2 = fuse_reduce || ml_fuse;
   if (m->cfg.integrator == PH_INT_VL2) {
     TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, 0.5, false, 1));
     TRY(exchange(m, m->U1, 1));
-    TRY(run_stage(m, m->U1, m->U0, 1.0, 0.0, 1.0, fuse_reduce, 2));
+    TRY(run_stage(m, m->U1, m->U0, 1.0, 0.0, 1.0, red2, 2));
   } else {
     TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, 1.0, false, 1));
     TRY(exchange(m, m->U1, 1));
-    TRY(run_stage(m, m->U1, m->U0, 0.5, 0.5, 0.5, fuse_reduce, 2));
+    TRY(run_stage(m, m->U1, m->U0, 0.5, 0.5, 0.5, red2, 2));
+  }
+  if (ml_fuse && !m->rfx_faces.empty()) {
+    CU(launch_rfx_reduce(m->d_rfx_faces, (int)m->rfx_faces.size(), m->U0, m->d_meta,
+                         m->partials + (int64_t)m->stage_ctas * 6, m->d_err, m->G, m->stream));
+    m->launches++;
   }
   TRY(exchange(m, m->U0, 1));
   bool tag_partials = false;  // the tag pass also reduced dt / totals of the unchanged mesh
@@ -1163,6 +1184,7 @@ static ph_status one_cycle(ph_mesh* m) {
     tag_partials = !changed;
   }
   if (fuse_reduce) TRY(reduce_finalize(m, nloc > 0 ? m->stage_ctas : 0, 1));
+  else if (ml_fuse) TRY(reduce_finalize(m, (nloc > 0 ? m->stage_ctas : 0) + (int)m->rfx_faces.size(), 1));
   else if (tag_partials) TRY(reduce_finalize(m, nloc * tag_ctas_per_block(m->G), 1));
   else TRY(standalone_reduce(m, m->U0, 1));
   return PH_OK;

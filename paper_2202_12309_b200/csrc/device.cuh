@@ -40,6 +40,7 @@ struct BlockMeta {
   int nb[6];         // direct halo: slot of the local same-level face neighbour, else -1 (use ghosts)
   int prank[6];      // fused peer put: rank receiving this face's g boundary layers, else -1
   long long poff[6]; // ... and the offset (doubles) of its [v][box] task in that rank's receive half
+  int rfx;           // bit f: face f receives flux correction (this block is the coarse side)
 };
 
 // Ghost-exchange task (fill-in-one).  One task fills one destination box.
@@ -189,6 +190,10 @@ cudaError_t launch_interior_copy(double* U, double* buf, int slot0, int nslots, 
                                  cudaStream_t s);
 // AMR indicator per block; with partials != null also the dt / totals partials of U (one row of 6
 // per CTA, tag_ctas_per_block(G) CTAs per block, same layout as reduce_kernel)
+// dt / totals partials of the cells in the corrected face layers (after the reflux), one row per
+// (block slot, face) pair; edge / corner cells counted once (by their lowest corrected face)
+cudaError_t launch_rfx_reduce(const int2* faces, int nfaces, const double* U, const BlockMeta* meta, double* partials,
+                              ErrWord* err, const Geom& G, cudaStream_t s);
 cudaError_t launch_tag(const double* U, const BlockMeta* meta, int nslots, unsigned long long* eps_bits,
                        double* partials, ErrWord* err, const Geom& G, cudaStream_t s);
 int tag_ctas_per_block(const Geom& G);

@@ -676,7 +676,16 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
           for (int v = 0; v < NVAR; ++v) dst[v * nbox] = un[v];
         }
       }
-      if (REDUCE) {
+      // multilevel: the cells of a flux-corrected face layer change after this kernel (reflux); they
+      // are reduced after it (rfx_reduce_kernel)
+      bool corrected = false;
+      if (ML && REDUCE && M.rfx) {
+        const int cc[3] = {x0 + tx, y0 + ty, c};
+#pragma unroll
+        for (int f = 0; f < 6; ++f)
+          if (((M.rfx >> f) & 1) && cc[f >> 1] == ((f & 1) ? G.n[f >> 1] - 1 : 0)) corrected = true;
+      }
+      if (REDUCE && !corrected) {
         double ir = rcp_nr(un[0]);
         double v1 = un[1] * ir, v2 = un[2] * ir, v3 = un[3] * ir;
         double ke = 0.5 * ((un[1] * v1 + un[2] * v2) + un[3] * v3);
@@ -1359,6 +1368,73 @@ __device__ __forceinline__ double pressure_rn(const double* u, int64_t vs, doubl
   double v1 = __dmul_rn(m1, ir), v2 = __dmul_rn(m2, ir), v3 = __dmul_rn(m3, ir);
   double ke = __dmul_rn(0.5, __dadd_rn(__dadd_rn(__dmul_rn(m1, v1), __dmul_rn(m2, v2)), __dmul_rn(m3, v3)));
   return __dmul_rn(gm1, __dsub_rn(u[4 * vs], ke));
+}
+
+// dt / totals of the flux-corrected face layers of coarse blocks (static multilevel meshes), run after
+// the reflux: one CTA per (slot, face) pair; a cell on several corrected layers is counted by its
+// lowest corrected face only.  Fast-path arithmetic of the stage kernel's reduction.
+__global__ void __launch_bounds__(256) rfx_reduce_kernel(const int2* faces, const double* U, const BlockMeta* meta,
+                                                         double* partials, ErrWord* err, Geom G) {
+  const int2 sf = faces[blockIdx.x];
+  const int slot = sf.x, f = sf.y, d = f >> 1;
+  const BlockMeta& M = meta[slot];
+  const int ta = (d == 0) ? 1 : 0, tb = (d == 2) ? 1 : 2;
+  const int na = G.n[ta], nb = G.n[tb];
+  double tmax = 0.0, ts[NVAR] = {0, 0, 0, 0, 0};
+  for (int t = threadIdx.x; t < na * nb; t += blockDim.x) {
+    int cc[3];
+    cc[d] = (f & 1) ? G.n[d] - 1 : 0;
+    cc[ta] = t % na;
+    cc[tb] = t / na;
+    bool dup = false;
+    for (int e = 0; e < f; ++e)
+      if (((M.rfx >> e) & 1) && cc[e >> 1] == ((e & 1) ? G.n[e >> 1] - 1 : 0)) dup = true;
+    if (dup) continue;
+    const double* u = U + (int64_t)slot * G.bstride + ((int64_t)(cc[2] + G.g) * G.N[1] + (cc[1] + G.g)) * G.N[0] +
+                      (cc[0] + G.g);
+    double un[NVAR];
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) un[v] = u[v * G.vstride];
+    const double ir = rcp_nr(un[0]);
+    const double v1 = un[1] * ir, v2 = un[2] * ir, v3 = un[3] * ir;
+    const double ke = 0.5 * ((un[1] * v1 + un[2] * v2) + un[3] * v3);
+    const double p = G.gm1 * (un[4] - ke);
+    if (!(un[0] > 0.0) || !(p > 0.0)) set_error(err, 0, M.gid, cc[2], cc[1], cc[0]);
+    const double cs = sound_speed(un[0], p, G.gamma);
+    const double s1 = (fabs(v1) + cs) * M.idx[0], s2 = (fabs(v2) + cs) * M.idx[1], s3 = (fabs(v3) + cs) * M.idx[2];
+    tmax = dmax(tmax, dmax(s1, dmax(s2, s3)));
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) ts[v] += un[v];
+  }
+  __shared__ double red[8][6];
+  for (int off = 16; off > 0; off >>= 1) {
+    tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) ts[v] += __shfl_xor_sync(0xffffffffu, ts[v], off);
+  }
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (lane == 0) {
+    red[warp][0] = tmax;
+    for (int v = 0; v < NVAR; ++v) red[warp][1 + v] = ts[v];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0, s[NVAR] = {0, 0, 0, 0, 0};
+    for (int w = 0; w < 8; ++w) {
+      m = fmax(m, red[w][0]);
+      for (int v = 0; v < NVAR; ++v) s[v] += red[w][1 + v];
+    }
+    double* o = partials + (int64_t)blockIdx.x * 6;
+    o[0] = m;
+    for (int v = 0; v < NVAR; ++v) o[1 + v] = s[v] * M.dV;
+  }
+}
+
+cudaError_t launch_rfx_reduce(const int2* faces, int nfaces, const double* U, const BlockMeta* meta, double* partials,
+                              ErrWord* err, const Geom& G, cudaStream_t s) {
+  if (nfaces <= 0) return cudaSuccess;
+  rfx_reduce_kernel<<<nfaces, 256, 0, s>>>(faces, U, meta, partials, err, G);
+  return cudaGetLastError();
 }
 
 // AMR indicator (O9, A14): eps_B = max over the block of |grad p| / p with central differences, in
