@@ -70,8 +70,8 @@ typedef enum { PH_INT_RK2 = 0, PH_INT_VL2 = 1 } ph_integrator;                  
 typedef enum { PH_WS_DAVIS = 0, PH_WS_EINFELDT = 1 } ph_wavespeed;
 typedef enum { PH_PROB_LINEAR_WAVE = 0, PH_PROB_SOD = 1, PH_PROB_BLAST = 2, PH_PROB_KH = 3 } ph_problem; /* P:699-702 */
 typedef enum { PH_REF_NONE = 0, PH_REF_STATIC = 1, PH_REF_ADAPTIVE = 2 } ph_refinement;
-/* How the per-cycle halo of a uniform multi-GPU mesh travels between GPUs.  Either way blocks with
- * remote faces are updated first and their faces sent while the interior blocks compute. */
+/* How the per-cycle halo of a (non-adaptive) multi-GPU mesh travels between GPUs.  On uniform meshes
+ * blocks with remote faces are updated first and their faces sent while the interior blocks compute. */
 typedef enum {
   PH_HALO_AUTO = 0,  /* peer memory when every rank can map its peers' receive buffers, else NCCL */
   PH_HALO_NCCL = 1,  /* pack -> grouped ncclSend/ncclRecv -> unpack into ghost cells (P:536-549) */
@@ -109,8 +109,8 @@ typedef struct {
   void* (*dev_alloc)(size_t bytes, void* ctx); /* optional device allocator (torch caching allocator) */
   void (*dev_free)(void* ptr, void* ctx);
   void* alloc_ctx;
-  int32_t halo_transport;           /* ph_halo_transport (ABI 2).  Peer memory applies to uniform,
-                                       non-adaptive, nghost-2 meshes with nranks > 1; its receive
+  int32_t halo_transport;           /* ph_halo_transport (ABI 2).  Peer memory applies to uniform or
+                                       static multilevel nghost-2 meshes with nranks > 1; its receive
                                        buffers come from cudaMalloc (CUDA IPC), not dev_alloc.
                                        The full exchange (ph_refresh, ph_exchange) stays on NCCL. */
   int32_t wavespeed;                /* ph_wavespeed (ABI 3); 0 = Davis */

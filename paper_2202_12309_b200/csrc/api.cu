@@ -807,7 +807,7 @@ static ph_status setup_peer(ph_mesh* m, bool* ok_out) {
   // Each per-cycle pack task is one face of one block (uniform mesh: faces only), whose source shift
   // so names the face -- so[d] = +n: the sender's +d layers, -n: its -d layers.
   int tx = 0, ty = 0;
-  m->fused_put = getenv("PH_FUSED_PUT") && atoi(getenv("PH_FUSED_PUT")) != 0 &&
+  m->fused_put = getenv("PH_FUSED_PUT") && atoi(getenv("PH_FUSED_PUT")) != 0 && !m->multilevel &&
                  stage_tile(m->G, m->cfg.recon, false, &tx, &ty);
   for (const XTask& t : PL.pack.tasks) {
     int d = 0;
@@ -1536,12 +1536,14 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
   }
   bool uniform = true;
   for (auto& b : m->blocks) uniform = uniform && b.loc.level == 0;
-  const bool peer_cfg = m->nranks > 1 && uniform && cfg->refinement != PH_REF_ADAPTIVE && !m->no_direct_halo &&
+  // peer transport: uniform or static multilevel meshes (the plan is fixed: AMR rebuilds it on remesh)
+  (void)uniform;
+  const bool peer_cfg = m->nranks > 1 && cfg->refinement != PH_REF_ADAPTIVE && !m->no_direct_halo &&
                         G.g == 2 && cfg->halo_transport != PH_HALO_NCCL;
   if (cfg->halo_transport == PH_HALO_PEER && !peer_cfg) {
     delete m->tree;
     delete m;
-    return fail(PH_ERR_UNSUPPORTED, "peer halo needs nranks > 1 and a static uniform nghost-2 mesh with the direct halo");
+    return fail(PH_ERR_UNSUPPORTED, "peer halo needs nranks > 1 and a non-adaptive nghost-2 mesh with the direct halo");
   }
   ph_status st = build_plan(m);
   if (st != PH_OK) {

@@ -817,8 +817,8 @@ __global__ void __launch_bounds__(XT) xfill_kernel(XArgs A, Geom G) {
         const int fi = 2 * i - t.so[0], fj = 2 * j - t.so[1], fk = 2 * k - t.so[2];
         const double* s = A.U + (int64_t)t.src_slot * G.bstride + ((int64_t)(fk + G.g) * G.N[1] + (fj + G.g)) * G.N[0] + (fi + G.g);
         const int64_t sj = G.N[0], sk = (int64_t)G.N[0] * G.N[1];
-        if (t.dst_slot < 0) {
-          double* d = A.sbuf + t.buf + c;
+        if (t.dst_slot < 0) {  // pack (or put into peer bc's receive buffer, as for copies)
+          double* d = (t.bc >= 0 ? A.peer_rbuf[t.bc] : A.sbuf) + t.buf + c;
 #pragma unroll
           for (int v = 0; v < NVAR; ++v) d[(int64_t)v * t.ncell] = mean8(s + v * G.vstride, sj, sk);
         } else if (t.kind == T_RESTRICT) {

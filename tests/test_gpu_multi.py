@@ -27,6 +27,8 @@ def _port():
 
 
 CASES = [(c, "auto") for c in ("smr2", "smr3_walls", "amr2", "wenoz")]
+# static multilevel meshes with the NCCL halo too (auto picks peer memory for them now)
+CASES += [(c, "nccl") for c in ("smr2", "smr3_walls")]
 # uniform meshes: both halo transports (NCCL pack/send/unpack, and peer memory read in place)
 CASES += [(c, h) for c in ("blast", "sod_walls", "wave64", "tiny") for h in ("nccl", "peer")]
 # the fused put: the boundary blocks' stage kernel stores its faces into the peers' buffers itself
