@@ -6,6 +6,7 @@
 // (P:640-650).  Formulas and their operation order follow SURVEY.md §8(c) O5-O8.
 //
 // No tensor cores: every kernel here is an fp64 stencil or copy (bandwidth / fp64-issue bound).
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -176,11 +177,12 @@ __device__ __forceinline__ double ppm_dm_rn(double a, double b, double c) {
   return dq > 0.0 ? m : -m;
 }
 
-__device__ __forceinline__ void ppm_cell_rn(const double* q, double& ql, double& qr) {
-  const double dm_m = ppm_dm_rn(q[0], q[1], q[2]), dm_0 = ppm_dm_rn(q[1], q[2], q[3]), dm_p = ppm_dm_rn(q[2], q[3], q[4]);
-  double L = __dsub_rn(__dadd_rn(q[1], __dmul_rn(0.5, __dsub_rn(q[2], q[1]))), __ddiv_rn(__dsub_rn(dm_0, dm_m), 6.0));
-  double R = __dsub_rn(__dadd_rn(q[2], __dmul_rn(0.5, __dsub_rn(q[3], q[2]))), __ddiv_rn(__dsub_rn(dm_p, dm_0), 6.0));
-  const double c = q[2];
+// PPM interface values of one cell from its neighbours qm, c, qp and the three limited slopes
+// dm_m, dm_0, dm_p (cells c-1, c, c+1); split out so a line march can reuse each slope three times.
+__device__ __forceinline__ void ppm_lr_rn(double qm, double c, double qp, double dm_m, double dm_0, double dm_p,
+                                          double& ql, double& qr) {
+  double L = __dsub_rn(__dadd_rn(qm, __dmul_rn(0.5, __dsub_rn(c, qm))), __ddiv_rn(__dsub_rn(dm_0, dm_m), 6.0));
+  double R = __dsub_rn(__dadd_rn(c, __dmul_rn(0.5, __dsub_rn(qp, c))), __ddiv_rn(__dsub_rn(dm_p, dm_0), 6.0));
   if (__dmul_rn(__dsub_rn(R, c), __dsub_rn(c, L)) <= 0.0) {
     L = c;
     R = c;
@@ -192,6 +194,11 @@ __device__ __forceinline__ void ppm_cell_rn(const double* q, double& ql, double&
   }
   ql = L;
   qr = R;
+}
+
+__device__ __forceinline__ void ppm_cell_rn(const double* q, double& ql, double& qr) {
+  const double dm_m = ppm_dm_rn(q[0], q[1], q[2]), dm_0 = ppm_dm_rn(q[1], q[2], q[3]), dm_p = ppm_dm_rn(q[2], q[3], q[4]);
+  ppm_lr_rn(q[1], q[2], q[3], dm_m, dm_0, dm_p, ql, qr);
 }
 
 __device__ __forceinline__ double wenoz_rn(double a, double b, double c, double d, double e) {
@@ -1286,6 +1293,98 @@ __global__ void hoflux_kernel(const double* W, double* F, Geom G) {
   }
 }
 
+// Line-march variant of hoflux_kernel (same arithmetic, bit for bit): one thread owns a line of
+// faces along DIR (or a segment of it, when there are too few lines to fill the GPU) and slides a
+// 6-cell register window up the line, so each cell is loaded once per line instead of six times,
+// and the per-cell pieces of the reconstruction are computed once and carried: PLM's limited slope
+// (used by the two faces of a cell) and PPM's limited slopes dm and right interface value (each
+// dm feeds three cells, each cell two faces).  WENO-Z's two face values share no exact
+// sub-expression (the mirrored smoothness indicators round differently), so only the loads are
+// saved.  Lines are numbered with the fastest non-DIR axis fastest (coalesced for DIR = y, z).
+template <int DIR, int RECON>
+__global__ void __launch_bounds__(128) holine_kernel(const double* W, double* F, int nslots, int nseg, Geom G) {
+  constexpr int AX = (DIR == 0) ? 1 : 0, BX = (DIR == 2) ? 1 : 2;
+  constexpr int CN = 1 + DIR, C1 = 1 + (DIR + 1) % 3, C2 = 1 + (DIR + 2) % 3;
+  const int na = G.n[AX], nb = G.n[BX], nm = G.n[DIR];
+  const int64_t lines = (int64_t)na * nb;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= lines * nseg * nslots) return;
+  const int64_t line = t % lines;
+  const int seg = (int)((t / lines) % nseg);
+  const int slot = (int)(t / (lines * nseg));
+  const int a = (int)(line % na), b = (int)(line / na);
+  const int m0 = (int)((int64_t)seg * (nm + 1) / nseg), m1 = (int)((int64_t)(seg + 1) * (nm + 1) / nseg);
+  int c3[3];
+  c3[DIR] = 0;
+  c3[AX] = a;
+  c3[BX] = b;
+  const int64_t st = (DIR == 0) ? 1 : ((DIR == 1) ? G.N[0] : (int64_t)G.N[0] * G.N[1]);
+  const double* p = W + (int64_t)slot * G.bstride + ((int64_t)(c3[2] + G.g) * G.N[1] + (c3[1] + G.g)) * G.N[0] + (c3[0] + G.g);
+  const int e0 = G.n[0] + (DIR == 0), e1 = G.n[1] + (DIR == 1), e2 = G.n[2] + (DIR == 2);
+  const int64_t fvs = (int64_t)e0 * e1 * e2;
+  const int64_t fst = (DIR == 0) ? 1 : ((DIR == 1) ? e0 : (int64_t)e0 * e1);
+  double* fb = F + (int64_t)slot * NVAR * fvs + ((int64_t)c3[2] * e1 + c3[1]) * e0 + c3[0];
+  const int cv[NVAR] = {0, CN, C1, C2, 4};
+  double q[NVAR][6], c1v[NVAR], c2v[NVAR], c3v[NVAR];  // window; carried per-cell terms
+#pragma unroll
+  for (int s = 0; s < NVAR; ++s) {
+    const double* qs = p + cv[s] * G.vstride;
+#pragma unroll
+    for (int u = 0; u < 6; ++u) q[s][u] = qs[(int64_t)(m0 - 3 + u) * st];
+    if (RECON <= 2) {
+      c1v[s] = slope_rn(q[s][1], q[s][2], q[s][3], RECON);  // slope of cell m0-1
+    } else if (RECON == 3) {
+      double Ldummy;
+      ppm_cell_rn(&q[s][0], Ldummy, c1v[s]);               // R of cell m0-1
+      c2v[s] = ppm_dm_rn(q[s][1], q[s][2], q[s][3]);       // dm of cell m0-1
+      c3v[s] = ppm_dm_rn(q[s][2], q[s][3], q[s][4]);       // dm of cell m0
+    }
+  }
+  for (int m = m0; m < m1; ++m) {
+    double nx[NVAR];
+    const bool more = m + 1 < m1;
+#pragma unroll
+    for (int s = 0; s < NVAR; ++s) nx[s] = more ? p[cv[s] * G.vstride + (int64_t)(m + 3) * st] : 0.0;
+    double wl[NVAR], wr[NVAR];
+#pragma unroll
+    for (int s = 0; s < NVAR; ++s) {
+      const double* qq = q[s];
+      if (RECON <= 2) {
+        const double sm = slope_rn(qq[2], qq[3], qq[4], RECON);
+        wl[s] = __dadd_rn(qq[2], __dmul_rn(0.5, c1v[s]));
+        wr[s] = __dsub_rn(qq[3], __dmul_rn(0.5, sm));
+        c1v[s] = sm;
+      } else if (RECON == 3) {
+        const double dp = ppm_dm_rn(qq[3], qq[4], qq[5]);
+        double L, R;
+        ppm_lr_rn(qq[2], qq[3], qq[4], c2v[s], c3v[s], dp, L, R);
+        wl[s] = c1v[s];
+        wr[s] = L;
+        c1v[s] = R;
+        c2v[s] = c3v[s];
+        c3v[s] = dp;
+      } else {
+        wl[s] = wenoz_rn(qq[0], qq[1], qq[2], qq[3], qq[4]);
+        wr[s] = wenoz_rn(qq[5], qq[4], qq[3], qq[2], qq[1]);
+      }
+    }
+    double Fn[NVAR];
+    hlle_rn(wl, wr, G, Fn);
+    double* fo = fb + (int64_t)m * fst;
+    fo[0] = Fn[0];
+    fo[CN * fvs] = Fn[1];
+    fo[C1 * fvs] = Fn[2];
+    fo[C2 * fvs] = Fn[3];
+    fo[4 * fvs] = Fn[4];
+#pragma unroll
+    for (int s = 0; s < NVAR; ++s) {
+#pragma unroll
+      for (int u = 0; u < 5; ++u) q[s][u] = q[s][u + 1];
+      q[s][5] = nx[s];
+    }
+  }
+}
+
 template <bool REDUCE, bool USE_U0>
 __global__ void houpdate_kernel(StageArgs A, const double* Fx, const double* Fy, const double* Fz, Geom G) {
   const int k = blockIdx.x % G.n[2];
@@ -1357,6 +1456,7 @@ __global__ void houpdate_kernel(StageArgs A, const double* Fx, const double* Fy,
     }
   }
 }
+
 
 // ------------------------------------------------------------------------------ AMR (O9)
 // Refinement indicator eps_B = max over interior cells of |grad p| / p with central differences
@@ -1829,12 +1929,41 @@ cudaError_t launch_interior_copy(double* U, double* buf, int slot0, int nslots, 
   return PH_CHECK_LAUNCH();
 }
 
+template <int DIR, int R>
+static void launch_holine(const double* W, double* F, int nslots, const Geom& G, cudaStream_t s) {
+  const int64_t lines = (int64_t)G.n[DIR == 0 ? 1 : 0] * G.n[DIR == 2 ? 1 : 2] * nslots;
+  // enough threads for ~4 resident CTAs of 128 per SM; split lines into segments only when short of that
+  const int64_t want = 148LL * 4 * 128;
+  int nseg = (int)std::min<int64_t>(G.n[DIR] + 1, std::max<int64_t>(1, (want + lines - 1) / lines));
+  if (const char* e = getenv("PH_HO_NSEG")) nseg = std::max(1, std::min(G.n[DIR] + 1, atoi(e)));  // tests
+  const int64_t threads = lines * nseg;
+  holine_kernel<DIR, R><<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(W, F, nslots, nseg, G);
+}
+
+// Flux kernel per direction (ncu, 256^3 in 64^3 blocks, us per launch, per-face / line march):
+//   PLM   x 530 / 1352   y 523 / 335   z 546 / 332
+//   PPM   x 2561 / 2388  y 2572 / 1803 z 2577 / 1785
+//   WENO  x 3795 / 4963  y 4036 / 4485 z 3975 / 4427
+// The x march is slow for PLM (its lines run across rows: 32 rows per warp load and store), and
+// WENO-Z shares nothing across faces while the march's window costs it occupancy, so those take the
+// per-face kernel.  PH_HO_FACE=1 / PH_HO_LINE=1 force one kernel for every direction (A/B, tests).
 template <int R>
 static cudaError_t launch_hoflux_r(const double* W, double* Fx, double* Fy, double* Fz, int nslots, const Geom& G,
                                    cudaStream_t s) {
-  hoflux_kernel<0, R><<<nslots * G.n[2], 128, 0, s>>>(W, Fx, G);
-  hoflux_kernel<1, R><<<nslots * G.n[2], 128, 0, s>>>(W, Fy, G);
-  hoflux_kernel<2, R><<<nslots * (G.n[2] + 1), 128, 0, s>>>(W, Fz, G);
+  const char* pf = getenv("PH_HO_FACE");
+  const char* pl = getenv("PH_HO_LINE");
+  const bool all_face = pf && pf[0] == '1', all_line = pl && pl[0] == '1';
+  const bool line_x = all_line || (!all_face && R == 3);
+  const bool line_yz = all_line || (!all_face && R != 4);
+  if (line_x) launch_holine<0, R>(W, Fx, nslots, G, s);
+  else hoflux_kernel<0, R><<<nslots * G.n[2], 128, 0, s>>>(W, Fx, G);
+  if (line_yz) {
+    launch_holine<1, R>(W, Fy, nslots, G, s);
+    launch_holine<2, R>(W, Fz, nslots, G, s);
+  } else {
+    hoflux_kernel<1, R><<<nslots * G.n[2], 128, 0, s>>>(W, Fy, G);
+    hoflux_kernel<2, R><<<nslots * (G.n[2] + 1), 128, 0, s>>>(W, Fz, G);
+  }
   return cudaGetLastError();
 }
 

@@ -261,15 +261,24 @@ def test_graph_replay_equals_eager(P, monkeypatch):
     assert outs[0][2] == outs[1][2]
 
 
-@pytest.mark.parametrize("recon", [0, 3, 4])
-def test_high_order_blast_and_sod(oracle_mod, P, recon):
+@pytest.mark.parametrize("recon", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("nseg", [None, "1", "7"])
+def test_high_order_blast_and_sod(oracle_mod, P, recon, nseg, monkeypatch):
     """NEXT 3: PPM / WENO-Z (nghost 3) through the generic high-order GPU path vs the oracle.
     This path computes in the oracle's exact operation order (WENO-Z weights and the PPM extremum
-    switch amplify round-off), so the states and dt must agree bit for bit."""
+    switch amplify round-off), so the states and dt must agree bit for bit.  nseg forces the number
+    of segments each line of faces is split into by the line-march flux kernel (None: its own
+    choice, which is many short segments at these sizes; "1": one march over the whole line, the
+    case of large meshes; "7": segment boundaries at ragged offsets)."""
+    if nseg is not None:  # the line march in every direction, with a forced segment count
+        monkeypatch.setenv("PH_HO_LINE", "1")
+        monkeypatch.setenv("PH_HO_NSEG", nseg)
     o, g = _run_both(oracle_mod, P, P.BLAST, [10.0, 0.1, 0.15], 8, recon=recon, nghost=3,
                      mesh_nx=(48, 48, 48), block_nx=(16, 16, 16), xmin=(-.5,) * 3, xmax=(.5,) * 3)
     _check_run(o, g)
     assert np.array_equal(gather(g), gather(o)) and g.time() == o.time()
+    if nseg is not None and recon in (1, 2):
+        return  # the 1-D Sod run below adds nothing for these two beyond minmod's
     kw = dict(mesh_nx=(128, 6, 6), block_nx=(32, 6, 6), gamma=1.4, recon=recon, nghost=3,
               bc_inner=(P.OUTFLOW, 0, 2), bc_outer=(P.OUTFLOW, 0, 2))
     o, g = _run_both(oracle_mod, P, P.SOD, [0.5], 100000, tlim=0.1, **kw)

@@ -38,6 +38,9 @@ def cases():
     c["ho-ppm"] = dict(kw=dict(mesh_nx=(256,) * 3, block_nx=(64,) * 3, recon=3, nghost=3, **u), prob=2, par=BLAST)
     c["ho-wenoz"] = dict(kw=dict(mesh_nx=(256,) * 3, block_nx=(64,) * 3, recon=4, nghost=3, **u), prob=2, par=BLAST)
     c["ho-plm"] = dict(kw=dict(mesh_nx=(256,) * 3, block_nx=(64,) * 3, recon=0, nghost=3, **u), prob=2, par=BLAST)
+    for r in ("ppm", "wenoz", "plm"):  # A/B: the per-face flux kernel instead of the line march
+        c[f"ho-{r}-face"] = dict(c[f"ho-{r}"], env={"PH_HO_FACE": "1"})
+        c[f"ho-{r}-line"] = dict(c[f"ho-{r}"], env={"PH_HO_LINE": "1"})
     # NEXT 1: the paper's own multilevel mesh: 256^3 root, 32^3 blocks, [0.3,0.7]^3 at
     # level 3 -> 296/1216/1352/21952 blocks (24,816; 813M cells; ~93 GB of block pools)
     c["nx1"] = dict(kw=dict(mesh_nx=(256,) * 3, block_nx=(32,) * 3, max_level=3, refinement=1,
