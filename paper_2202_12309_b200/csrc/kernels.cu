@@ -1258,7 +1258,7 @@ __global__ void prim_kernel(const double* U, double* W, const BlockMeta* meta, E
 }
 
 template <int DIR, int RECON>
-__global__ void hoflux_kernel(const double* W, double* F, Geom G) {
+__device__ __forceinline__ void hoflux_body(const double* W, double* F, const Geom& G) {
   const int e0 = G.n[0] + (DIR == 0), e1 = G.n[1] + (DIR == 1), e2 = G.n[2] + (DIR == 2);
   const int k = blockIdx.x % e2;
   const int slot = blockIdx.x / e2;
@@ -1302,7 +1302,7 @@ __global__ void hoflux_kernel(const double* W, double* F, Geom G) {
 // sub-expression (the mirrored smoothness indicators round differently), so only the loads are
 // saved.  Lines are numbered with the fastest non-DIR axis fastest (coalesced for DIR = y, z).
 template <int DIR, int RECON>
-__global__ void __launch_bounds__(128) holine_kernel(const double* W, double* F, int nslots, int nseg, Geom G) {
+__device__ __forceinline__ void holine_body(const double* W, double* F, int nslots, int nseg, const Geom& G) {
   constexpr int AX = (DIR == 0) ? 1 : 0, BX = (DIR == 2) ? 1 : 2;
   constexpr int CN = 1 + DIR, C1 = 1 + (DIR + 1) % 3, C2 = 1 + (DIR + 2) % 3;
   const int na = G.n[AX], nb = G.n[BX], nm = G.n[DIR];
@@ -1383,6 +1383,19 @@ __global__ void __launch_bounds__(128) holine_kernel(const double* W, double* F,
       q[s][5] = nx[s];
     }
   }
+}
+
+template <int DIR, int RECON>
+__global__ void hoflux_kernel(const double* W, double* F, Geom G) {
+  hoflux_body<DIR, RECON>(W, F, G);
+}
+// PPM's march is capped at 128 registers (4 CTAs of 128 per SM; some spills): +2 % over 158-174
+// registers, 3 % over a 168-register cap.  A cap on the per-face WENO-Z kernel (80/72/64 registers)
+// loses 7/14/23 % (profiles/r01_ho_line_march.md).
+template <int DIR, int RECON>
+__global__ void __launch_bounds__(128, RECON == 3 ? 4 : 1) holine_kernel(const double* W, double* F, int nslots,
+                                                                         int nseg, Geom G) {
+  holine_body<DIR, RECON>(W, F, nslots, nseg, G);
 }
 
 template <bool REDUCE, bool USE_U0>
@@ -1937,7 +1950,14 @@ static void launch_holine(const double* W, double* F, int nslots, const Geom& G,
   int nseg = (int)std::min<int64_t>(G.n[DIR] + 1, std::max<int64_t>(1, (want + lines - 1) / lines));
   if (const char* e = getenv("PH_HO_NSEG")) nseg = std::max(1, std::min(G.n[DIR] + 1, atoi(e)));  // tests
   const int64_t threads = lines * nseg;
-  holine_kernel<DIR, R><<<(unsigned)((threads + 127) / 128), 128, 0, s>>>(W, F, nslots, nseg, G);
+  const unsigned grid = (unsigned)((threads + 127) / 128);
+  holine_kernel<DIR, R><<<grid, 128, 0, s>>>(W, F, nslots, nseg, G);
+}
+
+template <int DIR, int R>
+static void launch_hoface(const double* W, double* F, int nslots, const Geom& G, cudaStream_t s) {
+  const int grid = nslots * (G.n[2] + (DIR == 2));
+  hoflux_kernel<DIR, R><<<grid, 128, 0, s>>>(W, F, G);
 }
 
 // Flux kernel per direction (ncu, 256^3 in 64^3 blocks, us per launch, per-face / line march):
@@ -1956,13 +1976,13 @@ static cudaError_t launch_hoflux_r(const double* W, double* Fx, double* Fy, doub
   const bool line_x = all_line || (!all_face && R == 3);
   const bool line_yz = all_line || (!all_face && R != 4);
   if (line_x) launch_holine<0, R>(W, Fx, nslots, G, s);
-  else hoflux_kernel<0, R><<<nslots * G.n[2], 128, 0, s>>>(W, Fx, G);
+  else launch_hoface<0, R>(W, Fx, nslots, G, s);
   if (line_yz) {
     launch_holine<1, R>(W, Fy, nslots, G, s);
     launch_holine<2, R>(W, Fz, nslots, G, s);
   } else {
-    hoflux_kernel<1, R><<<nslots * G.n[2], 128, 0, s>>>(W, Fy, G);
-    hoflux_kernel<2, R><<<nslots * (G.n[2] + 1), 128, 0, s>>>(W, Fz, G);
+    launch_hoface<1, R>(W, Fy, nslots, G, s);
+    launch_hoface<2, R>(W, Fz, nslots, G, s);
   }
   return cudaGetLastError();
 }
