@@ -116,16 +116,27 @@ def dist_env():
 
 
 # ------------------------------------------------------------------------------ oracle legs
-def oracle_sample(cfg_name, steps, warmup, threads):
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_sample(cfg_name, steps, warmup, threads, mesh_n=256):
     """The CPU oracle (as it stands) on a bounded sample of the workload: the same 64^3 blocks,
-    method and blast problem on a 128^3 periodic mesh (8 blocks); one oracle cycle per step."""
+    method and blast problem on a 256^3 periodic mesh (BASELINE configs[1] as written = reading 2a:
+    64 blocks, at least one per core); one oracle cycle per step."""
     import oracle
     oracle.build()
-    kw = dict(mesh_nx=(128, 128, 128), block_nx=(64, 64, 64), xmin=(-0.25,) * 3, xmax=(0.25,) * 3,
-              nthreads=threads)
+    h = 0.5 * mesh_n / 256
+    kw = dict(mesh_nx=(mesh_n,) * 3, block_nx=(64, 64, 64), xmin=(-h,) * 3, xmax=(h,) * 3, nthreads=threads)
     m = oracle.Mesh(**kw)
     m.set_problem(oracle.BLAST, BLAST)
-    cells = 128 ** 3
+    cells = mesh_n ** 3
     for _ in range(warmup):
         m.step(1)
     ts = []
@@ -134,7 +145,28 @@ def oracle_sample(cfg_name, steps, warmup, threads):
         m.step(1)
         ts.append(time.perf_counter() - t0)
     total = sum(ts)
-    return cells * steps / total, total / steps, "blast, 128^3 periodic mesh of 64^3 blocks (8 blocks), 1 oracle cycle per step"
+    nb = (mesh_n // 64) ** 3
+    return cells * steps / total, total / steps, (f"blast, {mesh_n}^3 periodic mesh of 64^3 blocks ({nb} blocks), "
+                                                   f"{steps} oracle cycle(s), {threads} OpenMP thread(s)")
+
+
+def cpu_baseline_block(steps):
+    """cpu_baseline object: all host cores on the 2a sample, one thread on one 64^3 block, the CPU model,
+    and the full BASELINE.md §3 plan as last measured on a GPU box (tools/cpu_baseline.py)."""
+    threads = len(os.sched_getaffinity(0))
+    zcs, sec, sample = oracle_sample("2a", steps, 0, threads)
+    z1, s1, sample1 = oracle_sample("1blk", 1, 0, 1, mesh_n=64)
+    out = {"value": zcs, "unit": "zone-cycles/s", "cores": threads, "kind": "oracle", "sample": sample,
+           "cpu_model": cpu_model(),
+           "single_thread": {"value": z1, "unit": "zone-cycles/s", "cores": 1, "sample": sample1}}
+    fp = os.path.join(ROOT, "profiles", "r02_cpu_baseline.json")
+    if os.path.exists(fp):
+        try:
+            out["full_plan"] = {"source": "profiles/r02_cpu_baseline.json (tools/cpu_baseline.py, not this run)",
+                                "rows": json.load(open(fp)).get("rows")}
+        except Exception:
+            pass
+    return out
 
 
 def run_reference(args):
@@ -148,7 +180,8 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": f"oracle sample of {args.config}", "sample": sample},
-        "cpu_baseline": {"value": zcs, "unit": "zone-cycles/s", "cores": threads, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": zcs, "unit": "zone-cycles/s", "cores": threads, "kind": "oracle", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": zcs, "unit": "zone-cycles/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -173,7 +206,8 @@ def run_ours(args):
     transport = {"auto": P.HALO_AUTO, "nccl": P.HALO_NCCL, "peer": P.HALO_PEER}[args.halo]
     mesh = P.Mesh(device=local, rank=rank, nranks=world, stream=stream, halo_transport=transport, **W)
     halo = "local direct halo" if world == 1 else (
-        "peer memory (stage kernels read remote faces over NVLink)" if mesh.plan_info()["peer_halo"]
+        "peer memory: the pack kernel stores boundary faces into the peer's receive buffer over NVLink "
+        "(CUDA IPC), release / acquire flags" if mesh.plan_info()["peer_halo"]
         else "NCCL send/recv of remote faces")
     nglob = mesh.num_blocks()
     n = W["block_nx"][0]
@@ -194,13 +228,18 @@ def run_ours(args):
     clk = Clocks(local)
     clk.start()
     barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    mesh.step(args.steps)
-    e1.record(stream)
+    # an event at every cycle boundary (the paper quotes the median of several tens of
+    # cycles): value stays total cells x K / total time, the median is reported beside it
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    evs[0].record(stream)
+    for i in range(args.steps):
+        mesh.step(1)
+        evs[i + 1].record(stream)
     barrier()
     clocks = clk.stop()
-    ms = e0.elapsed_time(e1)
+    ms = evs[0].elapsed_time(evs[-1])
+    per_cycle = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    med = statistics.median(per_cycle)
     stage_ms, stage_n, exch_ms, exch_n = mesh.kernel_timing(False)
     launches = mesh.launch_count() - l0
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -208,6 +247,10 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     value = cells * args.steps / (ms_max * 1e-3)
+    tm = torch.tensor([med], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    med_max = float(tm.item())
 
     # correctness guard: the run must still be physical and conserve mass
     hist = mesh.history()
@@ -290,20 +333,32 @@ def run_ours(args):
     else:
         workload_desc = f"blast 3D, {size} cells per GPU in 64^3 blocks " + base
     # co-limiter (SURVEY §8(d) "report both"): the fp64 pipe.  Instructions per cell-stage from the
-    # committed ncu capture of this kernel; peak = 148 SMs x 64 fp64 lanes/clk x 1965 MHz (B200 unit
-    # counts and max clock).
+    # committed ncu capture of the current stage kernel (profiles/stage_kernel_counts.json); peak =
+    # the measured fp64 lanes / clock / SM of profiles/r02_ubench_fp64.jsonl x 148 SMs x the median SM
+    # clock of this run.
     fp64 = None
-    pp = os.path.join(ROOT, "profiles", "r01_stage_2b_v11.json")
-    if os.path.exists(pp) and stage_n:
+    pc = os.path.join(ROOT, "profiles", "stage_kernel_counts.json")
+    pu = os.path.join(ROOT, "profiles", "r02_ubench_fp64.jsonl")
+    if os.path.exists(pc) and os.path.exists(pu) and stage_n:
         try:
-            per_cell = float(json.load(open(pp))["fp64_inst_per_cell"])
+            cnt = json.load(open(pc))
+            per_cell = float(cnt["fp64_inst_per_cell_stage"])
+            lanes = max(json.loads(l)["lane_ops_per_clk_per_sm"] for l in open(pu)
+                        if l.startswith("{\"op\": \"d") and "+" not in json.loads(l)["op"])
+            mhz = (clocks or {}).get("sm_mhz") or 1965.0
             ach = per_cell * nloc_cells * 2 * args.steps / (stage_ms * 1e-3)  # all timed stage launches
-            fpk = 148 * 64 * 1965e6
+            fpk = 148 * lanes * mhz * 1e6
             fp64 = {"bound": "alu", "achieved": ach, "peak": fpk, "unit": "fp64-pipe thread instr/s",
                     "frac": ach / fpk, "inst_per_cell_stage": per_cell,
-                    "source": "inst count: ncu profiles/r01_stage_2b_v11.json; peak: 148 SM x 64 lanes x 1.965 GHz"}
+                    "inst_total_per_cell_stage": cnt.get("thread_inst_per_cell_stage"),
+                    "source": f"inst count: {cnt.get('source')}; peak: 148 SM x {lanes:.1f} lanes/clk "
+                              f"(measured DADD/DMUL/DFMA, profiles/r02_ubench_fp64.jsonl) x {mhz:.0f} MHz"}
         except Exception:
             fp64 = None
+    cyc_bytes = nloc_cells * (2 * r * 40.0 + 120.0)  # both stages, algorithmic (B_min), per GPU
+    per_gpu = {"bytes_per_cycle": cyc_bytes, "ms_per_cycle": ms_max / args.steps,
+               "achieved": cyc_bytes / (ms_max / args.steps * 1e-3) / 1e9,
+               "frac": cyc_bytes / (ms_max / args.steps * 1e-3) / 1e9 / peak}
     line = {
         "metric": "zone-cycles/s", "value": value, "unit": "zone-cycles/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
@@ -313,9 +368,18 @@ def run_ours(args):
                    "global_blocks": nglob, "block": n, "nghost": 2,
                    "l2": "inputs larger than L2 (state %.1f GB per GPU vs 126 MB L2)" % (2 * nloc * 5 * (n + 4) ** 3 * 8 / 1e9),
                    "parallelism": f"morton-partition dp{world}", "halo": halo},
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                     "kernel": "stage_kernel (fused cons->prim, PLM, HLLE x/y/z, divergence, RK combine)",
+        "median": {"ms_per_step": med_max, "value": cells / (med_max * 1e-3),
+                   "note": "median of per-cycle CUDA events (P:1005-1007), max over ranks"},
+        "roofline": {"bound": "hbm", "achieved": achieved if world == 1 else per_gpu["achieved"], "peak": peak,
+                     "unit": "GB/s",
+                     "frac": ((achieved if world == 1 else per_gpu["achieved"]) / peak) if achieved else None,
+                     "traffic": traffic,
+                     "definition": ("algorithmic bytes per stage launch / mean launch time (CUDA events)" if world == 1
+                                    else "per GPU: algorithmic bytes of both stages per cycle / cycle time "
+                                         "(each stage is a boundary and an interior launch running concurrently)"),
+                     "per_launch": {"achieved": achieved, "frac": (achieved / peak) if achieved else None},
+                     "per_gpu_cycle": per_gpu,
+                     "kernel": "stage kernel (stage2.cu: fused cons->prim, PLM, HLLE x/y/z, divergence, RK combine)",
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
                      "algorithmic_bytes_per_launch": stage_bytes,
                      "stage_ms_avg": stage_avg_ms, "stage_share_of_step": stage_ms / ms if ms else None,
@@ -330,10 +394,7 @@ def run_ours(args):
     }
     # ---- CPU baseline: the oracle on the host cores, rank 0 at N=1 only
     if world == 1 and not args.no_cpu:
-        threads = len(os.sched_getaffinity(0))
-        zcs, sec, sample = oracle_sample(args.config, args.cpu_steps, 0, threads)
-        line["cpu_baseline"] = {"value": zcs, "unit": "zone-cycles/s", "cores": threads, "kind": "oracle",
-                                "sample": sample}
+        line["cpu_baseline"] = cpu_baseline_block(args.cpu_steps)
     if rank == 0:
         print(json.dumps(line), flush=True)
     mesh.close()
@@ -355,7 +416,7 @@ def main():
                     help="multi-GPU halo transport (auto: peer memory when every rank can map its peers)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-steps", type=int, default=2)
+    ap.add_argument("--cpu-steps", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=12)
     args = ap.parse_args()
     if args.warmup < 3:

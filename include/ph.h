@@ -12,7 +12,9 @@
  *   Readings where the paper is silent are SURVEY.md §8(c) A1-A30 plus DESIGN.md A5'-A41.
  *
  * Conventions
- *   - Every function returns ph_status; PH_OK == 0.  No C++ exception crosses this boundary.
+ *   - Every function returns ph_status; PH_OK == 0.  No C++ exception crosses this boundary: every
+ *     entry point catches (std::bad_alloc -> PH_ERR_OOM, std::logic_error -> PH_ERR_INVALID_ARG,
+ *     anything else -> PH_ERR_STATE) and reports the exception text through ph_last_error().
  *     On error, ph_last_error() returns a thread-local message valid until the next call.
  *   - Ownership: the caller owns every host buffer it passes and states its capacity; the
  *     library never retains host pointers.  The library owns all device memory (obtained
@@ -192,11 +194,14 @@ ph_status ph_exchange(ph_mesh* m); /* ghost exchange of U0 only (O7); collective
 ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info /*nullable*/);
 /* Host-buffer end-to-end call: upload the interiors of all local blocks from `host_in`
  * ([nlocal][5][n3][n2][n1], local gid order), run ncycles, download them into `host_out`.
- * Times the full path incl. host<->device copies (bench e2e leg). */
+ * Times the full path incl. host<->device copies (bench e2e leg).  Both buffers hold exactly
+ * nelem doubles (checked against the local block count; PH_ERR_INVALID_ARG otherwise).
+ * Adaptive meshes return PH_ERR_UNSUPPORTED: a remesh inside the call would change the local
+ * block set, and with it the layout of host_out. */
 ph_status ph_step_host(ph_mesh* m, const double* host_in, double* host_out, int64_t nelem,
                        int32_t ncycles, double tlim);
 /* The same, enqueued on cfg->stream without waiting (host buffers must be pinned and stay valid until
- * ph_sync; AMR meshes still synchronise inside their tag passes).  Two meshes on two streams can
+ * ph_sync; adaptive meshes: PH_ERR_UNSUPPORTED as above).  Two meshes on two streams can
  * overlap one problem's device->host copy with the next one's host->device copy. */
 ph_status ph_step_host_async(ph_mesh* m, const double* host_in, double* host_out, int64_t nelem,
                              int32_t ncycles, double tlim);

@@ -1051,6 +1051,7 @@ static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a
     A.nkc = m->nkc;
     A.KC = m->KC;
     A.cta_base = p0 * per_blk;
+    A.pool_slots = (int)std::max<int64_t>((int64_t)m->local_gids.size(), 1);
     A.stage = stage;
     if (put && m->fused_put) A.peer_rbuf = m->d_prbuf[Uout == m->U1 ? 0 : 1];
     if (m->Hpool) {
@@ -1437,19 +1438,32 @@ static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, 
 }
 
 /* ------------------------------------------------------------------------------- C ABI */
+// Every extern "C" entry point runs inside PH_API_BEGIN / PH_API_END: no C++ exception crosses the
+// ABI (ph.h); a throw becomes a status code with the message in ph_last_error().
+#define PH_API_BEGIN try {
+#define PH_API_END                                                                          \
+  }                                                                                         \
+  catch (const std::bad_alloc&) { return fail(PH_ERR_OOM, "out of host memory"); }         \
+  catch (const std::logic_error& e) { return fail(PH_ERR_INVALID_ARG, e.what()); }         \
+  catch (const std::exception& e) { return fail(PH_ERR_STATE, e.what()); }                 \
+  catch (...) { return fail(PH_ERR_STATE, "unknown C++ exception"); }
+
 extern "C" {
 
 const char* ph_last_error(void) { return g_err.c_str(); }
 
 ph_status ph_nccl_unique_id(void* out, int32_t cap) {
+  PH_API_BEGIN
   if (!out || cap < (int32_t)sizeof(ncclUniqueId)) return fail(PH_ERR_INVALID_ARG, "need 128 bytes");
   ncclUniqueId id;
   NC(ncclGetUniqueId(&id));
   memcpy(out, &id, sizeof id);
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
+  PH_API_BEGIN
   if (!cfg || !out) return fail(PH_ERR_INVALID_ARG, "null argument");
   *out = nullptr;
   if (cfg->abi_version != PH_ABI_VERSION) return fail(PH_ERR_INVALID_ARG, "abi_version mismatch");
@@ -1611,9 +1625,11 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
   }
   *out = m;
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_mesh_destroy(ph_mesh* m) {
+  PH_API_BEGIN
   if (!m) return PH_OK;
   if (m->graph_exec) cudaGraphExecDestroy(m->graph_exec);
   if (m->ev_fork) cudaEventDestroy(m->ev_fork);
@@ -1649,6 +1665,7 @@ ph_status ph_mesh_destroy(ph_mesh* m) {
   delete m->tree;
   delete m;
   return PH_OK;
+  PH_API_END
 }
 
 static ph_status need_device(const ph_mesh* m) {
@@ -1658,20 +1675,25 @@ static ph_status need_device(const ph_mesh* m) {
 }
 
 ph_status ph_exchange(ph_mesh* m) {
+  PH_API_BEGIN
   TRY(need_device(m));
   TRY(exchange(m, m->U0, 0));
   return check_err(m);
+  PH_API_END
 }
 
 ph_status ph_refresh(ph_mesh* m) {
+  PH_API_BEGIN
   TRY(need_device(m));
   TRY(exchange(m, m->U0, 0));
   TRY(standalone_reduce(m, m->U0, 0));
   m->have_state = true;
   return check_err(m);
+  PH_API_END
 }
 
 ph_status ph_set_problem(ph_mesh* m, int32_t problem, const double* p, int32_t np) {
+  PH_API_BEGIN
   TRY(need_device(m));
   PgenArgs P{};
   P.problem = problem;
@@ -1715,6 +1737,7 @@ ph_status ph_set_problem(ph_mesh* m, int32_t problem, const double* p, int32_t n
   TRY(standalone_reduce(m, m->U0, 0));
   m->have_state = true;
   return check_err(m);
+  PH_API_END
 }
 
 static int64_t slot_of(const ph_mesh* m, int64_t gid) {
@@ -1724,6 +1747,7 @@ static int64_t slot_of(const ph_mesh* m, int64_t gid) {
 }
 
 ph_status ph_set_state(ph_mesh* m, int64_t gid, const double* cons, int64_t nelem) {
+  PH_API_BEGIN
   TRY(need_device(m));
   int64_t s = slot_of(m, gid);
   if (s == -2) return fail(PH_ERR_INVALID_ARG, "bad gid");
@@ -1737,9 +1761,11 @@ ph_status ph_set_state(ph_mesh* m, int64_t gid, const double* cons, int64_t nele
   CU(cudaStreamSynchronize(m->stream));
   m->have_state = true;
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_get_state(const ph_mesh* mc, int64_t gid, double* cons, int64_t nelem) {
+  PH_API_BEGIN
   ph_mesh* m = const_cast<ph_mesh*>(mc);
   TRY(need_device(m));
   int64_t s = slot_of(m, gid);
@@ -1754,9 +1780,11 @@ ph_status ph_get_state(const ph_mesh* mc, int64_t gid, double* cons, int64_t nel
   CU(cudaMemcpyAsync(cons, m->stage_buf, ni * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_get_state_full(const ph_mesh* mc, int64_t gid, double* out, int64_t nelem) {
+  PH_API_BEGIN
   ph_mesh* m = const_cast<ph_mesh*>(mc);
   TRY(need_device(m));
   int64_t s = slot_of(m, gid);
@@ -1771,9 +1799,11 @@ ph_status ph_get_state_full(const ph_mesh* mc, int64_t gid, double* out, int64_t
   CU(cudaMemcpyAsync(out, m->U0 + s * m->G.bstride, nelem * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
   CU(cudaStreamSynchronize(m->stream));
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_set_state_full(ph_mesh* m, int64_t gid, const double* in, int64_t nelem) {
+  PH_API_BEGIN
   TRY(need_device(m));
   int64_t s = slot_of(m, gid);
   if (s == -2) return fail(PH_ERR_INVALID_ARG, "bad gid");
@@ -1783,9 +1813,11 @@ ph_status ph_set_state_full(ph_mesh* m, int64_t gid, const double* in, int64_t n
   CU(cudaStreamSynchronize(m->stream));
   m->have_state = true;
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) {
+  PH_API_BEGIN
   TRY(need_device(m));
   if (!m->have_state) return fail(PH_ERR_STATE, "no state: call ph_set_problem or ph_set_state + ph_refresh");
   CU(launch_cycle_begin(m->d_st, tlim, 1, m->stream));
@@ -1849,22 +1881,32 @@ ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) 
     info->zone_cycles = cells * ncycles;
   }
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_step_host(ph_mesh* m, const double* host_in, double* host_out, int64_t nelem, int32_t ncycles,
                        double tlim) {
+  PH_API_BEGIN
   TRY(ph_step_host_async(m, host_in, host_out, nelem, ncycles, tlim));
   return check_err(m);
+  PH_API_END
 }
 
 ph_status ph_sync(ph_mesh* m) {
+  PH_API_BEGIN
   TRY(need_device(m));
   return check_err(m);
+  PH_API_END
 }
 
 ph_status ph_step_host_async(ph_mesh* m, const double* host_in, double* host_out, int64_t nelem, int32_t ncycles,
                              double tlim) {
+  PH_API_BEGIN
   TRY(need_device(m));
+  // an adaptive mesh may remesh inside ph_step: the local block set (and so the layout of host_out)
+  // would change under the copy-back
+  if (m->cfg.refinement == PH_REF_ADAPTIVE)
+    return fail(PH_ERR_UNSUPPORTED, "ph_step_host on an adaptive mesh: use ph_set_state / ph_step / ph_get_state");
   const Geom& G = m->G;
   int64_t nloc = (int64_t)m->local_gids.size();
   int64_t ni = nloc * NVAR * G.n[0] * G.n[1] * G.n[2];
@@ -1884,16 +1926,20 @@ ph_status ph_step_host_async(ph_mesh* m, const double* host_in, double* host_out
   }
   if (ni) CU(cudaMemcpyAsync(host_out, m->stage_buf, ni * sizeof(double), cudaMemcpyDeviceToHost, m->stream));
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_num_blocks(const ph_mesh* m, int64_t* nglobal, int64_t* nlocal) {
+  PH_API_BEGIN
   if (!m) return fail(PH_ERR_INVALID_ARG, "null mesh");
   if (nglobal) *nglobal = (int64_t)m->blocks.size();
   if (nlocal) *nlocal = (int64_t)m->local_gids.size();
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_get_blocks(const ph_mesh* m, ph_block* out, int64_t cap, int64_t* n) {
+  PH_API_BEGIN
   if (!m || !n) return fail(PH_ERR_INVALID_ARG, "null argument");
   *n = (int64_t)m->blocks.size();
   for (int64_t g = 0; g < *n && g < cap; ++g) {
@@ -1908,9 +1954,11 @@ ph_status ph_get_blocks(const ph_mesh* m, ph_block* out, int64_t cap, int64_t* n
     }
   }
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_get_neighbors(const ph_mesh* m, int64_t gid, ph_neighbor* out, int32_t cap, int32_t* n) {
+  PH_API_BEGIN
   if (!m || !n) return fail(PH_ERR_INVALID_ARG, "null argument");
   if (gid < 0 || gid >= (int64_t)m->blocks.size()) return fail(PH_ERR_INVALID_ARG, "bad gid");
   const BlockInfo& b = m->blocks[gid];
@@ -1925,16 +1973,20 @@ ph_status ph_get_neighbors(const ph_mesh* m, int64_t gid, ph_neighbor* out, int3
     out[q].fine[1] = e.fine[1];
   }
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_get_refine_flags(const ph_mesh* m, int8_t* out, int64_t cap, int64_t* n) {
+  PH_API_BEGIN
   if (!m || !n) return fail(PH_ERR_INVALID_ARG, "null argument");
   *n = (int64_t)m->last_flags.size();
   for (int64_t i = 0; i < *n && i < cap; ++i) out[i] = m->last_flags[i];
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_get_history(const ph_mesh* mc, double* out, int64_t cap_rows, int64_t* nrows) {
+  PH_API_BEGIN
   ph_mesh* m = const_cast<ph_mesh*>(mc);
   TRY(need_device(m));
   TRY(check_err(m));
@@ -1950,9 +2002,11 @@ ph_status ph_get_history(const ph_mesh* mc, double* out, int64_t cap_rows, int64
     for (int c = 0; c < 7; ++c) out[r * 7 + c] = h[q * 7 + c];
   }
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_get_time(const ph_mesh* mc, double* t, double* dt, int64_t* cycle) {
+  PH_API_BEGIN
   ph_mesh* m = const_cast<ph_mesh*>(mc);
   TRY(need_device(m));
   TRY(check_err(m));
@@ -1962,9 +2016,11 @@ ph_status ph_get_time(const ph_mesh* mc, double* t, double* dt, int64_t* cycle) 
   if (dt) *dt = st.dt;
   if (cycle) *cycle = st.cycle;
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_totals(ph_mesh* m, double out[5]) {
+  PH_API_BEGIN
   TRY(need_device(m));
   int nloc = (int)m->local_gids.size();
   if (nloc > 0) {
@@ -1979,9 +2035,11 @@ ph_status ph_totals(ph_mesh* m, double out[5]) {
   TRY(check_err(m));
   CU(cudaMemcpy(out, m->tot5, 5 * sizeof(double), cudaMemcpyDeviceToHost));
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_get_plan_info(const ph_mesh* m, ph_plan_info* out) {
+  PH_API_BEGIN
   if (!m || !out) return fail(PH_ERR_INVALID_ARG, "null argument");
   memset(out, 0, sizeof *out);
   const Plan& PL = m->plan[0];
@@ -2002,16 +2060,20 @@ ph_status ph_get_plan_info(const ph_mesh* m, ph_plan_info* out) {
   out->peer_halo = m->peer ? 1 : 0;
   out->n_cyc_local_tasks = (int64_t)m->plan[1].local.tasks.size();
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_launch_count(const ph_mesh* m, int64_t* n) {
+  PH_API_BEGIN
   if (!m || !n) return fail(PH_ERR_INVALID_ARG, "null argument");
   *n = m->launches;
   return PH_OK;
+  PH_API_END
 }
 
 ph_status ph_kernel_timing(ph_mesh* m, int32_t enable, double* stage_ms, int64_t* stage_launches, double* exch_ms,
                            int64_t* exch_launches) {
+  PH_API_BEGIN
   TRY(need_device(m));
   CU(cudaStreamSynchronize(m->stream));
   double s = 0, x = 0;
@@ -2035,6 +2097,7 @@ ph_status ph_kernel_timing(ph_mesh* m, int32_t enable, double* stage_ms, int64_t
   m->ev_pool.clear();
   m->timing = enable != 0;
   return PH_OK;
+  PH_API_END
 }
 
 }  // extern "C"

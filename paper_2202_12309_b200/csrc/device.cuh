@@ -132,6 +132,7 @@ struct StageArgs {
   // fused peer put (boundary blocks, peer transport): finished cells within g layers of a remote face
   // are also stored into that peer's receive half (M.prank / M.poff); null = off
   double* const* peer_rbuf;
+  int pool_slots;       // slots allocated in the U0 / U1 / H pools (tensor-map extent, stage2.cu)
 };
 
 struct XArgs {
@@ -202,6 +203,10 @@ cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, d
 cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslots, const StageArgs& a, double* W,
                                    double* Fx, double* Fy, double* Fz, const Geom& G, cudaStream_t s);
 size_t stage_smem_bytes();
+// stage2.cu: the round-2 uniform-mesh stage kernel (16 x 16 tiles, bulk-copy plane ring); applies to
+// minmod + Davis on uniform levels with n1, n2 multiples of 16 and nghost 2 (PH_STAGE_V1=1 disables it)
+bool stage2_applies(const Geom& G, int recon, bool ml);
+cudaError_t launch_stage2(bool reduce, bool use_u0, int nctas, const StageArgs& a, const Geom& G, cudaStream_t s);
 // stage-kernel tile (tx x ty columns) for this block extent; true = full-tile (minmod, uniform) path
 bool stage_tile(const Geom& G, int recon, bool ml, int* tx, int* ty);
 

@@ -11,19 +11,11 @@
 #include <cstdlib>
 
 #include "device.cuh"
+#include "point.cuh"
 
 namespace ph {
 
 // ------------------------------------------------------------------------------ point math
-// textbook minmod: same strict sign -> the smaller magnitude, else 0.  The sign test
-// reads only the high words (integer pipe); one DSETP with |.| modifiers picks the magnitude.
-// (+-0 operands give +-0, whose use q +- 0.5*(+-0) == q matches the oracle's 0.)
-__device__ __forceinline__ double minmod_i(double a, double b) {
-  const int ha = __double2hiint(a), hb = __double2hiint(b);
-  const double m = (fabs(a) < fabs(b)) ? a : b;
-  return ((ha ^ hb) >= 0) ? m : 0.0;
-}
-
 // full-tile path: the tile-boundary faces (x face 0 of every row, y face row 0) of planes c+1 and
 // c+2 are computed during plane c's 4th face round by warps that would otherwise wait at the
 // barrier, into a small side buffer; those planes then need 3 face rounds (4/3/3 instead of 4/4/4).
@@ -32,11 +24,6 @@ constexpr int EXTRA_AHEAD = 2;
 __device__ __forceinline__ double ld_plane(const double* p) { return __ldcg(p); }
 // finished cells are stored L2-only (st.global.cg; +0.1 % over plain / .cs stores, which are equal)
 __device__ __forceinline__ void st_cell(double* p, double v) { __stcg(p, v); }
-__device__ __forceinline__ double minmod_pick(double a, double b) { return (fabs(a) < fabs(b)) ? a : b; }
-__device__ __forceinline__ double minmod_half(double a, double b) {
-  return ((__double2hiint(a) ^ __double2hiint(b)) >= 0) ? 0.5 : 0.0;
-}
-
 template <int RECON>
 __device__ __forceinline__ double slope(double dl, double dr) {
   if (RECON == 0) return minmod_i(dl, dr);
@@ -65,37 +52,6 @@ __device__ __forceinline__ void plm_face(double q0, double q1, double q2, double
   wr = fma(-0.5, s2, q2);
 }
 
-// MUFU-seeded reciprocal with one third-order correction: r (1 + e + e^2), e = 1 - x r.  The
-// rcp.approx seed (~2^-23) becomes ~1 ulp in 3 fp64 ops.  The paper fixes no rounding; parity
-// with the oracle's IEEE division is at round-off (A31).
-__device__ __forceinline__ double rcp_nr(double x) {
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
-  const double e = fma(-x, r, 1.0);
-  return fma(r, fma(e, e, e), r);
-}
-
-// MUFU-seeded reciprocal square root with one third-order correction:
-// y (1 + e/2 + 3e^2/8), e = 1 - x y^2 (5 fp64 ops)
-__device__ __forceinline__ double rsqrt_nr(double x) {
-  double y;
-  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-  const double e = fma(-x, y * y, 1.0);
-  return fma(y, e * fma(0.375, e, 0.5), y);
-}
-
-// sound speed c = sqrt(gamma p / rho) = (gamma p) * rsqrt(gamma p rho): one MUFU, no division
-__device__ __forceinline__ double sound_speed(double rho, double p, double gamma) {
-  double gp = gamma * p;
-  return gp * rsqrt_nr(gp * rho);
-}
-
-// min / max as plain compare-selects (DSETP + 2 FSEL).  fmin/fmax carry IEEE NaN semantics that
-// cost a SEL, a predicated LOP3 and register moves per call (+1.3 % on 2b without them); a NaN state
-// is already flagged by the cons->prim positivity check, so only finite operands matter here.
-__device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
-__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
-
 // HLLE in the clamped branch-free form (a4; A4, A5).  w = (rho, u_n, v_t1, v_t2, p).  Wave speeds:
 // Davis (EIN = false), or Einfeldt (EIN = true): the Roe averages (sqrt(rho) weights) of velocity
 // and total enthalpy H = (E + p) / rho give c~^2 = (gamma - 1)(H~ - |v~|^2 / 2), and
@@ -105,9 +61,14 @@ __device__ __forceinline__ void hlle(const double* wl, const double* wr, const G
   double cl = sound_speed(wl[0], wl[4], G.gamma);
   double cr = sound_speed(wr[0], wr[4], G.gamma);
   double mul = wl[0] * wl[1];
-  double El = wl[4] * G.inv_gm1 + (0.5 * wl[0]) * (wl[1] * wl[1] + (wl[2] * wl[2] + wl[3] * wl[3]));
   double mur = wr[0] * wr[1];
+#ifdef PH_STRICT  // strict diagnostic build: p / (gamma - 1) as the oracle writes it
+  double El = wl[4] / G.gm1 + (0.5 * wl[0]) * (wl[1] * wl[1] + (wl[2] * wl[2] + wl[3] * wl[3]));
+  double Er = wr[4] / G.gm1 + (0.5 * wr[0]) * (wr[1] * wr[1] + (wr[2] * wr[2] + wr[3] * wr[3]));
+#else
+  double El = wl[4] * G.inv_gm1 + (0.5 * wl[0]) * (wl[1] * wl[1] + (wl[2] * wl[2] + wl[3] * wl[3]));
   double Er = wr[4] * G.inv_gm1 + (0.5 * wr[0]) * (wr[1] * wr[1] + (wr[2] * wr[2] + wr[3] * wr[3]));
+#endif
   double sl, sr;
   if (EIN) {
     const double rl = wl[0] * rsqrt_nr(wl[0]), rr = wr[0] * rsqrt_nr(wr[0]);  // sqrt(rho)
@@ -135,16 +96,6 @@ __device__ __forceinline__ void hlle(const double* wl, const double* wr, const G
   F[4] = ((bp * ((El + wl[4]) * wl[1]) - bm * ((Er + wr[4]) * wr[1])) + bb * (Er - El)) * inv;
 }
 
-__device__ __forceinline__ void set_error(ErrWord* err, int stage, long long gid, int k, int j, int i) {
-  if (atomicCAS(&err->flag, 0, 1) == 0) {
-    err->stage = stage;
-    err->gid = gid;
-    err->k = k;
-    err->j = j;
-    err->i = i;
-    __threadfence();
-  }
-}
 
 // ---- exact-arithmetic variants (explicitly rounded, the oracle's operation order).  WENO-Z's
 // nonlinear weights and PPM's extremum switch amplify round-off (a smoothness indicator that is 0
@@ -648,9 +599,15 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
       double un[NVAR];
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
+#ifdef PH_STRICT  // strict diagnostic build: the oracle's division by dx
+        double d1 = (sFx[v * FXS + ty * (TX + 1) + tx + 1] - sFx[v * FXS + ty * (TX + 1) + tx]) / M.dx[0];
+        double d2 = (sFy[v * FYS + (ty + 1) * TX + tx] - sFy[v * FYS + ty * TX + tx]) / M.dx[1];
+        double d3 = (fzu[v * FZS] - fzl[v * FZS]) / M.dx[2];
+#else
         double d1 = (sFx[v * FXS + ty * (TX + 1) + tx + 1] - sFx[v * FXS + ty * (TX + 1) + tx]) * idx1;
         double d2 = (sFy[v * FYS + (ty + 1) * TX + tx] - sFy[v * FYS + ty * TX + tx]) * idx2;
         double d3 = (fzu[v * FZS] - fzl[v * FZS]) * idx3;
+#endif
         double L = -((d1 + d2) + d3);
         double out;
         if (HB && USE_U0) {
@@ -748,6 +705,11 @@ size_t stage_smem_bytes() { return stage_smem_bytes_t<TILE_X, TILE_Y>(); }
 // with bounds checks.  Returns whether the full-tile path applies.
 bool stage_tile(const Geom& G, int recon, bool ml, int* tx, int* ty) {
   const bool mm = recon == 0 && !ml && G.wavespeed == 0;  // the Einfeldt variant runs bounds-checked tiles
+  if (stage2_applies(G, recon, ml)) {  // stage2.cu: 16 x 16 tiles
+    *tx = 16;
+    *ty = 16;
+    return true;
+  }
   if (mm && G.n[0] % TILE_X == 0 && G.n[1] % TILE_Y == 0) {
     *tx = TILE_X;
     *ty = TILE_Y;
@@ -920,12 +882,12 @@ __global__ void __launch_bounds__(XT) xfill_kernel(XArgs A, Geom G) {
 // U_c(adjacent cell) += w dt s (F_own - F_corr) / dx, F_corr = pairwise mean of 4 fine fluxes.
 __global__ void reflux_kernel(const RefluxTask* tasks, double* U, const BlockMeta* meta, const double* fbuf,
                               const double* rbuf, const CycleState* st, double w, Geom G) {
-  const RefluxTask t = tasks[blockIdx.y];
+  const RefluxTask t = tasks[blockIdx.x];  // tasks on x: up to 2^31 - 1
   const int d = t.dir;
   const int ta = (d == 0) ? 1 : 0, tb = (d == 2) ? 1 : 2;  // tangential dims, increasing
   const int na = G.n[ta], nb = G.n[tb];
   const int qa = na / 2, qb = nb / 2;
-  const int idxc = blockIdx.x * blockDim.x + threadIdx.x;
+  const int idxc = blockIdx.y * blockDim.x + threadIdx.x;
   if (idxc >= qa * qb) return;
   const int A0 = idxc % qa, B0 = idxc / qa;
   const int Ac = t.t0lo + A0, Bc = t.t1lo + B0;
@@ -957,12 +919,12 @@ __global__ void reflux_kernel(const RefluxTask* tasks, double* U, const BlockMet
 }
 
 __global__ void flux_pack_kernel(const FluxPackTask* tasks, const double* fbuf, double* sbuf, Geom G) {
-  const FluxPackTask t = tasks[blockIdx.y];
+  const FluxPackTask t = tasks[blockIdx.x];
   const int d = t.dir;
   const int ta = (d == 0) ? 1 : 0, tb = (d == 2) ? 1 : 2;
   const int na = G.n[ta], nb = G.n[tb];
   const int qa = na / 2, qb = nb / 2;
-  const int idxc = blockIdx.x * blockDim.x + threadIdx.x;
+  const int idxc = blockIdx.y * blockDim.x + threadIdx.x;
   if (idxc >= qa * qb) return;
   const int A0 = idxc % qa, B0 = idxc / qa;
   const int a0 = 2 * A0, b0 = 2 * B0;
@@ -1685,8 +1647,8 @@ int tag_ctas_per_block(const Geom& G) { return ((G.n[0] + TGX - 1) / TGX) * ((G.
 // siblings (A10) -- optionally through the migration buffers
 __global__ void remesh_kernel(const RemeshTask* tasks, const double* Uold, double* Unew, const double* rbuf,
                               double* sbuf, Geom G) {
-  const RemeshTask t = tasks[blockIdx.y];
-  const int k = blockIdx.x;
+  const RemeshTask t = tasks[blockIdx.x];  // tasks on x: up to 2^31 - 1
+  const int k = blockIdx.y;
   const bool oct = (t.kind == R_OCT || t.kind == R_OCTCOPY);
   const int e0 = oct ? G.nc[0] : G.n[0], e1 = oct ? G.nc[1] : G.n[1], e2 = oct ? G.nc[2] : G.n[2];
   if (k >= e2) return;
@@ -1778,6 +1740,7 @@ static cudaError_t launch_stage_ml(bool ml, int n, const StageArgs& a, const Geo
   const bool full = stage_tile(G, R, ml, &tx, &ty);
   if (a.H && !full) return cudaErrorInvalidValue;  // the host enables H only where the full-tile path runs
   if (a.peer_rbuf && !full) return cudaErrorInvalidValue;  // the host fuses the put only on full tiles
+  if (full && tx == 16 && a.H && !a.peer_rbuf && stage2_applies(G, R, ml)) return launch_stage2(RD, U0, n, a, G, s);
   if (full && tx == 16) {
     if (a.peer_rbuf)
       return a.H ? launch_stage_t<0, RD, U0, false, true, true, 16, 16, false, true>(n, a, G, s)
@@ -1892,7 +1855,7 @@ static int max_quarter(const Geom& G) {
 cudaError_t launch_reflux(int ntasks, const RefluxTask* t, double* U, const BlockMeta* meta, const double* fbuf,
                           const double* rbuf, const CycleState* st, double w, const Geom& G, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
-  dim3 grid((max_quarter(G) + 127) / 128, ntasks);
+  dim3 grid(ntasks, (max_quarter(G) + 127) / 128);
   reflux_kernel<<<grid, 128, 0, s>>>(t, U, meta, fbuf, rbuf, st, w, G);
   return PH_CHECK_LAUNCH();
 }
@@ -1900,7 +1863,7 @@ cudaError_t launch_reflux(int ntasks, const RefluxTask* t, double* U, const Bloc
 cudaError_t launch_flux_pack(int ntasks, const FluxPackTask* t, const double* fbuf, double* sbuf, const Geom& G,
                              cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
-  dim3 grid((max_quarter(G) + 127) / 128, ntasks);
+  dim3 grid(ntasks, (max_quarter(G) + 127) / 128);
   flux_pack_kernel<<<grid, 128, 0, s>>>(t, fbuf, sbuf, G);
   return PH_CHECK_LAUNCH();
 }
@@ -2024,7 +1987,7 @@ cudaError_t launch_tag(const double* U, const BlockMeta* meta, int nslots, unsig
 cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, double* Unew, const double* rbuf,
                           double* sbuf, const Geom& G, cudaStream_t s) {
   if (ntasks <= 0) return cudaSuccess;
-  dim3 grid(G.n[2], ntasks);
+  dim3 grid(ntasks, G.n[2]);
   remesh_kernel<<<grid, 128, 0, s>>>(t, Uold, Unew, rbuf, sbuf, G);
   return cudaGetLastError();
 }

@@ -1,0 +1,69 @@
+// point.cuh -- pointwise fp64 device math shared by the stage kernels (kernels.cu, stage2.cu).
+// Product code only; nothing here is shared with oracle/.
+#pragma once
+#include "device.cuh"
+
+namespace ph {
+// textbook minmod: same strict sign -> the smaller magnitude, else 0.  The sign test
+// reads only the high words (integer pipe); one DSETP with |.| modifiers picks the magnitude.
+// (+-0 operands give +-0, whose use q +- 0.5*(+-0) == q matches the oracle's 0.)
+__device__ __forceinline__ double minmod_i(double a, double b) {
+  const int ha = __double2hiint(a), hb = __double2hiint(b);
+  const double m = (fabs(a) < fabs(b)) ? a : b;
+  return ((ha ^ hb) >= 0) ? m : 0.0;
+}
+
+__device__ __forceinline__ double minmod_pick(double a, double b) { return (fabs(a) < fabs(b)) ? a : b; }
+__device__ __forceinline__ double minmod_half(double a, double b) {
+  return ((__double2hiint(a) ^ __double2hiint(b)) >= 0) ? 0.5 : 0.0;
+}
+
+// MUFU-seeded reciprocal with one third-order correction: r (1 + e + e^2), e = 1 - x r.  The
+// rcp.approx seed (~2^-23) becomes ~1 ulp in 3 fp64 ops.  The paper fixes no rounding; parity
+// with the oracle's IEEE division is at round-off (A31).
+__device__ __forceinline__ double rcp_nr(double x) {
+#ifdef PH_STRICT  // strict diagnostic build: IEEE division as in the oracle
+  return 1.0 / x;
+#endif
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
+// MUFU-seeded reciprocal square root with one third-order correction:
+// y (1 + e/2 + 3e^2/8), e = 1 - x y^2 (5 fp64 ops)
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double e = fma(-x, y * y, 1.0);
+  return fma(y, e * fma(0.375, e, 0.5), y);
+}
+
+// sound speed c = sqrt(gamma p / rho) = (gamma p) * rsqrt(gamma p rho): one MUFU, no division
+__device__ __forceinline__ double sound_speed(double rho, double p, double gamma) {
+#ifdef PH_STRICT  // strict diagnostic build: c = sqrt(gamma p / rho), IEEE ops (O5)
+  return sqrt(gamma * p / rho);
+#endif
+  double gp = gamma * p;
+  return gp * rsqrt_nr(gp * rho);
+}
+
+// min / max as plain compare-selects (DSETP + 2 FSEL).  fmin/fmax carry IEEE NaN semantics that
+// cost a SEL, a predicated LOP3 and register moves per call (+1.3 % on 2b without them); a NaN state
+// is already flagged by the cons->prim positivity check, so only finite operands matter here.
+__device__ __forceinline__ double dmin(double a, double b) { return a < b ? a : b; }
+__device__ __forceinline__ double dmax(double a, double b) { return a > b ? a : b; }
+
+__device__ __forceinline__ void set_error(ErrWord* err, int stage, long long gid, int k, int j, int i) {
+  if (atomicCAS(&err->flag, 0, 1) == 0) {
+    err->stage = stage;
+    err->gid = gid;
+    err->k = k;
+    err->j = j;
+    err->i = i;
+    __threadfence();
+  }
+}
+
+}  // namespace ph

@@ -308,20 +308,39 @@ class Mesh:
         _check(lib().ph_step(self._h, ncycles, tlim, None))
         return None
 
+    @staticmethod
+    def _host_pair(host_in, host_out, pinned):
+        """Both buffers: contiguous float64 of the same size (torch CPU tensors or numpy arrays);
+        pinned=True (the async form) also requires page-locked torch tensors."""
+        def info(x):
+            if hasattr(x, "data_ptr"):
+                import torch
+                if x.device.type != "cpu" or x.dtype != torch.float64 or not x.is_contiguous():
+                    raise ValueError("host buffers must be contiguous float64 CPU tensors")
+                if pinned and not x.is_pinned():
+                    raise ValueError("step_host_async needs pinned host buffers (tensor.pin_memory())")
+                return x.data_ptr(), x.numel()
+            a = np.asarray(x)
+            if a.dtype != np.float64 or not a.flags["C_CONTIGUOUS"]:
+                raise ValueError("host buffers must be C-contiguous float64 arrays")
+            if pinned:
+                raise ValueError("step_host_async needs pinned torch tensors, not numpy arrays")
+            return a.ctypes.data, a.size
+        pi, ni = info(host_in)
+        po, no = info(host_out)
+        if ni != no:
+            raise ValueError(f"host_in has {ni} elements, host_out {no}")
+        return pi, po, ni
+
     def step_host(self, host_in, host_out, ncycles, tlim=0.0):
         """End-to-end call with host buffers ([nlocal][5][n3][n2][n1]); pinned torch tensors or numpy."""
-        def ptr(x):
-            return x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data
-        n = host_in.numel() if hasattr(host_in, "numel") else host_in.size
-        _check(lib().ph_step_host(self._h, C.c_void_p(ptr(host_in)), C.c_void_p(ptr(host_out)), n, ncycles, tlim))
+        pi, po, n = self._host_pair(host_in, host_out, pinned=False)
+        _check(lib().ph_step_host(self._h, C.c_void_p(pi), C.c_void_p(po), n, ncycles, tlim))
 
     def step_host_async(self, host_in, host_out, ncycles, tlim=0.0):
         """Enqueue step_host on the mesh's stream and return (pinned buffers; call sync())."""
-        def ptr(x):
-            return x.data_ptr() if hasattr(x, "data_ptr") else x.ctypes.data
-        n = host_in.numel() if hasattr(host_in, "numel") else host_in.size
-        _check(lib().ph_step_host_async(self._h, C.c_void_p(ptr(host_in)), C.c_void_p(ptr(host_out)), n, ncycles,
-                                        tlim))
+        pi, po, n = self._host_pair(host_in, host_out, pinned=True)
+        _check(lib().ph_step_host_async(self._h, C.c_void_p(pi), C.c_void_p(po), n, ncycles, tlim))
 
     def sync(self):
         _check(lib().ph_sync(self._h))

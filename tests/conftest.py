@@ -13,6 +13,17 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: long CPU test")
 
 
+def pytest_collection_modifyitems(config, items):
+    # slow CPU pins (minutes of oracle time) run only with PH_SLOW=1; their last results are
+    # recorded under profiles/ (reading A42)
+    if os.environ.get("PH_SLOW") == "1":
+        return
+    skip = pytest.mark.skip(reason="slow CPU pin: set PH_SLOW=1")
+    for it in items:
+        if "slow" in it.keywords:
+            it.add_marker(skip)
+
+
 @pytest.fixture(scope="session")
 def oracle_mod():
     import oracle

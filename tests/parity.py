@@ -6,6 +6,9 @@ sqrt(rho E) ~ rho c is the momentum scale at which the momentum equation's round
 its flux carries p ~ rho c^2, so reordering the arithmetic moves momentum by ~1e-16 * rho c even
 where the momentum itself is tiny (the linear wave has |m| ~ A = 1e-6; Sod has m2 = m3 = 0).
 """
+import json
+import os
+
 import numpy as np
 
 TOL = 1e-12  # north_star: max relative error 1e-12 per cell after 10 cycles
@@ -35,9 +38,33 @@ def errors(g, o):
     return out
 
 
+def diagnostics(g, o):
+    """c.3's extra report per variable: the un-floored max relative error |g - o| / |o| over cells with
+    o != 0 (and how many cells have o == 0 but g != 0), and the max absolute error."""
+    g = np.asarray(g)
+    o = np.asarray(o)
+    if o.ndim == 4:
+        g, o = g[None], o[None]
+    out = {}
+    for v in range(5):
+        gv, ov = g[:, v], o[:, v]
+        d = np.abs(gv - ov)
+        nz = ov != 0
+        out[v] = {"rel_unfloored": float(np.max(d[nz] / np.abs(ov[nz]))) if nz.any() else 0.0,
+                  "zero_ref_nonzero_gpu": int(np.count_nonzero(d[~nz])),
+                  "abs": float(d.max()) if d.size else 0.0}
+    return out
+
+
 def assert_parity(g, o, tol=TOL):
     e = errors(g, o)
-    assert max(e.values()) <= tol, e
+    diag = diagnostics(g, o)
+    log = os.environ.get("PH_PARITY_LOG")
+    if log:
+        with open(log, "a") as f:
+            f.write(json.dumps({"test": os.environ.get("PYTEST_CURRENT_TEST", "?"), "metric": e, "diag": diag}) + "\n")
+    print("parity", {v: (e[v], diag[v]["rel_unfloored"], diag[v]["abs"]) for v in range(5)})
+    assert max(e.values()) <= tol, (e, diag)
     return e
 
 

@@ -133,6 +133,21 @@ def test_static_two_level_blast_with_flux_correction(oracle_mod, P):
     assert abs(t1[0] - t0[0]) <= 1e-12 * t0[0] and abs(t1[4] - t0[4]) <= 1e-12 * t0[4]
 
 
+def test_static_multilevel_32cube_blocks_next1_path(oracle_mod, P):
+    """The NEXT 1 (paper mesh) code path at a size the oracle finishes in seconds: exactly tiling 32^3
+    blocks on a static 3-level mesh take the full-tile multilevel stage kernel with the fused dt /
+    totals reduction and rfx_reduce_kernel (the corrected face layers reduced after the reflux)."""
+    kw = dict(mesh_nx=(128, 128, 128), block_nx=(32, 32, 32), xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=2,
+              refinement=P.REF_STATIC, regions=[(2, -0.12, 0.12, -0.12, 0.12, -0.12, 0.12)])
+    o, g = _run_both(oracle_mod, P, P.BLAST, [10.0, 0.1, 0.1], 5, **kw)
+    levels = [b["level"] for b in g.blocks()]
+    assert set(levels) == {0, 1, 2}, sorted(set(levels))
+    _check_run(o, g)
+    t0 = g.history()[0, 2:]
+    t1 = g.totals()
+    assert abs(t1[0] - t0[0]) <= 1e-12 * t0[0] and abs(t1[4] - t0[4]) <= 1e-12 * t0[4]
+
+
 def test_three_level_outflow_sod_like(oracle_mod, P):
     kw = dict(mesh_nx=(32, 16, 16), block_nx=(8, 8, 8), max_level=2, refinement=P.REF_STATIC, gamma=1.4,
               regions=[(2, 0.45, 0.55, 0.2, 0.6, 0.3, 0.7)], bc_inner=(1, 1, 2), bc_outer=(1, 2, 1))
@@ -284,3 +299,42 @@ def test_high_order_blast_and_sod(oracle_mod, P, recon, nseg, monkeypatch):
     o, g = _run_both(oracle_mod, P, P.SOD, [0.5], 100000, tlim=0.1, **kw)
     _check_run(o, g)
     assert np.array_equal(gather(g), gather(o)) and g.time() == o.time()
+
+
+_STRICT_SCRIPT = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, 'tests')
+import paper_2202_12309_b200 as P
+import oracle as O
+from parity import diagnostics, gather
+kw = dict(mesh_nx=(32, 32, 32), block_nx=(32, 32, 32))
+g, o = P.Mesh(device=0, **kw), O.Mesh(**kw)
+for m in (g, o):
+    m.set_problem(P.LINEAR_WAVE, [1e-6, 1, 1, 1])
+    m.step(10)
+print(json.dumps({"diag": diagnostics(gather(g), gather(o)), "dt": [g.time()[1], o.time()[1]]}))
+"""
+
+
+def test_strict_build_config1_unfloored(oracle_mod, P):
+    """SURVEY §8(c) c.3 strict diagnostic build: no FMA contraction, IEEE division / square root and
+    the oracle's division by dx (the round-1 stage kernel with the general RK finish).  Config 1's
+    fluxes then agree with the oracle's to the last bit or two, so every variable -- the momenta
+    included -- meets 1e-12 *without* the momentum floor of reading A27' (un-floored |g-o|/|o|)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from paper_2202_12309_b200 import _build
+    lib = _build.build_strict()
+    env = dict(os.environ, PH_LIB=lib, PH_STAGE_V1="1", PH_NO_HBASE="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, "-c", _STRICT_SCRIPT], cwd=root, env=env, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    print("strict config 1:", res)
+    for v, d in res["diag"].items():
+        assert d["rel_unfloored"] <= 1e-12 and d["zero_ref_nonzero_gpu"] == 0, (v, d)
+    assert abs(res["dt"][0] - res["dt"][1]) <= 1e-14 * res["dt"][1]

@@ -238,3 +238,66 @@ def test_refinement_indicator_closed_form_on_a_linear_pressure(oracle_mod, axis)
     for b in m.blocks():
         want = d / (p0 + d * first[b["lx"][axis]])
         assert abs(eps[b["gid"]] - want) <= 1e-13 * want, (b, eps[b["gid"]], want)
+
+
+# ------------------------------------------------------------------ method of images (bc_coarse pin)
+def _mirror_pair(O, nlev, cycles, rng_seed):
+    """A: [0,1] x [0,1]^2, reflecting walls in x1 (A9), periodic x2/x3, level jumps that touch
+    the x1 = 0 wall.  B: [-1,1] x [0,1]^2 fully periodic with the mirror image of A's state and
+    regions on x1 < 0.  A reflecting wall is a mirror plane, so A must equal B's x1 >= 0 half
+    bitwise: the fine-ghost BCs, the coarse-staging BCs (bc_coarse, O7-B) and the staging geometry
+    at walls (A12) are pinned by the periodic exchange, which never applies a physical BC."""
+    L = nlev
+    regA = [(L, 0.0, 0.2, 0.3, 0.7, 0.2, 0.6), (1, 0.7, 1.0, 0.0, 0.3, 0.5, 0.9)]
+    regB = list(regA) + [(r[0], -r[2], -r[1], *r[3:]) for r in regA]
+    n = 8
+    A = O.Mesh(mesh_nx=(16, 16, 16), block_nx=(n,) * 3, max_level=L, refinement=O.REF_STATIC, regions=regA,
+               bc_inner=(O.REFLECT, O.PERIODIC, O.PERIODIC), bc_outer=(O.REFLECT, O.PERIODIC, O.PERIODIC))
+    B = O.Mesh(mesh_nx=(32, 16, 16), block_nx=(n,) * 3, xmin=(-1.0, 0.0, 0.0), xmax=(1.0, 1.0, 1.0),
+               max_level=L, refinement=O.REF_STATIC, regions=regB)
+    assert max(b["level"] for b in A.blocks()) == L
+    rng = np.random.default_rng(rng_seed)
+    bA = {(b["level"], b["lx"]): b["gid"] for b in A.blocks()}
+    bB = {(b["level"], b["lx"]): b["gid"] for b in B.blocks()}
+    assert len(bB) == 2 * len(bA)
+    for (lev, (i, j, k)), gid in bA.items():
+        W = np.stack([1.0 + 0.4 * rng.random((n, n, n)), 0.3 * rng.standard_normal((n, n, n)),
+                      0.3 * rng.standard_normal((n, n, n)), 0.3 * rng.standard_normal((n, n, n)),
+                      1.0 + 0.4 * rng.random((n, n, n))])
+        U = np.stack([W[0], W[0] * W[1], W[0] * W[2], W[0] * W[3],
+                      W[4] / (5 / 3 - 1) + 0.5 * W[0] * (W[1] ** 2 + W[2] ** 2 + W[3] ** 2)])
+        A.set_state(gid, U)
+        nx = 2 * 2 ** lev  # root blocks of A along x1 at this level
+        B.set_state(bB[(lev, (i + nx, j, k))], U)
+        M = U[:, :, :, ::-1].copy()
+        M[1] *= -1.0
+        B.set_state(bB[(lev, (nx - 1 - i, j, k))], M)
+    for m in (A, B):
+        m.exchange()
+        m.compute_dt()
+    assert A.compute_dt() == B.compute_dt()
+    A.step(cycles)
+    B.step(cycles)
+    return A, B, bA, bB
+
+
+@pytest.mark.parametrize("nlev", [1, 2])
+def test_reflecting_wall_equals_mirrored_periodic_domain(oracle_mod, nlev):
+    O = oracle_mod
+    A, B, bA, bB = _mirror_pair(O, nlev, 4, 11 + nlev)
+    for (lev, (i, j, k)), gid in bA.items():
+        a = A.get_state(gid)
+        b = B.get_state(bB[(lev, (i + 2 * 2 ** lev, j, k))])
+        assert np.array_equal(a, b), (lev, i, j, k, float(np.abs(a - b).max()))
+    assert A.time() == B.time()
+
+
+def test_reflecting_wall_ghosts_equal_mirrored_interior(oracle_mod):
+    """Right after an exchange, every ghost of A (fine ghosts at the wall and those prolongated from
+    coarse staging that reaches the wall) equals the corresponding cell of B."""
+    O = oracle_mod
+    A, B, bA, bB = _mirror_pair(O, 2, 0, 5)
+    for (lev, (i, j, k)), gid in bA.items():
+        a = A.get_state_full(gid)
+        b = B.get_state_full(bB[(lev, (i + 2 * 2 ** lev, j, k))])
+        assert np.array_equal(a, b), (lev, i, j, k, float(np.abs(a - b).max()))

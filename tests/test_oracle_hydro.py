@@ -167,6 +167,17 @@ def test_linear_wave_oblique_3d_second_order(oracle_mod):
     assert r[0] >= 2.1 and r[1] >= 2.4 and r[1] > r[0], (e, r)
 
 
+@pytest.mark.slow
+def test_linear_wave_oblique_3d_second_order_cpin(oracle_mod):
+    """SURVEY C-PIN as written: oblique (1,1,1) 3D wave, minmod, N = 32/64/128, ratios >= 2.4 then
+    >= 2.9 (SURVEY measured 2.56, 3.11).  ~2 min of oracle time on 8 cores, so it runs with
+    PH_SLOW=1; the fast test above checks the same convergence at N = 16/32/64 (reading A42)."""
+    e = [_wave_l1(oracle_mod, N, (1, 1, 1), False) for N in (32, 64, 128)]
+    r = [e[0] / e[1], e[1] / e[2]]
+    print("oblique C-PIN", e, r)
+    assert r[0] >= 2.4 and r[1] >= 2.9, (e, r)
+
+
 def test_linear_wave_vl2_second_order_and_close_to_rk2(oracle_mod):
     """VL2 (NEXT 2): second order in space and time on the aligned wave; with the same PLM in both
     stages its error is within a few percent of RK2's (the SURVEY prototype: 0.5 %)"""

@@ -41,23 +41,13 @@ CASES = {
 }
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--case", default="blast")
-    ap.add_argument("--halo", default="auto", choices=["auto", "nccl", "peer"])
-    ap.add_argument("--cycles", type=int, default=0, help="override the case's cycle count (soak runs)")
-    a = ap.parse_args()
+def run_case(P, case, halo, cycles, rank, world, local):
     import numpy as np
-    import torch
     import torch.distributed as dist
-    import paper_2202_12309_b200 as P
-    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    C = dict(CASES[a.case])
-    if a.cycles > 0:
-        C["cycles"] = a.cycles
-    transport = {"auto": P.HALO_AUTO, "nccl": P.HALO_NCCL, "peer": P.HALO_PEER}[a.halo]
+    C = dict(CASES[case])
+    if cycles > 0:
+        C["cycles"] = cycles
+    transport = {"auto": P.HALO_AUTO, "nccl": P.HALO_NCCL, "peer": P.HALO_PEER}[halo]
     m = P.Mesh(device=local, rank=rank, nranks=world, halo_transport=transport, **C["kw"])
     m.set_problem(C["problem"], C["params"])
     m.step(C["cycles"])
@@ -84,21 +74,45 @@ def main():
         single.set_problem(C["problem"], C["params"])
         single.step(C["cycles"])
         S = np.stack([single.get_state(g) for g in range(single.num_blocks())])
+        single.close()
         bitwise = bool(S.shape == G.shape and np.array_equal(S, G))
         same_mesh = [(b["gid"], b["level"], b["lx"]) for b in orc.blocks()] == \
             [(b["gid"], b["level"], b["lx"]) for b in m.blocks()]
         to = orc.time()
         ho = orc.history()
-        res = dict(case=a.case, world=world, parity=e, max_err=max(e.values()), bitwise_vs_1gpu=bitwise,
+        res = dict(case=case, world=world, parity=e, max_err=max(e.values()), bitwise_vs_1gpu=bitwise,
                    same_mesh=same_mesh, nblocks=len(allb),
                    t=tm, t_oracle=to, dt_rel=abs(tm[1] - to[1]) / to[1],
                    mass_rel=float(abs(hist[-1, 2] - ho[-1, 2]) / ho[-1, 2]),
-                   send_doubles=info["send_doubles_to"], halo=a.halo, peer_halo=info["peer_halo"])
+                   send_doubles=info["send_doubles_to"], halo=halo, peer_halo=info["peer_halo"])
         ok = res["max_err"] <= 1e-12 and bitwise and same_mesh and res["dt_rel"] <= 1e-12 and tm[2] == to[2]
-        ok = ok and (info["peer_halo"] == (a.halo == "peer") or a.halo == "auto")
+        ok = ok and (info["peer_halo"] == (halo == "peer") or halo == "auto")
         res["ok"] = ok
         print("MULTI_CHECK " + json.dumps(res), flush=True)
     m.close()
+    return ok
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--case", default="blast")
+    ap.add_argument("--halo", default="auto", choices=["auto", "nccl", "peer"])
+    ap.add_argument("--cases", default="",
+                    help="comma-separated case:halo list run in this one process group (one torchrun start "
+                         "for many cases); overrides --case / --halo")
+    ap.add_argument("--cycles", type=int, default=0, help="override the case's cycle count (soak runs)")
+    a = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+    import paper_2202_12309_b200 as P
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    todo = [tuple(c.split(":")) for c in a.cases.split(",") if c] or [(a.case, a.halo)]
+    ok = True
+    for case, halo in todo:
+        ok = run_case(P, case, halo, a.cycles, rank, world, local) and ok
+        dist.barrier()
     dist.destroy_process_group()
     sys.exit(0 if ok else 1)
 
