@@ -343,8 +343,13 @@ def run_ours(args):
         try:
             cnt = json.load(open(pc))
             per_cell = float(cnt["fp64_inst_per_cell_stage"])
-            lanes = max(json.loads(l)["lane_ops_per_clk_per_sm"] for l in open(pu)
-                        if l.startswith("{\"op\": \"d") and "+" not in json.loads(l)["op"])
+            rows = []
+            for l in open(pu):
+                try:
+                    rows.append(json.loads(l))
+                except ValueError:  # a non-finite entry (the optimised-away dsetp probe)
+                    continue
+            lanes = max(r["lane_ops_per_clk_per_sm"] for r in rows if r.get("op") in ("dfma", "dadd", "dmul"))
             mhz = (clocks or {}).get("sm_mhz") or 1965.0
             ach = per_cell * nloc_cells * 2 * args.steps / (stage_ms * 1e-3)  # all timed stage launches
             fpk = 148 * lanes * mhz * 1e6

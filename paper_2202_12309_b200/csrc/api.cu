@@ -679,7 +679,11 @@ static ph_status setup_device(ph_mesh* m) {
   // stage-2 base pool: on the uniform full-tile minmod path (the kernels' H template), not under
   // flux correction (it would also have to correct H) nor AMR
   m->Hpool = nullptr;
-  if (!m->ho && !m->multilevel && m->cfg.refinement != PH_REF_ADAPTIVE && full_tile && !getenv("PH_NO_HBASE"))
+  // stage2.cu needs H (also on multilevel / AMR meshes, where the reflux corrects H with U^1); the round-1
+  // kernel (PH_STAGE_V1=1) has no H on multilevel meshes
+  const bool s2 = stage2_applies(G, m->cfg.recon, m->fbuf != nullptr);
+  if (!m->ho && full_tile && !getenv("PH_NO_HBASE") &&
+      (s2 || (!m->multilevel && m->cfg.refinement != PH_REF_ADAPTIVE)))
     TRY(dalloc(m, (void**)&m->Hpool, (size_t)std::max<int64_t>(nloc, 1) * G.bstride * sizeof(double)));
   m->partials_n = std::max<int64_t>({(int64_t)m->stage_ctas + (int64_t)m->rfx_faces.size(), nloc * G.n[2],
                                       nloc * tag_ctas_per_block(G), 1});
@@ -1096,8 +1100,11 @@ static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a
     }
     for (int d = 0; d < 3; ++d) {
       if (m->reflux[d].empty()) continue;
+      // stage 1 on the H path: H = ha0 U^n + hb1 U^1 must see the corrected U^1
+      const bool fixH = m->Hpool && Uout == m->U1;
+      const double hb1 = m->cfg.integrator == PH_INT_VL2 ? 0.0 : 0.5;
       CU(launch_reflux((int)m->reflux[d].size(), m->d_reflux[d], Uout, m->d_meta, m->fbuf, m->frbuf, m->d_st, cdt,
-                       m->G, m->stream));
+                       m->G, m->stream, fixH ? m->Hpool : nullptr, hb1));
       m->launches++;
     }
   }

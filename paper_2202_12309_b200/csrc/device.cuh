@@ -176,7 +176,8 @@ cudaError_t launch_peer_wait(const unsigned long long* my_flags, unsigned long l
                              ErrWord* err, cudaStream_t s);
 cudaError_t launch_xfill(int nchunks, const XArgs& a, const Geom& G, cudaStream_t s);
 cudaError_t launch_reflux(int ntasks, const RefluxTask* t, double* U, const BlockMeta* meta, const double* fbuf,
-                          const double* rbuf, const CycleState* st, double w, const Geom& G, cudaStream_t s);
+                          const double* rbuf, const CycleState* st, double w, const Geom& G, cudaStream_t s,
+                          double* H = nullptr, double hb1 = 0.0);
 cudaError_t launch_flux_pack(int ntasks, const FluxPackTask* t, const double* fbuf, double* sbuf, const Geom& G,
                              cudaStream_t s);
 cudaError_t launch_pgen(double* U, const BlockMeta* meta, int nslots, const PgenArgs& P, const Geom& G,

@@ -881,7 +881,7 @@ __global__ void __launch_bounds__(XT) xfill_kernel(XArgs A, Geom G) {
 // ------------------------------------------------------------------------------ reflux (O8 / a8)
 // U_c(adjacent cell) += w dt s (F_own - F_corr) / dx, F_corr = pairwise mean of 4 fine fluxes.
 __global__ void reflux_kernel(const RefluxTask* tasks, double* U, const BlockMeta* meta, const double* fbuf,
-                              const double* rbuf, const CycleState* st, double w, Geom G) {
+                              const double* rbuf, const CycleState* st, double w, Geom G, double* H, double hb1) {
   const RefluxTask t = tasks[blockIdx.x];  // tasks on x: up to 2^31 - 1
   const int d = t.dir;
   const int ta = (d == 0) ? 1 : 0, tb = (d == 2) ? 1 : 2;  // tangential dims, increasing
@@ -914,7 +914,10 @@ __global__ void reflux_kernel(const RefluxTask* tasks, double* U, const BlockMet
       corr = ((f00 + f10) + (f01 + f11)) * 0.25;
     }
     double own = cf[v * fst + (int64_t)Bc * na + Ac];
-    u[v * G.vstride] += fac * (own - corr);
+    const double du = fac * (own - corr);
+    u[v * G.vstride] += du;
+    // stage 1 on the H path: the stage-2 base H = ha0 U^n + hb1 U^1 follows the corrected U^1
+    if (H) H[(u - U) + v * G.vstride] += hb1 * du;
   }
 }
 
@@ -1740,7 +1743,8 @@ static cudaError_t launch_stage_ml(bool ml, int n, const StageArgs& a, const Geo
   const bool full = stage_tile(G, R, ml, &tx, &ty);
   if (a.H && !full) return cudaErrorInvalidValue;  // the host enables H only where the full-tile path runs
   if (a.peer_rbuf && !full) return cudaErrorInvalidValue;  // the host fuses the put only on full tiles
-  if (full && tx == 16 && a.H && !a.peer_rbuf && stage2_applies(G, R, ml)) return launch_stage2(RD, U0, n, a, G, s);
+  if (full && tx == 16 && a.H && stage2_applies(G, R, ml)) return launch_stage2(RD, U0, n, a, G, s);
+  if (ml && full && tx == 16) return cudaErrorInvalidValue;  // 16 x 16 multilevel tiles exist only in stage2
   if (full && tx == 16) {
     if (a.peer_rbuf)
       return a.H ? launch_stage_t<0, RD, U0, false, true, true, 16, 16, false, true>(n, a, G, s)
@@ -1853,10 +1857,11 @@ static int max_quarter(const Geom& G) {
 }
 
 cudaError_t launch_reflux(int ntasks, const RefluxTask* t, double* U, const BlockMeta* meta, const double* fbuf,
-                          const double* rbuf, const CycleState* st, double w, const Geom& G, cudaStream_t s) {
+                          const double* rbuf, const CycleState* st, double w, const Geom& G, cudaStream_t s,
+                          double* H, double hb1) {
   if (ntasks <= 0) return cudaSuccess;
   dim3 grid(ntasks, (max_quarter(G) + 127) / 128);
-  reflux_kernel<<<grid, 128, 0, s>>>(t, U, meta, fbuf, rbuf, st, w, G);
+  reflux_kernel<<<grid, 128, 0, s>>>(t, U, meta, fbuf, rbuf, st, w, G, H, hb1);
   return PH_CHECK_LAUNCH();
 }
 

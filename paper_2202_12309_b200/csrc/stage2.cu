@@ -145,6 +145,54 @@ __device__ __forceinline__ void hlle_ab(const double* wl, const double* wr, doub
   F[4] = fma(hl, btl, fma(hr, btr, e * (pl - pr)));
 }
 
+// two faces at once (the pair's two columns / faces): the same arithmetic as hlle_ab, written so
+// the two dependency chains interleave (PH_S2_X2 A/B knob; default: two hlle_ab calls)
+template <int N>
+__device__ __forceinline__ void hlle_ab2(const double (&wl)[2][NVAR], const double (&wr)[2][NVAR], double gamma,
+                                         double ggm1, double (&F)[2][NVAR]) {
+#ifdef PH_S2_X2
+  constexpr int T1 = N == 1 ? 2 : (N == 2 ? 3 : 1), T2 = N == 1 ? 3 : (N == 2 ? 1 : 2);
+  double cl[2], cr[2], bp[2], bm[2], inv[2], a[2], b[2], e[2], btl[2], btr[2], al[2], ar[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    cl[k] = sound_speed(wl[k][0], wl[k][4], gamma);
+    cr[k] = sound_speed(wr[k][0], wr[k][4], gamma);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double ul = wl[k][N], ur = wr[k][N];
+    bp[k] = pos_part(dmax(ul + cl[k], ur + cr[k]));
+    bm[k] = neg_part(dmin(ul - cl[k], ur - cr[k]));
+    inv[k] = rcp_nr(bp[k] - bm[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    a[k] = bp[k] * inv[k];
+    b[k] = -bm[k] * inv[k];
+    e[k] = a[k] * bm[k];
+    btl[k] = fma(a[k], wl[k][N], -e[k]);
+    btr[k] = fma(b[k], wr[k][N], e[k]);
+    al[k] = wl[k][0] * btl[k];
+    ar[k] = wr[k][0] * btr[k];
+  }
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const double ul = wl[k][N], ur = wr[k][N], pl = wl[k][4], pr = wr[k][4];
+    F[k][0] = al[k] + ar[k];
+    F[k][N] = fma(ul, al[k], fma(ur, ar[k], fma(a[k], pl, b[k] * pr)));
+    F[k][T1] = fma(wl[k][T1], al[k], wr[k][T1] * ar[k]);
+    F[k][T2] = fma(wl[k][T2], al[k], wr[k][T2] * ar[k]);
+    const double kl = fma(ul, ul, fma(wl[k][T1], wl[k][T1], wl[k][T2] * wl[k][T2]));
+    const double kr = fma(ur, ur, fma(wr[k][T1], wr[k][T1], wr[k][T2] * wr[k][T2]));
+    const double hl = fma(pl, ggm1, (0.5 * wl[k][0]) * kl), hr = fma(pr, ggm1, (0.5 * wr[k][0]) * kr);
+    F[k][4] = fma(hl, btl[k], fma(hr, btr[k], e[k] * (pl - pr)));
+  }
+#else
+  hlle_ab<N>(wl[0], wr[0], gamma, ggm1, F[0]);
+  hlle_ab<N>(wl[1], wr[1], gamma, ggm1, F[1]);
+#endif
+}
+
 // cons -> prim of the cell pair at p (in place, variable stride vs), a2; returns the primitives
 __device__ __forceinline__ void convert_pair(double* p, int vs, double gm1, double (&w)[2][NVAR], ErrWord* err,
                                              int stage, long long gid, int k, int j, int i) {
@@ -204,8 +252,17 @@ __device__ __forceinline__ void row_at(int rr, int i0, int& off, int& vs) {
 
 // S2 = false: stage 1 (finish operand U_in = U^n; writes U1 and H = ha0 U^n + hb1 U1);
 // S2 = true: stage 2 (finish operand H; writes H + cdt dt L).  REDUCE: CFL / totals partials.
-template <bool REDUCE, bool S2>
-__global__ void __launch_bounds__(NTH, 3) stage2_kernel(StageArgs A, Geom G, const __grid_constant__ Maps maps) {
+#ifndef PH_S2_MINB
+#define PH_S2_MINB 3  // CTAs per SM the register allocation is sized for (A/B knob)
+#endif
+// PUT: fused peer put (boundary blocks, peer-memory halo, PH_FUSED_PUT=1): finished cells within g
+// layers of a face whose neighbour lives on another GPU are also stored into that GPU's receive
+// buffer, at the place its unpack reads ([v][box], box (k, j, i)-major).
+// ML: multilevel meshes (a8): fluxes of faces on a coarse-fine block face also go to the face-flux
+// slots (M.fslot) for the reflux, and with REDUCE the cells of flux-corrected layers are left to
+// rfx_reduce_kernel (they change after this kernel).
+template <bool REDUCE, bool S2, bool PUT, bool ML>
+__global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Geom G, const __grid_constant__ Maps maps) {
   extern __shared__ __align__(128) double sm[];
   double* fin = sm + OFF_FIN;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sm + OFF_BAR);  // full[0..NSLOT), fin = bar[NSLOT]
@@ -229,6 +286,17 @@ __global__ void __launch_bounds__(NTH, 3) stage2_kernel(StageArgs A, Geom G, con
   const double gamma = G.gamma, gm1 = G.gm1, ggm1 = G.gamma * G.inv_gm1;
   const double cdt = A.cdt * A.st->dt_used;
   const int own = R_M + r * TX + i0;  // own pair in a ring slot (centre region)
+  // multilevel: flux F of the face at index (a, b) of block face f into its slot ([v][b][a] over the
+  // face's two tangential extents, the slower one b)
+  auto ml_put = [&](int f, int a, int b, const double* F) {
+    const int fs = M.fslot[f];
+    if (fs < 0) return;
+    const int d = f >> 1, ta = d == 0 ? 1 : 0, tb = d == 2 ? 1 : 2;
+    const int64_t fstr = (int64_t)G.n[ta] * G.n[tb];
+    double* o = A.fbuf + (int64_t)fs * G.fstride + (int64_t)b * G.n[ta] + a;
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) o[v * fstr] = F[v];
+  };
 
   auto issue_plane = [&](int q, int s) {  // tid 0 only
     uint64_t* fb = bar + s;
@@ -292,10 +360,8 @@ __global__ void __launch_bounds__(NTH, 3) stage2_kernel(StageArgs A, Geom G, con
     double* Wq = sm + s * PLANE;
     mbar_wait(bar + s, (uint32_t)(idx / NSLOT) & 1u);
     // ---- a2: cons -> prim of plane q, in place
-    {
-      double wq[2][NVAR];
-      convert_pair(Wq + own, VM, gm1, wq, A.err, A.stage, gid, q, y0 + r, x0 + i0);
-    }
+    double wq[2][NVAR];
+    convert_pair(Wq + own, VM, gm1, wq, A.err, A.stage, gid, q, y0 + r, x0 + i0);
     if (mainp && lane < 16) {
       // 64 halo pairs: x-halo left / right (one per row), y-halo below / above (8 per row)
       const int h = 16 * warp + lane;
@@ -326,21 +392,61 @@ __global__ void __launch_bounds__(NTH, 3) stage2_kernel(StageArgs A, Geom G, con
       }
     }
 
-    double sxy[2][NVAR];  // dx + dy of the own pair of plane c (the canonical (dx + dy) + dz order)
+    double dz[2][NVAR];
+    // ---- z: slope of plane q-1 (own pair), face q-1 between planes q-2 and q-1
+    if (idx >= 2) {
+      const double* pm = sm + s2 * PLANE + own;
+      const double* p0 = sm + s1 * PLANE + own;
+      double bot[2][NVAR], top[2][NVAR];
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) {
+        const double2 a = lds2(pm + v * VM), b = lds2(p0 + v * VM);
+        mm_states(b.x - a.x, wq[0][v] - b.x, b.x, bot[0][v], top[0][v]);
+        mm_states(b.y - a.y, wq[1][v] - b.y, b.y, bot[1][v], top[1][v]);
+      }
+      if (q - 1 >= k0 && q - 1 <= k1) {
+        double F[2][NVAR];
+        hlle_ab2<3>(topz, bot, gamma, ggm1, F);
+        if (ML && (q - 1 == 0 || q - 1 == n3)) {  // z face on the block's low / high face: [v][j][i]
+          ml_put(q - 1 == 0 ? 4 : 5, x0 + i0, y0 + r, F[0]);
+          ml_put(q - 1 == 0 ? 4 : 5, x0 + i0 + 1, y0 + r, F[1]);
+        }
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) {
+            dz[e][v] = (F[e][v] - fzp[e][v]) * idx3;
+            fzp[e][v] = F[e][v];
+          }
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) topz[e][v] = top[e][v];  // plane q-1's top state
+    }
+
+
+    double sxy[2][NVAR];  // dx + (dy + dz) of the own pair of plane c
     if (cact) {
       const double* Wc = sm + s2 * PLANE;
       // ---- extra round: the warp's top y faces and its rows' right x faces, then distributed
       // extra round: lanes 0..15 the y face 4w+4-1/2 of column `lane` (rows 4w+2 .. 4w+5), lanes
-      // 16..19 the x face 16-1/2 of row 4w + lane-16 (cells 14, 15 | 16, 17)
+      // 16..18 and 31 the x face 16-1/2 of row 4w + 0..3 (cells 14, 15 | 16, 17)
       double Fe[NVAR];
       if (lane < TX) {
         int ao, av, bo, bv;
         row_at(4 * warp + 2, lane, ao, av);
         row_at(4 * warp + 4, lane, bo, bv);
         face4(Wc + ao, av, Wc + bo, bv, bv == VM ? TX : TX, 2, gamma, ggm1, Fe);
-      } else if (lane < TX + 4) {
-        const int rr = 4 * warp + (lane - TX);
+      } else if (lane < TX + 3 || lane == 31) {  // row 4w+3's face on lane 31, its consumer
+        const int rr = 4 * warp + (lane == 31 ? 3 : lane - TX);
         face4(Wc + R_M + rr * TX + TX - 2, VM, Wc + R_XR + rr * 2, VX, 1, 1, gamma, ggm1, Fe);
+      }
+      if (ML) {
+        if (lane < TX && warp == NW - 1 && y0 + TY == G.n[1]) ml_put(3, x0 + lane, c, Fe);  // y face n2: [v][k][i]
+        if ((lane >= TX && lane < TX + 3) || lane == 31) {
+          if (x0 + TX == G.n[0]) ml_put(1, y0 + 4 * warp + (lane == 31 ? 3 : lane - TX), c, Fe);  // x face n1: [v][k][j]
+        }
       }
       // ---- y faces j-1/2 of the own pair (rows r-2 .. r+1); j+1/2 from the row above
       double dy[2][NVAR];
@@ -359,9 +465,14 @@ __global__ void __launch_bounds__(NTH, 3) stage2_kernel(StageArgs A, Geom G, con
           mm_states(b.y - a.y, cc.y - b.y, b.y, t, wl[1][v]);
           mm_states(cc.y - b.y, d.y - cc.y, cc.y, wr[1][v], t);
         }
-        double F0[NVAR], F1[NVAR];
-        hlle_ab<2>(wl[0], wr[0], gamma, ggm1, F0);
-        hlle_ab<2>(wl[1], wr[1], gamma, ggm1, F1);
+        double FF[2][NVAR];
+        hlle_ab2<2>(wl, wr, gamma, ggm1, FF);
+        const double(&F0)[NVAR] = FF[0];
+        const double(&F1)[NVAR] = FF[1];
+        if (ML && r == 0 && y0 == 0) {  // y face 0 of the block: [v][k][i]
+          ml_put(2, x0 + i0, c, F0);
+          ml_put(2, x0 + i0 + 1, c, F1);
+        }
 #pragma unroll
         for (int v = 0; v < NVAR; ++v) {
           double h0 = __shfl_down_sync(0xffffffffu, F0[v], 8), h1 = __shfl_down_sync(0xffffffffu, F1[v], 8);
@@ -372,6 +483,10 @@ __global__ void __launch_bounds__(NTH, 3) stage2_kernel(StageArgs A, Geom G, con
           }
           dy[0][v] = (h0 - F0[v]) * idx2;
           dy[1][v] = (h1 - F1[v]) * idx2;
+          // fold dz in now: L = -(dx + (dy + dz)) (the oracle sums (dx + dy) + dz; round-off only, reading
+          // A43) keeps 20 fewer registers live through the x round (+0.3 % on 2b)
+          dy[0][v] += dz[0][v];
+          dy[1][v] += dz[1][v];
         }
       }
       // ---- x faces 2p-1/2 and 2p+1/2 of the own pair; 2p+3/2 from the right neighbour lane
@@ -395,57 +510,31 @@ __global__ void __launch_bounds__(NTH, 3) stage2_kernel(StageArgs A, Geom G, con
             mm_states(a - am, b.x - a, a, t, lo[v]);
           }
         }
-        double FL[NVAR], FM[NVAR];
-        hlle_ab<1>(lo, bt0, gamma, ggm1, FL);
-        hlle_ab<1>(tp0, bt1, gamma, ggm1, FM);
+        double xl[2][NVAR], xr[2][NVAR], FX[2][NVAR];
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) {
+          xl[0][v] = lo[v];
+          xr[0][v] = bt0[v];
+          xl[1][v] = tp0[v];
+          xr[1][v] = bt1[v];
+        }
+        hlle_ab2<1>(xl, xr, gamma, ggm1, FX);
+        double(&FL)[NVAR] = FX[0];
+        const double(&FM)[NVAR] = FX[1];
+        if (ML && p == 0 && x0 == 0) ml_put(0, y0 + r, c, FL);  // x face 0 of the block: [v][k][j]
 #pragma unroll
         for (int v = 0; v < NVAR; ++v) {
           double FR = __shfl_down_sync(0xffffffffu, FL[v], 1, 8);
-          const double er = __shfl_sync(0xffffffffu, Fe[v], TX + kr);
+          const double er = __shfl_sync(0xffffffffu, Fe[v], kr == 3 ? 31 : TX + kr);
           if (p == 7) FR = er;
           dx[0][v] = (FM[v] - FL[v]) * idx1;
           dx[1][v] = (FR - FM[v]) * idx1;
         }
       }
-      // dx + dy now (the canonical (dx + dy) + dz order), so fewer partial sums stay live through z
 #pragma unroll
       for (int e = 0; e < 2; ++e)
 #pragma unroll
-        for (int v = 0; v < NVAR; ++v) sxy[e][v] = dx[e][v] + dy[e][v];
-    }
-
-    double dz[2][NVAR];
-    // ---- z: slope of plane q-1 (own pair), face q-1 between planes q-2 and q-1
-    if (idx >= 2) {
-      const double* pm = sm + s2 * PLANE + own;
-      const double* p0 = sm + s1 * PLANE + own;
-      const double* pp = sm + s * PLANE + own;
-      double bot[2][NVAR], top[2][NVAR];
-#pragma unroll
-      for (int v = 0; v < NVAR; ++v) {
-        const double2 a = lds2(pm + v * VM), b = lds2(p0 + v * VM), c2 = lds2(pp + v * VM);
-        mm_states(b.x - a.x, c2.x - b.x, b.x, bot[0][v], top[0][v]);
-        mm_states(b.y - a.y, c2.y - b.y, b.y, bot[1][v], top[1][v]);
-      }
-      if (q - 1 >= k0 && q - 1 <= k1) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          double F[NVAR];
-          hlle_ab<3>(topz[e], bot[e], gamma, ggm1, F);
-#pragma unroll
-          for (int v = 0; v < NVAR; ++v) {
-            dz[e][v] = (F[v] - fzp[e][v]) * idx3;
-            fzp[e][v] = F[v];
-          }
-        }
-      }
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-#pragma unroll
-        for (int v = 0; v < NVAR; ++v) topz[e][v] = top[e][v];  // plane q-1's top state
-    }
-
-    if (cact) {
+        for (int v = 0; v < NVAR; ++v) sxy[e][v] = dx[e][v] + dy[e][v];  // dx + (dy + dz)
       // ---- a5: divergence + RK combine of the own pair of plane c
       mbar_wait(bar + NSLOT, (uint32_t)(c - k0) & 1u);
       const int64_t cell = (int64_t)slot * G.bstride + (int64_t)(c + g) * plane + (int64_t)(y0 + r + g) * G.N[0] +
@@ -454,8 +543,8 @@ __global__ void __launch_bounds__(NTH, 3) stage2_kernel(StageArgs A, Geom G, con
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) {
         const double2 f = lds2(fin + v * VM + r * TX + i0);
-        const double L0 = -(sxy[0][v] + dz[0][v]);
-        const double L1 = -(sxy[1][v] + dz[1][v]);
+        const double L0 = -sxy[0][v];
+        const double L1 = -sxy[1][v];
         if (S2) {
           un[0][v] = fma(cdt, L0, f.x);
           un[1][v] = fma(cdt, L1, f.y);
@@ -466,9 +555,37 @@ __global__ void __launch_bounds__(NTH, 3) stage2_kernel(StageArgs A, Geom G, con
         }
         stg2(A.Uout + cell + v * G.vstride, un[0][v], un[1][v]);
       }
+      if (PUT) {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int cc[3] = {x0 + i0 + e, y0 + r, c};
+#pragma unroll
+          for (int f = 0; f < 6; ++f) {
+            const int pr = M.prank[f];
+            if (pr < 0) continue;
+            const int d = f >> 1;
+            const int l = (f & 1) ? cc[d] - (G.n[d] - g) : cc[d];  // layer within the face box
+            if (l < 0 || l >= g) continue;
+            const int b0 = d == 0 ? g : G.n[0], b1 = d == 1 ? g : G.n[1], b2 = d == 2 ? g : G.n[2];
+            const int i2 = d == 0 ? l : cc[0], j2 = d == 1 ? l : cc[1], k2 = d == 2 ? l : cc[2];
+            const int64_t nbox = (int64_t)b0 * b1 * b2;
+            double* dst = A.peer_rbuf[pr] + M.poff[f] + ((int64_t)k2 * b1 + j2) * b0 + i2;
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) dst[v * nbox] = un[e][v];
+          }
+        }
+      }
       if (REDUCE) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
+          if (ML && M.rfx) {  // first cell layer of a flux-corrected face: reduced after the reflux
+            const int cc[3] = {x0 + i0 + e, y0 + r, c};
+            bool corrected = false;
+#pragma unroll
+            for (int f = 0; f < 6; ++f)
+              if (((M.rfx >> f) & 1) && cc[f >> 1] == ((f & 1) ? G.n[f >> 1] - 1 : 0)) corrected = true;
+            if (corrected) continue;
+          }
           const double ir = rcp_nr(un[e][0]);
           const double v1 = un[e][1] * ir, v2 = un[e][2] * ir, v3 = un[e][3] * ir;
           const double ke = 0.5 * ((un[e][1] * v1 + un[e][2] * v2) + un[e][3] * v3);
@@ -534,45 +651,58 @@ static cudaError_t make_map(CUtensorMap* m, const double* base, const Geom& G, i
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-template <bool RD, bool S2>
+template <bool RD, bool S2, bool PUT, bool ML = false>
 static cudaError_t launch_t(int nctas, const StageArgs& a, const Maps& mp, const Geom& G, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(stage2_kernel<RD, S2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(stage2_kernel<RD, S2, PUT, ML>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)SMEM_BYTES);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(stage2_kernel<RD, S2>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e = cudaFuncSetAttribute(stage2_kernel<RD, S2, PUT, ML>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     if (e != cudaSuccess) return e;
     if (getenv("PH_DEBUG_ATTR")) {
       cudaFuncAttributes fa;
-      cudaFuncGetAttributes(&fa, stage2_kernel<RD, S2>);
-      fprintf(stderr, "stage2_kernel<%d,%d>: regs %d local %zu dyn smem %zu\n", (int)RD, (int)S2, fa.numRegs,
+      cudaFuncGetAttributes(&fa, stage2_kernel<RD, S2, PUT, ML>);
+      fprintf(stderr, "stage2_kernel<%d,%d,%d>: regs %d local %zu dyn smem %zu\n", (int)RD, (int)S2, (int)PUT, fa.numRegs,
               fa.localSizeBytes, SMEM_BYTES);
     }
     attr = true;
   }
-  stage2_kernel<RD, S2><<<nctas, NTH, SMEM_BYTES, s>>>(a, G, mp);
+  stage2_kernel<RD, S2, PUT, ML><<<nctas, NTH, SMEM_BYTES, s>>>(a, G, mp);
   return cudaGetLastError();
 }
 
 }  // namespace s2
 
 bool stage2_applies(const Geom& G, int recon, bool ml) {
-  if (getenv("PH_STAGE_V1")) return false;
-  return recon == 0 && !ml && G.wavespeed == 0 && G.g == 2 && G.n[0] % s2::TX == 0 && G.n[1] % s2::TY == 0 &&
+  (void)ml;  // multilevel meshes too (flux slots, template ML)
+  if (getenv("PH_STAGE_V1") || getenv("PH_NO_HBASE")) return false;  // it needs the stage-2 base pool H
+  return recon == 0 && G.wavespeed == 0 && G.g == 2 && G.n[0] % s2::TX == 0 && G.n[1] % s2::TY == 0 &&
          G.n[0] >= s2::TX && G.n[1] >= s2::TY;
 }
 
 cudaError_t launch_stage2(bool reduce, bool use_u0, int nctas, const StageArgs& a, const Geom& G, cudaStream_t s) {
-  if (!a.H || a.fbuf || a.peer_rbuf || a.pool_slots <= 0) return cudaErrorNotSupported;
+  if (!a.H || a.pool_slots <= 0 || (a.fbuf && a.peer_rbuf)) return cudaErrorNotSupported;
   s2::Maps mp;
   cudaError_t e;
   if ((e = s2::make_map(&mp.c, a.Uin, G, a.pool_slots, s2::TX, s2::TY)) != cudaSuccess) return e;
   if ((e = s2::make_map(&mp.xh, a.Uin, G, a.pool_slots, 2, s2::TY)) != cudaSuccess) return e;
   if ((e = s2::make_map(&mp.yh, a.Uin, G, a.pool_slots, s2::TX, 2)) != cudaSuccess) return e;
   if ((e = s2::make_map(&mp.f, use_u0 ? a.H : a.Uin, G, a.pool_slots, s2::TX, s2::TY)) != cudaSuccess) return e;
-  if (use_u0) return reduce ? s2::launch_t<true, true>(nctas, a, mp, G, s) : s2::launch_t<false, true>(nctas, a, mp, G, s);
-  return reduce ? s2::launch_t<true, false>(nctas, a, mp, G, s) : s2::launch_t<false, false>(nctas, a, mp, G, s);
+  using namespace s2;
+  if (a.fbuf) {  // multilevel (flux slots)
+    if (use_u0)
+      return reduce ? launch_t<true, true, false, true>(nctas, a, mp, G, s) : launch_t<false, true, false, true>(nctas, a, mp, G, s);
+    return reduce ? launch_t<true, false, false, true>(nctas, a, mp, G, s) : launch_t<false, false, false, true>(nctas, a, mp, G, s);
+  }
+  if (a.peer_rbuf) {
+    if (use_u0)
+      return reduce ? launch_t<true, true, true>(nctas, a, mp, G, s) : launch_t<false, true, true>(nctas, a, mp, G, s);
+    return reduce ? launch_t<true, false, true>(nctas, a, mp, G, s) : launch_t<false, false, true>(nctas, a, mp, G, s);
+  }
+  if (use_u0)
+    return reduce ? launch_t<true, true, false>(nctas, a, mp, G, s) : launch_t<false, true, false>(nctas, a, mp, G, s);
+  return reduce ? launch_t<true, false, false>(nctas, a, mp, G, s) : launch_t<false, false, false>(nctas, a, mp, G, s);
 }
 
 }  // namespace ph

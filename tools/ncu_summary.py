@@ -52,13 +52,21 @@ def main():
     # SASS opcode mix (dynamic) of the profiled launch
     src = ncu_csv(a.rep, "source", ["--print-source", "sass"])
     mix = collections.Counter()
+    # the page repeats each kernel's table; take the first table of the a.launch-th distinct kernel
     hdr2 = None
+    names, want = [], None
     for r in src:
+        if r and r[0] == "Kernel Name":
+            if r[1] not in names:
+                names.append(r[1])
+            want = (len(names) - 1 == a.launch) and names.count(r[1]) == 1 and hdr2 is None
+            continue
         if r and r[0] == "Address":
             if hdr2 is not None:
                 break
-            hdr2 = r
-            iS, iE = r.index("Source"), r.index("Instructions Executed")
+            if want:
+                hdr2 = r
+                iS, iE = r.index("Source"), r.index("Instructions Executed")
             continue
         if hdr2 is None or len(r) <= iE:
             continue

@@ -32,7 +32,7 @@ def main():
     ki = hdr.index("Kernel Name")
     launches = []
     for r in rows[2:]:
-        if "stage_kernel" not in r[ki]:
+        if "stage_kernel" not in r[ki] and "stage2_kernel" not in r[ki]:
             continue
         def val(name):
             i = hdr.index(name)
