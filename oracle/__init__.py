@@ -12,7 +12,9 @@ Parity status per function ("Oracle pins"):
   Morton, partition, tree/2:1, neighbours, exchange, flux correction, dt, totals, RK2, VL2
                                                            -> pinned (tests/test_oracle_*.py)
   AMR refinement criterion (A14: closed form on a linear pressure)  -> pinned
-  derefinement gate (A16), staging geometry (A12)          -> parity unpinned by the paper
+  physical BCs on fine ghosts and coarse staging, staging geometry at walls (A12)
+                                                           -> pinned (method of images)
+  derefinement gate (A16)                                  -> parity unpinned by the paper
 """
 from __future__ import annotations
 

@@ -208,10 +208,11 @@ static uint64_t mix(uint64_t h, uint64_t x) {
   return h;
 }
 
-static void add_chunks(Phase& P, const XTask& t) {
+static void add_chunks(Phase& P, const XTask& t, const Geom& G) {
   int id = (int)P.tasks.size();
   P.tasks.push_back(t);
-  for (int b = 0; b < t.ncell; b += XCHUNK) P.chunks.push_back(Chunk{id, b});
+  const int step = xtask_pairs(t, G.g, G.cg) ? 2 * XCHUNK : XCHUNK;  // pair mode: 2 cells per thread
+  for (int b = 0; b < t.ncell; b += step) P.chunks.push_back(Chunk{id, b});
 }
 
 static int bc_bits(const ph_mesh* m, const BlockInfo& b) {
@@ -305,7 +306,7 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
       if (dst_here && src_here) {
         t.dst_slot = cs;
         t.src_slot = (int)s.local;
-        add_chunks(P.local, t);
+        add_chunks(P.local, t, m->G);
       } else if (src_here) {  // pack for b.rank
         int peer = b.rank;
         t.dst_slot = -1;
@@ -315,7 +316,7 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
         soff[peer] += (int64_t)NVAR * t.ncell;
         P.send_hash[peer] = mix(P.send_hash[peer], (uint64_t)b.gid * 64 + (uint64_t)(&e - &b.nbrs[0]));
         pack_peer.push_back(peer);
-        add_chunks(P.pack, t);
+        add_chunks(P.pack, t, m->G);
       } else {  // unpack from s.rank
         int peer = s.rank;
         t.kind = (t.kind == T_CCOPY) ? T_UNPACK_C : T_UNPACK_U;
@@ -325,7 +326,7 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
         roff[peer] += (int64_t)NVAR * t.ncell;
         P.recv_hash[peer] = mix(P.recv_hash[peer], (uint64_t)b.gid * 64 + (uint64_t)(&e - &b.nbrs[0]));
         unpack_peer.push_back(peer);
-        add_chunks(P.unpack, t);
+        add_chunks(P.unpack, t, m->G);
       }
     }
   }
@@ -372,7 +373,7 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
         t.lo[1] = lo1; t.ext[1] = e1;
         t.lo[2] = lo2; t.ext[2] = e2;
         t.ncell = e0 * e1 * e2;
-        if (t.ncell > 0) add_chunks(P.b1, t);
+        if (t.ncell > 0) add_chunks(P.b1, t, m->G);
       };
       if (getenv("PH_FULL_STAGING") || nc[0] <= 2 * T || nc[1] <= 2 * T || nc[2] <= 2 * T) {
         shell(0, nc[0], 0, nc[1], 0, nc[2]);
@@ -398,7 +399,7 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
           r.so[d] = 0;
         }
         r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
-        add_chunks(P.b1, r);
+        add_chunks(P.b1, r, m->G);
       }
       for (int q = 0; q < 27 && anyphys; ++q) {
         if (q == 13) continue;
@@ -415,7 +416,7 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
           else { r.lo[d] = 0; r.ext[d] = m->G.nc[d]; }
         }
         r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
-        add_chunks(P.b2, r);
+        add_chunks(P.b2, r, m->G);
       }
       for (int q = 0; q < 27; ++q) {
         if (q == 13 || kind[q] != -1) continue;
@@ -430,7 +431,7 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
           else { r.lo[d] = 0; r.ext[d] = m->G.nc[d]; }
         }
         r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
-        add_chunks(P.pro, r);
+        add_chunks(P.pro, r, m->G);
       }
     }
     if (anyphys) {
@@ -450,7 +451,7 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
           else { r.lo[d] = 0; r.ext[d] = n[d]; }
         }
         r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
-        add_chunks(P.bcf, r);
+        add_chunks(P.bcf, r, m->G);
       }
     }
   }

@@ -164,7 +164,24 @@ struct RemeshTask {
   int ch[3];
 };
 
-constexpr int XCHUNK = 256;  // cells per exchange chunk (one CTA, one cell per thread)
+constexpr int XCHUNK = 256;  // cells per exchange chunk (one CTA, one cell per thread; 2 per thread in pair mode)
+
+// Pair mode of a copy / unpack / pack task: every thread moves two cells adjacent in i with 16-byte
+// accesses.  Needs an even row extent and even (16-B aligned) first indices on both sides; the host
+// (chunking) and the kernel evaluate the same rule.
+__host__ __device__ inline bool xtask_pairs(const XTask& t, int g, int cg) {
+  if ((t.ext[0] & 1) || (g & 1) || (cg & 1) || (t.lo[0] & 1)) return false;
+  switch (t.kind) {
+    case T_COPY:
+    case T_CCOPY:
+      return ((t.so[0] & 1) == 0) && (t.dst_slot >= 0 || (t.buf & 1) == 0);
+    case T_UNPACK_U:
+    case T_UNPACK_C:
+      return (t.buf & 1) == 0;
+    default:
+      return false;
+  }
+}
 
 // launchers (kernels.cu)
 cudaError_t launch_stage(int recon, bool reduce, bool use_u0, int nblk_cta, const StageArgs& a, const Geom& G,

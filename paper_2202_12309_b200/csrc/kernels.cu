@@ -750,11 +750,50 @@ __device__ __forceinline__ int bc_map(int idx, int n, int lo_kind, int hi_kind, 
   return idx;
 }
 
+// pair mode (xtask_pairs): copies, packs and unpacks move two i-adjacent cells per thread with 16-byte
+// loads / stores (the x-face boxes are rows of 2 cells, the y / z ones rows of n)
+__device__ __forceinline__ void xfill_pair(const XArgs& A, const XTask& t, const Geom& G, int c, int i, int j, int k) {
+  double2 v[NVAR];
+  if (t.kind == T_UNPACK_U || t.kind == T_UNPACK_C) {
+    const double* s = A.rbuf + t.buf + c;
+#pragma unroll
+    for (int q = 0; q < NVAR; ++q) v[q] = *reinterpret_cast<const double2*>(s + (int64_t)q * t.ncell);
+  } else {
+    const double* s = A.U + (int64_t)t.src_slot * G.bstride +
+                      ((int64_t)(k + t.so[2] + G.g) * G.N[1] + (j + t.so[1] + G.g)) * G.N[0] + (i + t.so[0] + G.g);
+#pragma unroll
+    for (int q = 0; q < NVAR; ++q) v[q] = __ldcg(reinterpret_cast<const double2*>(s + q * G.vstride));
+  }
+  double* d;
+  int64_t vs;
+  if (t.dst_slot < 0) {  // pack into my send buffer or put into peer bc's receive buffer ([v][cell])
+    d = (t.bc >= 0 ? A.peer_rbuf[t.bc] : A.sbuf) + t.buf + c;
+    vs = t.ncell;
+  } else if (t.kind == T_COPY || t.kind == T_UNPACK_U) {
+    d = A.U + (int64_t)t.dst_slot * G.bstride + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
+    vs = G.vstride;
+  } else {
+    d = A.C + (int64_t)t.dst_slot * G.cbstride + ((int64_t)(k + G.cg) * G.NC[1] + (j + G.cg)) * G.NC[0] + (i + G.cg);
+    vs = G.cvstride;
+  }
+#pragma unroll
+  for (int q = 0; q < NVAR; ++q) *reinterpret_cast<double2*>(d + q * vs) = v[q];
+}
+
 __global__ void __launch_bounds__(XT) xfill_kernel(XArgs A, Geom G) {
   const Chunk ch = A.chunks[blockIdx.x];
   const XTask t = A.tasks[ch.task];
-  const int end = min(ch.begin + XCHUNK, t.ncell);
   const int e0 = t.ext[0], e01 = t.ext[0] * t.ext[1];
+  if (xtask_pairs(t, G.g, G.cg)) {
+    const int end = min(ch.begin + 2 * XCHUNK, t.ncell);
+    for (int c = ch.begin + 2 * threadIdx.x; c < end; c += 2 * XT) {
+      const int ck = c / e01, rem = c - ck * e01;
+      const int cj = rem / e0, ci = rem - cj * e0;
+      xfill_pair(A, t, G, c, t.lo[0] + ci, t.lo[1] + cj, t.lo[2] + ck);
+    }
+    return;
+  }
+  const int end = min(ch.begin + XCHUNK, t.ncell);
   for (int c = ch.begin + threadIdx.x; c < end; c += XT) {
     const int ck = c / e01, rem = c - ck * e01;
     const int cj = rem / e0, ci = rem - cj * e0;
@@ -832,14 +871,21 @@ __global__ void __launch_bounds__(XT) xfill_kernel(XArgs A, Geom G) {
 #pragma unroll
           for (int a = 0; a < 2; ++a)
 #pragma unroll
-            for (int b = 0; b < 2; ++b)
+            for (int b = 0; b < 2; ++b) {
+              double val[2];
 #pragma unroll
-              for (int e = 0; e < 2; ++e) {
-                double val = __dadd_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(e ? 0.25 : -0.25, s1)),
-                                                 __dmul_rn(b ? 0.25 : -0.25, s2)),
-                                       __dmul_rn(a ? 0.25 : -0.25, s3));
-                q[a * fk + b * fj + e] = val;
+              for (int e = 0; e < 2; ++e)
+                val[e] = __dadd_rn(__dadd_rn(__dadd_rn(c0, __dmul_rn(e ? 0.25 : -0.25, s1)),
+                                             __dmul_rn(b ? 0.25 : -0.25, s2)),
+                                   __dmul_rn(a ? 0.25 : -0.25, s3));
+              // fine cells 2i, 2i+1 are 16-B aligned when g is even: one 128-bit store
+              if ((G.g & 1) == 0) {
+                *reinterpret_cast<double2*>(q + a * fk + b * fj) = make_double2(val[0], val[1]);
+              } else {
+                q[a * fk + b * fj] = val[0];
+                q[a * fk + b * fj + 1] = val[1];
               }
+            }
         }
         break;
       }

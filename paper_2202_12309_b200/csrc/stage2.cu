@@ -494,20 +494,21 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
       {
         double lo[NVAR], bt0[NVAR], tp0[NVAR], bt1[NVAR], tp1[NVAR];
         // x stencil cells 2p-1 and 2p+2: centre region, or the x-halo columns for the outer lanes
-        const int xlo = p > 0 ? own - 1 : R_XL + r * 2 + 1, xlv = p > 0 ? VM : VX;
+        // cells 2p-2, 2p-1 as one 128-bit load (lane 0: the x-halo cells -2, -1)
+        const int xlo = p > 0 ? own - 2 : R_XL + r * 2, xlv = p > 0 ? VM : VX;
         const int xro = p < 7 ? own + 2 : R_XR + r * 2, xrv = p < 7 ? VM : VX;
 #pragma unroll
         for (int v = 0; v < NVAR; ++v) {
-          const double a = Wc[xlo + v * xlv], d = Wc[xro + v * xrv];
+          const double2 lf = lds2(Wc + xlo + v * xlv);
+          const double a = lf.y, d = Wc[xro + v * xrv];
           const double2 b = lds2(Wc + own + v * VM);
           const double d0 = b.y - b.x;
           mm_states(b.x - a, d0, b.x, bt0[v], tp0[v]);
           mm_states(d0, d - b.y, b.y, bt1[v], tp1[v]);
           lo[v] = __shfl_up_sync(0xffffffffu, tp1[v], 1, 8);
           if (p == 0) {  // top state of the halo cell -1 (cells -2, -1 in the x-halo, 0 own)
-            const double am = Wc[R_XL + r * 2 + v * VX];
             double t;
-            mm_states(a - am, b.x - a, a, t, lo[v]);
+            mm_states(a - lf.x, b.x - a, a, t, lo[v]);
           }
         }
         double xl[2][NVAR], xr[2][NVAR], FX[2][NVAR];

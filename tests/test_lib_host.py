@@ -103,7 +103,7 @@ def test_random_multilevel_meshes_match_oracle(oracle_mod, P):
 
 def test_exchange_plan_is_symmetric_across_ranks(P):
     """What rank s packs for rank d is exactly what d unpacks from s (sizes and order)."""
-    for R in (2, 3, 4):
+    for R in (2, 3, 4, 8):
         kw = dict(mesh_nx=(128, 64, 64), block_nx=(16, 16, 16), max_level=1, refinement=1,
                   regions=[(1, 0.2, 0.5, 0.3, 0.6, 0.1, 0.4)])
         infos = [P.Mesh(host_only=True, rank=r, nranks=R, **kw).plan_info() for r in range(R)]

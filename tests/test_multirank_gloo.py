@@ -65,6 +65,10 @@ def _run(world, kw):
     (2, dict(mesh_nx=(64, 64, 64), block_nx=(16, 16, 16), max_level=1, refinement=1,
              regions=[(1, 0.2, 0.6, 0.1, 0.5, 0.3, 0.7)], bc_inner=(1, 0, 2), bc_outer=(1, 0, 2))),
     (4, dict(mesh_nx=(128, 128, 64), block_nx=(32, 32, 32))),
+    # the 8-GPU weak configuration shape (every rank has 7 peers) and a multilevel mesh over 8 ranks
+    (8, dict(mesh_nx=(128, 128, 128), block_nx=(32, 32, 32))),
+    (8, dict(mesh_nx=(64, 64, 64), block_nx=(16, 16, 16), max_level=1, refinement=1,
+             regions=[(1, 0.2, 0.6, 0.1, 0.5, 0.3, 0.7)])),
 ])
 def test_plan_consistent_across_gloo_ranks(world, kw):
     objs, ok = _run(world, kw)
