@@ -60,5 +60,17 @@ def build_strict(force: bool = False) -> str:
     return build(force=True, defines=("PH_STRICT",), out=STRICT_LIB, extra=("-fmad=false",))
 
 
+JITTER_LIB = os.path.join(HERE, "libph_jitter.so")
+
+
+def build_jitter(force: bool = False) -> str:
+    """Race-probe build (-DPH_JITTER=1, point.cuh): warps sleep at random probe points; its results must
+    equal the normal build's bit for bit (tests/test_gpu_races.py)."""
+    if (not force and os.path.exists(JITTER_LIB) and os.path.exists(LIB)
+            and os.path.getmtime(JITTER_LIB) >= os.path.getmtime(LIB) and not _stale()):
+        return JITTER_LIB
+    return build(force=True, defines=("PH_JITTER=1",), out=JITTER_LIB)
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

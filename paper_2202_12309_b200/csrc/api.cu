@@ -357,14 +357,15 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
     int bits = bc_bits(m, b);
     if (b.has_coarser) {
       int cs = cslot[gid];
-      // own interior into the staging.  Phase C (prolongation) reads the staging at and next to its
-      // ghost layer, and physical BCs on the staging mirror cg interior layers, so the outer cg coarse
-      // layers of the interior suffice: a non-overlapping shell (x slabs whole, y slabs without the x
-      // slabs, z slabs inside both); the whole interior when the shell would cover it anyway.  This
-      // phase is HBM-bound (it reads the block's fine interior), so the shell saves its bytes.
+      // own interior into the staging -- only the coarse cells something reads: the prolongation of the
+      // first ghost layer at each coarser-neighbour offset o takes minmod slopes over +-1 coarse cell, so
+      // it reads the interior layer next to o (I_d = 0 for o_d < 0, nc_d - 1 for o_d > 0, all I_d for
+      // o_d = 0); physical BCs on the staging mirror the cg interior layers next to each physical face.
+      // A mask over the nc^3 staging interior, cut into disjoint boxes (x-runs merged over j, then k).
+      // This phase is HBM-bound (it reads fine interior cells): round 1 restricted the whole 2-layer shell.
       const int* nc = m->G.nc;
       const int T = m->G.cg;
-      auto shell = [&](int lo0, int e0, int lo1, int e1, int lo2, int e2) {
+      auto restrict_box = [&](int lo0, int e0, int lo1, int e1, int lo2, int e2) {
         XTask t{};
         t.kind = T_CRESTRICT;
         t.dst_slot = cs;
@@ -375,15 +376,73 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
         t.ncell = e0 * e1 * e2;
         if (t.ncell > 0) add_chunks(P.b1, t, m->G);
       };
-      if (getenv("PH_FULL_STAGING") || nc[0] <= 2 * T || nc[1] <= 2 * T || nc[2] <= 2 * T) {
-        shell(0, nc[0], 0, nc[1], 0, nc[2]);
+      if (getenv("PH_FULL_STAGING")) {
+        restrict_box(0, nc[0], 0, nc[1], 0, nc[2]);
       } else {
-        shell(0, T, 0, nc[1], 0, nc[2]);
-        shell(nc[0] - T, T, 0, nc[1], 0, nc[2]);
-        shell(T, nc[0] - 2 * T, 0, T, 0, nc[2]);
-        shell(T, nc[0] - 2 * T, nc[1] - T, T, 0, nc[2]);
-        shell(T, nc[0] - 2 * T, T, nc[1] - 2 * T, 0, T);
-        shell(T, nc[0] - 2 * T, T, nc[1] - 2 * T, nc[2] - T, T);
+        const int64_t NCV = (int64_t)nc[0] * nc[1] * nc[2];
+        std::vector<uint8_t> need((size_t)NCV, 0);
+        auto mark = [&](const int lo[3], const int hi[3]) {
+          for (int k = std::max(lo[2], 0); k < std::min(hi[2], nc[2]); ++k)
+            for (int j = std::max(lo[1], 0); j < std::min(hi[1], nc[1]); ++j)
+              for (int i = std::max(lo[0], 0); i < std::min(hi[0], nc[0]); ++i)
+                need[((size_t)k * nc[1] + j) * nc[0] + i] = 1;
+        };
+        for (int q = 0; q < 27; ++q) {
+          if (q == 13 || kind[q] != -1) continue;
+          const int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
+          int lo[3], hi[3];
+          for (int d = 0; d < 3; ++d) {
+            lo[d] = o[d] > 0 ? nc[d] - 1 : 0;
+            hi[d] = o[d] < 0 ? 1 : nc[d];
+          }
+          mark(lo, hi);
+        }
+        for (int d = 0; d < 3; ++d) {
+          for (int side = 0; side < 2; ++side) {
+            if (!(side ? b.phys_hi[d] : b.phys_lo[d])) continue;
+            int lo[3] = {0, 0, 0}, hi[3] = {nc[0], nc[1], nc[2]};
+            if (side) lo[d] = nc[d] - T; else hi[d] = T;
+            mark(lo, hi);
+          }
+        }
+        // disjoint boxes: x-runs per (j, k) row, merged over consecutive j with the same run, then over
+        // consecutive k with the same (run, j-range)
+        struct Box { int i0, ie, j0, je, k0, ke; };
+        std::vector<Box> prev, cur, done;
+        for (int k = 0; k < nc[2]; ++k) {
+          std::vector<Box> plane;
+          for (int j = 0; j < nc[1]; ++j) {
+            for (int i = 0; i < nc[0];) {
+              if (!need[((size_t)k * nc[1] + j) * nc[0] + i]) { ++i; continue; }
+              int e = i;
+              while (e < nc[0] && need[((size_t)k * nc[1] + j) * nc[0] + e]) ++e;
+              bool merged = false;
+              for (Box& bx : plane)
+                if (bx.i0 == i && bx.ie == e && bx.je == j) { bx.je = j + 1; merged = true; break; }
+              if (!merged) plane.push_back(Box{i, e, j, j + 1, k, k + 1});
+              i = e;
+            }
+          }
+          cur.clear();
+          for (Box bx : plane) {
+            bool merged = false;
+            for (Box& pb : prev)
+              if (pb.i0 == bx.i0 && pb.ie == bx.ie && pb.j0 == bx.j0 && pb.je == bx.je && pb.ke == k) {
+                pb.ke = k + 1;
+                cur.push_back(pb);
+                pb.ke = -1;  // moved to cur
+                merged = true;
+                break;
+              }
+            if (!merged) cur.push_back(bx);
+          }
+          for (Box& pb : prev)
+            if (pb.ke >= 0) done.push_back(pb);
+          prev.swap(cur);
+        }
+        for (Box& pb : prev) done.push_back(pb);
+        for (const Box& bx : done)
+          restrict_box(bx.i0, bx.ie - bx.i0, bx.j0, bx.je - bx.j0, bx.k0, bx.ke - bx.k0);
       }
       for (int q = 0; q < 27; ++q) {
         if (q == 13 || kind[q] == -2 || kind[q] == -1) continue;
@@ -497,6 +556,26 @@ static ph_status build_plan(ph_mesh* m) {
   m->direct_halo = !m->no_direct_halo && !m->ho;
   build_exchange(m, m->plan[0], false, cslot);
   build_exchange(m, m->plan[1], m->direct_halo, cslot);
+  if (const char* dump = getenv("PH_PLAN_DUMP")) {  // diagnostics: tasks / cells per phase and task kind
+    if (FILE* f = fopen(dump, "a")) {
+      const char* names[] = {"pack", "local", "unpack", "b1", "b2", "pro", "bcf"};
+      for (int pi = 0; pi < 2; ++pi) {
+        auto ph = m->plan[pi].phases();
+        for (size_t q = 0; q < ph.size(); ++q) {
+          int64_t nt[16] = {0}, nc[16] = {0};
+          for (const XTask& t : ph[q]->tasks) {
+            nt[t.kind & 15]++;
+            nc[t.kind & 15] += t.ncell;
+          }
+          for (int k = 0; k < 16; ++k)
+            if (nt[k])
+              fprintf(f, "{\"plan\": %d, \"phase\": \"%s\", \"kind\": %d, \"tasks\": %lld, \"cells\": %lld, "
+                         "\"chunks\": %d}\n", pi, names[q], k, (long long)nt[k], (long long)nc[k], ph[q]->nchunks());
+        }
+      }
+      fclose(f);
+    }
+  }
   // reflux tasks (coarse side) and, across ranks, the fine-side flux packs (O8).
   // Per (sender, receiver) pair both ranks enumerate coarse blocks in gid order and their finer
   // face entries in canonical order, so buffer offsets agree without any handshake.

@@ -403,6 +403,7 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
   for (int q = qbeg; q < qend; ++q) {
     store_prims(q);
     if (q + 1 < qend) issue_load(q + 1);  // the next plane's loads fly during this plane's faces
+    ph_jitter(2 * q);
     __syncthreads();
     const int c = q - 2;                 // plane whose x/y faces and cells are done now
     const int fz = q - 1;                // z face between planes q-2 and q-1
@@ -591,6 +592,7 @@ __global__ void __launch_bounds__(TXv * TYv, 2) stage_kernel(StageArgs A, Geom G
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) topz[v] = top[v];
     }
+    ph_jitter(2 * q + 1);
     __syncthreads();
     // ---- finish the cells of plane c: L = -(((dF1 + dF2) + dF3)) and the RK combine ----
     if (xy && own) {
@@ -738,6 +740,13 @@ __device__ __forceinline__ double mean8(const double* p, int64_t sj, int64_t sk)
   return (((a + b) + (c + d)) + ((e + f) + (gg + h))) * 0.125;  // pairwise, (k,j,i) order (A10)
 }
 
+// mean8 with the i-pairs as 16-byte loads (p 16-B aligned); same sums in the same order (A10)
+__device__ __forceinline__ double mean8v(const double* p, int64_t sj, int64_t sk) {
+  const double2 ab = *reinterpret_cast<const double2*>(p), cd = *reinterpret_cast<const double2*>(p + sj);
+  const double2 ef = *reinterpret_cast<const double2*>(p + sk), gh = *reinterpret_cast<const double2*>(p + sk + sj);
+  return (((ab.x + ab.y) + (cd.x + cd.y)) + ((ef.x + ef.y) + (gh.x + gh.y))) * 0.125;
+}
+
 __device__ __forceinline__ int bc_map(int idx, int n, int lo_kind, int hi_kind, bool& flip) {
   if (idx < 0 && lo_kind) {
     if (lo_kind == 2) { flip = !flip; return -1 - idx; }
@@ -781,6 +790,7 @@ __device__ __forceinline__ void xfill_pair(const XArgs& A, const XTask& t, const
 }
 
 __global__ void __launch_bounds__(XT) xfill_kernel(XArgs A, Geom G) {
+  ph_jitter(threadIdx.x & 31);
   const Chunk ch = A.chunks[blockIdx.x];
   const XTask t = A.tasks[ch.task];
   const int e0 = t.ext[0], e01 = t.ext[0] * t.ext[1];
@@ -825,18 +835,22 @@ __global__ void __launch_bounds__(XT) xfill_kernel(XArgs A, Geom G) {
         const int fi = 2 * i - t.so[0], fj = 2 * j - t.so[1], fk = 2 * k - t.so[2];
         const double* s = A.U + (int64_t)t.src_slot * G.bstride + ((int64_t)(fk + G.g) * G.N[1] + (fj + G.g)) * G.N[0] + (fi + G.g);
         const int64_t sj = G.N[0], sk = (int64_t)G.N[0] * G.N[1];
+        const bool vec = ((t.so[0] | G.g) & 1) == 0;  // fine i-pairs 16-B aligned (uniform per task)
+        double m8[NVAR];
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) m8[v] = vec ? mean8v(s + v * G.vstride, sj, sk) : mean8(s + v * G.vstride, sj, sk);
         if (t.dst_slot < 0) {  // pack (or put into peer bc's receive buffer, as for copies)
           double* d = (t.bc >= 0 ? A.peer_rbuf[t.bc] : A.sbuf) + t.buf + c;
 #pragma unroll
-          for (int v = 0; v < NVAR; ++v) d[(int64_t)v * t.ncell] = mean8(s + v * G.vstride, sj, sk);
+          for (int v = 0; v < NVAR; ++v) d[(int64_t)v * t.ncell] = m8[v];
         } else if (t.kind == T_RESTRICT) {
           double* d = A.U + (int64_t)t.dst_slot * G.bstride + ((int64_t)(k + G.g) * G.N[1] + (j + G.g)) * G.N[0] + (i + G.g);
 #pragma unroll
-          for (int v = 0; v < NVAR; ++v) d[v * G.vstride] = mean8(s + v * G.vstride, sj, sk);
+          for (int v = 0; v < NVAR; ++v) d[v * G.vstride] = m8[v];
         } else {
           double* d = A.C + (int64_t)t.dst_slot * G.cbstride + ((int64_t)(k + G.cg) * G.NC[1] + (j + G.cg)) * G.NC[0] + (i + G.cg);
 #pragma unroll
-          for (int v = 0; v < NVAR; ++v) d[v * G.cvstride] = mean8(s + v * G.vstride, sj, sk);
+          for (int v = 0; v < NVAR; ++v) d[v * G.cvstride] = m8[v];
         }
         break;
       }
@@ -1628,16 +1642,14 @@ __global__ void __launch_bounds__(TGT, 4) tag_kernel(const double* U, const Bloc
       const int c = tid + s * TGT;
       if (!need_cell(c, q, i, j)) continue;
       const double* un = uq[s];
-      const double ir = __ddiv_rn(1.0, un[0]);
-      const double v1 = __dmul_rn(un[1], ir), v2 = __dmul_rn(un[2], ir), v3 = __dmul_rn(un[3], ir);
-      const double ke = __dmul_rn(0.5, __dadd_rn(__dadd_rn(__dmul_rn(un[1], v1), __dmul_rn(un[2], v2)), __dmul_rn(un[3], v3)));
-      P[c] = __dmul_rn(G.gm1, __dsub_rn(un[4], ke));
+      // one cons -> prim per cell (the stage kernels' MUFU-seeded arithmetic, A31): the pressure feeds
+      // the indicator (reading A46) and, for the tile's own cells, the dt / totals partials
+      const double fr = rcp_nr(un[0]);
+      const double w1 = un[1] * fr, w2 = un[2] * fr, w3 = un[3] * fr;
+      const double fke = 0.5 * ((un[1] * w1 + un[2] * w2) + un[3] * w3);
+      const double p = G.gm1 * (un[4] - fke);
+      P[c] = p;
       if (partials && q >= 0 && q < G.n[2] && i >= 0 && i < nxt && j >= 0 && j < nyt) {
-        // dt / totals of the tile's own cells (the standalone reduction's arithmetic)
-        const double fr = rcp_nr(un[0]);
-        const double w1 = un[1] * fr, w2 = un[2] * fr, w3 = un[3] * fr;
-        const double fke = 0.5 * ((un[1] * w1 + un[2] * w2) + un[3] * w3);
-        const double p = G.gm1 * (un[4] - fke);
         if (!(un[0] > 0.0) || !(p > 0.0)) set_error(err, 0, M.gid, q, y0 + j, x0 + i);
         const double cs = sound_speed(un[0], p, G.gamma);
         const double s1 = (fabs(w1) + cs) * M.idx[0], s2 = (fabs(w2) + cs) * M.idx[1], s3 = (fabs(w3) + cs) * M.idx[2];
@@ -1647,6 +1659,7 @@ __global__ void __launch_bounds__(TGT, 4) tag_kernel(const double* U, const Bloc
       }
     }
     if (q < G.n[2]) load_plane(q + 1);
+    ph_jitter(q + 7);
     __syncthreads();
     const int c = q - 1;  // plane whose indicator is complete now
     if (c >= 0 && own) {
@@ -1654,11 +1667,13 @@ __global__ void __launch_bounds__(TGT, 4) tag_kernel(const double* U, const Bloc
       const double* P0 = sp[(c + 3) % 3];
       const double* Pp = sp[(c + 4) % 3];
       const int o = (ty + 1) * TGW + (tx + 1);
-      const double g1 = __dmul_rn(0.5, __dsub_rn(P0[o + 1], P0[o - 1]));
-      const double g2 = __dmul_rn(0.5, __dsub_rn(P0[o + TGW], P0[o - TGW]));
-      const double g3 = __dmul_rn(0.5, __dsub_rn(Pp[o], Pm[o]));
-      const double s = __dadd_rn(__dadd_rn(__dmul_rn(g1, g1), __dmul_rn(g2, g2)), __dmul_rn(g3, g3));
-      mx = fmax(mx, __ddiv_rn(__dsqrt_rn(s), P0[o]));
+      const double g1 = 0.5 * (P0[o + 1] - P0[o - 1]);
+      const double g2 = 0.5 * (P0[o + TGW] - P0[o - TGW]);
+      const double g3 = 0.5 * (Pp[o] - Pm[o]);
+      const double s = (g1 * g1 + g2 * g2) + g3 * g3;
+      // sqrt(s) / p with MUFU-seeded rsqrt / rcp (a uniform region gives s = 0 exactly, eps = 0)
+      const double e = s > 0.0 ? (s * rsqrt_nr(s)) * rcp_nr(P0[o]) : 0.0;
+      mx = fmax(mx, e);
     }
     __syncthreads();
   }

@@ -66,4 +66,22 @@ __device__ __forceinline__ void set_error(ErrWord* err, int stage, long long gid
   }
 }
 
+// Race probe (the jitter build, -DPH_JITTER=<seed>; compute-sanitizer is closed on this GPU pool): one
+// warp in four sleeps up to ~2 us at each probe point, chosen by a hash of (CTA, warp, salt, seed), so
+// warps reach barriers, mbarrier waits and shared / global accesses in orders the normal build never
+// produces.  tests/test_gpu_races.py requires the jitter build's results to equal the normal build's
+// bit for bit.  A no-op in normal builds.
+__device__ __forceinline__ void ph_jitter(unsigned salt) {
+#ifdef PH_JITTER
+  unsigned h = (blockIdx.x * 0x9E3779B1u) ^ ((threadIdx.x >> 5) * 0x85EBCA77u) ^ (salt * 0xC2B2AE3Du) ^
+               ((unsigned)PH_JITTER * 0x27D4EB2Fu);
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  if ((h & 3u) == 0u) __nanosleep(h & 2047u);
+#else
+  (void)salt;
+#endif
+}
+
 }  // namespace ph

@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
     const int c = q - 2;
     const bool mainp = q >= k0 && q < k1, cact = c >= k0 && c < k1;
     double* Wq = sm + s * PLANE;
+    ph_jitter(4 * q + 0);
     mbar_wait(bar + s, (uint32_t)(idx / NSLOT) & 1u);
     // ---- a2: cons -> prim of plane q, in place
     double wq[2][NVAR];
@@ -382,7 +383,9 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
       double wh[2][NVAR];
       convert_pair(Wq + off, vs, gm1, wh, A.err, A.stage, gid, q, y0 + jj, x0 + ii);
     }
+    ph_jitter(4 * q + 1);
     __syncthreads();  // plane q primitives visible; step q-1 done everywhere (its slot and fin free)
+    ph_jitter(4 * q + 2);
     if (tid == 0) {
       if (q + 1 < qend) issue_plane(q + 1, (s + 1) & (NSLOT - 1));
       if (cact) {
@@ -537,6 +540,7 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
 #pragma unroll
         for (int v = 0; v < NVAR; ++v) sxy[e][v] = dx[e][v] + dy[e][v];  // dx + (dy + dz)
       // ---- a5: divergence + RK combine of the own pair of plane c
+      ph_jitter(4 * q + 3);
       mbar_wait(bar + NSLOT, (uint32_t)(c - k0) & 1u);
       const int64_t cell = (int64_t)slot * G.bstride + (int64_t)(c + g) * plane + (int64_t)(y0 + r + g) * G.N[0] +
                            (x0 + i0 + g);

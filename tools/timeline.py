@@ -45,25 +45,33 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cycles", type=int, default=2)
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "timeline"))
+    ap.add_argument("--config", default="2b", choices=["2b", "3"], help="3: the AMR blast on one GPU")
     a = ap.parse_args()
     import torch
     import torch.distributed as dist
     from torch.profiler import ProfilerActivity, profile
     import paper_2202_12309_b200 as P
     from bench import BLAST, workload
-    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    rank, world, local = (int(os.environ.get(k, d)) for k, d in (("RANK", 0), ("WORLD_SIZE", 1), ("LOCAL_RANK", 0)))
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    W = workload("2b", world)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if a.config == "3":
+        W = dict(mesh_nx=(128,) * 3, block_nx=(32,) * 3, max_level=3, refinement=2, refine_tol=0.1,
+                 derefine_tol=0.025, derefine_interval=8, xmin=(-.5,) * 3, xmax=(.5,) * 3)
+    else:
+        W = workload("2b", world)
     m = P.Mesh(device=local, rank=rank, nranks=world, stream=torch.cuda.current_stream(), **W)
     m.set_problem(P.BLAST, BLAST)
     m.step(3)
     torch.cuda.synchronize()
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     with profile(activities=[ProfilerActivity.CUDA]) as prof:
         m.step(a.cycles)
         torch.cuda.synchronize()
-    dist.barrier()
+    if world > 1:
+        dist.barrier()
     if rank == 0:
         trace = a.out + "_trace.json"
         prof.export_chrome_trace(trace)
@@ -96,13 +104,25 @@ def main():
             f.write("\n| kernel | stream | start us | dur us |\n|---|---|---|---|\n")
             for r in rows[:80]:
                 f.write(f"| {r['name'][:60]} | {r['stream']} | {r['start_us']:.0f} | {r['dur_us']:.0f} |\n")
+            tot = {}
+            for r in rows:
+                k = r["name"][:60]
+                tot[k] = tot.get(k, [0, 0.0])
+                tot[k][0] += 1
+                tot[k][1] += r["dur_us"]
+            f.write("\n| kernel (all launches) | launches | total us |\n|---|---|---|\n")
+            for k, (n_, t_) in sorted(tot.items(), key=lambda x: -x[1][1]):
+                f.write(f"| {k} | {n_} | {t_:.0f} |\n")
+            busy_all = intervals_union([(r["start_us"], r["start_us"] + r["dur_us"]) for r in rows])
+            f.write(f"\nGPU busy {sum(e - s_ for s_, e in busy_all):.0f} us of {span:.0f} us span (idle gaps = host work / launch latency)\n")
             hin = sum(r["dur_us"] for r in halo)
             hov = overlap(intervals_union([(r["start_us"], r["start_us"] + r["dur_us"]) for r in halo]), busy[si])
             f.write(f"\nhalo kernels (pack / put / signal / wait / NCCL): {hin:.0f} us, of which {hov:.0f} us "
                     f"run while the interior stream computes\n")
         print(open(a.out + ".md").read()[:1500])
     m.close()
-    dist.destroy_process_group()
+    if world > 1:
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
