@@ -17,6 +17,8 @@
 #include <array>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/ph.h"
 #include "device.cuh"
 #include "mesh.hpp"
@@ -26,6 +28,13 @@ constexpr int TX = TILE_X, TY = TILE_Y;
 }
 
 using namespace ph;
+
+// NVTX ranges (header-only NVTX3) around each stage, exchange, tag / remesh and cycle: named spans in any
+// CUPTI / Nsight timeline of a run (tools/timeline.py records the kernels themselves).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 static thread_local std::string g_err;
 static ph_status fail(ph_status s, const std::string& m) {
@@ -1028,6 +1037,7 @@ static ph_status exchange_end(ph_mesh* m, double* U, int which) {
 }
 
 static ph_status exchange(ph_mesh* m, double* U, int which) {
+  NvtxRange nvtx_("ph:exchange");
   cudaEvent_t t0 = nullptr, t1 = nullptr;
   if (m->timing) {
     t0 = pool_event(m);
@@ -1066,6 +1076,7 @@ static ph_status standalone_reduce(ph_mesh* m, double* U, int mode) {
 /* one stage over all local blocks, pack by pack (a2-a5) */
 static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a0, double b1, double cdt,
                            bool reduce, int stage, int s0 = 0, int s1 = -1, bool post = true, bool put = false) {
+  NvtxRange nvtx_(stage == 1 ? "ph:stage1" : "ph:stage2");
   const int nloc = (int)m->local_gids.size();
   if (s1 < 0) s1 = nloc;
   if (m->ho) {
@@ -1195,6 +1206,7 @@ static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, 
                                 int deref_interval = 0);
 
 static ph_status one_cycle(ph_mesh* m) {
+  NvtxRange nvtx_("ph:cycle");
   CU(launch_cycle_begin(m->d_st, 0.0, 0, m->stream));
   m->launches++;
   const bool adaptive = m->cfg.refinement == PH_REF_ADAPTIVE;
@@ -1470,6 +1482,7 @@ static ph_status remesh(ph_mesh* m, const std::unordered_set<LocKey>& leaves, bo
  * this cycle's increment is a multiple of the interval (A16). */
 static ph_status tag_and_remesh(ph_mesh* m, bool refine_only, bool allow_deref, bool move, bool* changed,
                                 int deref_interval) {
+  NvtxRange nvtx_("ph:tag_remesh");
   *changed = false;
   const int nloc = (int)m->local_gids.size();
   const int R = m->nranks;
@@ -1934,7 +1947,10 @@ ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) 
         cudaError_t ec = cudaStreamEndCapture(m->stream, &gr);
         if (st == PH_OK && ec != cudaSuccess) st = fail(PH_ERR_CUDA, std::string("capture: ") + cudaGetErrorString(ec));
         if (st == PH_OK) {
-          cudaError_t ei = cudaGraphInstantiate(&m->graph_exec, gr, 0);
+          // keep the captured stream priorities (the boundary-first schedule's high-priority stream B):
+          // without this flag a graph runs every node at the launching stream's priority, and the
+          // interior blocks' stage kernel can take the GPU before the boundary blocks' one
+          cudaError_t ei = cudaGraphInstantiate(&m->graph_exec, gr, cudaGraphInstantiateFlagUseNodePriority);
           if (ei != cudaSuccess) st = fail(PH_ERR_CUDA, std::string("instantiate: ") + cudaGetErrorString(ei));
         }
         if (gr) cudaGraphDestroy(gr);

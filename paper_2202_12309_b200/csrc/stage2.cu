@@ -20,8 +20,9 @@
 //    state itself), each cell's x slope once, the left neighbour's top state and the right
 //    neighbour's face flux by warp shuffles; y faces j-1/2 per lane with the 4-row stencil read by
 //    128-bit shared loads, face j+1/2 shuffled down from the row above; the warp's top y faces
-//    and its rows' right x faces (20 faces) in one extra round.  z: each column's top state and
-//    last face flux are carried in registers (one slope per cell).
+//    and its rows' right x faces (20 faces) in one extra round, handed to their consumer lanes through
+//    a per-warp shared-memory area.  z: each column's top state and last face flux are carried in
+//    registers (one slope per cell).  The 128 halo cells of a plane are converted one per thread.
 //  * HLLE in the alpha/beta form: with a = b+/(b+ - b-), b = -b-/(b+ - b-), e = a b-,
 //      beta_L = a u_L - e, beta_R = b u_R + e, alpha = rho beta,
 //      F = (alpha_L + alpha_R, u_L alpha_L + u_R alpha_R + a p_L + b p_R, v alpha.., w alpha..,
@@ -31,8 +32,8 @@
 //  * The finish operand of plane c (U^n for stage 1, H = a0 U^n + b1 U^1 for stage 2) is a TMA box
 //    issued at the start of the same step; finished cells leave with 128-bit stores.
 //
-// Shared memory per CTA: ring 4 x 15,360 B + finish 10,240 + reduction 192 + 5 mbarriers = 71,912 B
-// (3 CTAs per SM).
+// Shared memory per CTA: ring 4 x 15,360 B + finish 10,240 + reduction 192 + extra-round faces 3,200
+// + 5 mbarriers = 75,112 B (3 CTAs per SM: 3 x (75,112 + 1,024 reserved) <= 228 KB).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -55,7 +56,8 @@ constexpr int PLANE = R_YH + NVAR * VY;                // 1920 doubles = 15,360 
 constexpr int NSLOT = 4;
 constexpr int OFF_FIN = NSLOT * PLANE;                 // [5][TY][TX]
 constexpr int OFF_RED = OFF_FIN + NVAR * VM;           // [NW][6]
-constexpr int OFF_BAR = OFF_RED + NW * 6;              // full[NSLOT], fin
+constexpr int OFF_FE = OFF_RED + NW * 6;               // [NW][5][20]: the extra round's faces
+constexpr int OFF_BAR = OFF_FE + NW * NVAR * 20;       // full[NSLOT], fin
 constexpr int SMEM_DOUBLES = OFF_BAR + NSLOT + 1;
 constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
 constexpr uint32_t MAIN_BYTES = PLANE * 8;             // centre + 4 halo boxes
@@ -363,25 +365,37 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
     // ---- a2: cons -> prim of plane q, in place
     double wq[2][NVAR];
     convert_pair(Wq + own, VM, gm1, wq, A.err, A.stage, gid, q, y0 + r, x0 + i0);
-    if (mainp && lane < 16) {
-      // 64 halo pairs: x-halo left / right (one per row), y-halo below / above (8 per row)
-      const int h = 16 * warp + lane;
+    if (mainp) {
+      // 128 halo cells, one per thread (no idle half-warps): x-halo left / right (2 per row), y-halo
+      // below / above (16 per row)
+      const int h = tid;
       int off, vs, jj, ii;
-      if (h < 32) {
-        const int rr = h & 15;
-        off = (h < 16 ? R_XL : R_XR) + rr * 2;
+      if (h < 64) {
+        const int rr = (h >> 1) & 15, e = h & 1;
+        off = (h < 32 ? R_XL : R_XR) + rr * 2 + e;
         vs = VX;
         jj = rr;
-        ii = h < 16 ? -2 : TX;
+        ii = (h < 32 ? -2 : TX) + e;
       } else {
-        const int hh = h - 32, hr = (hh >> 3) & 1, cp = hh & 7;
-        off = (hh < 16 ? R_YL : R_YH) + hr * TX + 2 * cp;
+        const int hh = h - 64, hr = (hh >> 4) & 1, col = hh & 15;
+        off = (hh < 32 ? R_YL : R_YH) + hr * TX + col;
         vs = VY;
-        jj = hh < 16 ? hr - 2 : TY + hr;
-        ii = 2 * cp;
+        jj = hh < 32 ? hr - 2 : TY + hr;
+        ii = col;
       }
-      double wh[2][NVAR];
-      convert_pair(Wq + off, vs, gm1, wh, A.err, A.stage, gid, q, y0 + jj, x0 + ii);
+      double u[NVAR];
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) u[v] = Wq[off + v * vs];
+      const double rho = u[0], ir = rcp_nr(rho);
+      const double v1 = u[1] * ir, v2 = u[2] * ir, v3 = u[3] * ir;
+      const double ke = 0.5 * ((u[1] * v1 + u[2] * v2) + u[3] * v3);
+      const double pr = gm1 * (u[4] - ke);
+      if (!(rho > 0.0) || !(pr > 0.0)) set_error(A.err, A.stage, gid, q, y0 + jj, x0 + ii);
+      Wq[off] = rho;
+      Wq[off + vs] = v1;
+      Wq[off + 2 * vs] = v2;
+      Wq[off + 3 * vs] = v3;
+      Wq[off + 4 * vs] = pr;
     }
     ph_jitter(4 * q + 1);
     __syncthreads();  // plane q primitives visible; step q-1 done everywhere (its slot and fin free)
@@ -445,6 +459,15 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
         const int rr = 4 * warp + (lane == 31 ? 3 : lane - TX);
         face4(Wc + R_M + rr * TX + TX - 2, VM, Wc + R_XR + rr * 2, VX, 1, 1, gamma, ggm1, Fe);
       }
+      double* fe = sm + OFF_FE + warp * NVAR * 20;
+      {
+        const int es = lane < TX ? lane : (lane == 31 ? TX + 3 : lane - TX + TX);
+        if (lane < TX + 3 || lane == 31) {
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) fe[v * 20 + es] = Fe[v];
+        }
+      }
+      __syncwarp();
       if (ML) {
         if (lane < TX && warp == NW - 1 && y0 + TY == G.n[1]) ml_put(3, x0 + lane, c, Fe);  // y face n2: [v][k][i]
         if ((lane >= TX && lane < TX + 3) || lane == 31) {
@@ -479,10 +502,10 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
 #pragma unroll
         for (int v = 0; v < NVAR; ++v) {
           double h0 = __shfl_down_sync(0xffffffffu, F0[v], 8), h1 = __shfl_down_sync(0xffffffffu, F1[v], 8);
-          const double e0 = __shfl_sync(0xffffffffu, Fe[v], i0), e1 = __shfl_sync(0xffffffffu, Fe[v], i0 + 1);
           if (kr == 3) {
-            h0 = e0;
-            h1 = e1;
+            const double2 ee = lds2(fe + v * 20 + i0);
+            h0 = ee.x;
+            h1 = ee.y;
           }
           dy[0][v] = (h0 - F0[v]) * idx2;
           dy[1][v] = (h1 - F1[v]) * idx2;
@@ -529,8 +552,7 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
 #pragma unroll
         for (int v = 0; v < NVAR; ++v) {
           double FR = __shfl_down_sync(0xffffffffu, FL[v], 1, 8);
-          const double er = __shfl_sync(0xffffffffu, Fe[v], kr == 3 ? 31 : TX + kr);
-          if (p == 7) FR = er;
+          if (p == 7) FR = fe[v * 20 + TX + kr];
           dx[0][v] = (FM[v] - FL[v]) * idx1;
           dx[1][v] = (FR - FM[v]) * idx1;
         }
