@@ -285,6 +285,65 @@ static bool region_physical(const BlockInfo& b, const int o[3]) {
  * the direct-halo path -- drops the face copies between local same-level blocks (the stage kernel
  * reads those neighbours' interiors directly) and, on uniform meshes, all edge / corner regions
  * (the stage stencil is a plus shape: it never reads them). */
+// Per-cycle plan of a block with coarse staging and no physical face: the staging cells of the first
+// ghost layer at a non-coarser offset op that a prolongation actually reads.  The prolongation of the
+// first ghost layer R_o at each coarser-neighbour offset o takes one minmod slope per dimension over
+// +-1 coarse cell, so it reads R_o +- e_d; the part of that in op's ghost layer, as a bounding box in
+// coarse coordinates [lo, hi).  false: nothing there is read.
+static bool staging_need(const ph_mesh* m, const int kind[27], const int op[3], int lo[3], int hi[3]) {
+  const int* nc = m->G.nc;
+  int glo[3], ghi[3];
+  for (int d = 0; d < 3; ++d) {
+    glo[d] = op[d] < 0 ? -1 : (op[d] > 0 ? nc[d] : 0);
+    ghi[d] = op[d] < 0 ? 0 : (op[d] > 0 ? nc[d] + 1 : nc[d]);
+    lo[d] = 1 << 30;
+    hi[d] = -(1 << 30);
+  }
+  bool any = false;
+  for (int q = 0; q < 27; ++q) {
+    if (q == 13 || kind[q] != -1) continue;
+    const int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
+    int rlo[3], rhi[3];
+    for (int d = 0; d < 3; ++d) {
+      rlo[d] = o[d] < 0 ? -1 : (o[d] > 0 ? nc[d] : 0);
+      rhi[d] = o[d] < 0 ? 0 : (o[d] > 0 ? nc[d] + 1 : nc[d]);
+    }
+    for (int d = 0; d < 3; ++d)
+      for (int sgn = -1; sgn <= 1; sgn += 2) {
+        int a[3], b[3];
+        bool ok = true;
+        for (int e = 0; e < 3; ++e) {
+          a[e] = std::max(rlo[e] + (e == d ? sgn : 0), glo[e]);
+          b[e] = std::min(rhi[e] + (e == d ? sgn : 0), ghi[e]);
+          ok = ok && a[e] < b[e];
+        }
+        if (!ok) continue;
+        any = true;
+        for (int e = 0; e < 3; ++e) {
+          lo[e] = std::min(lo[e], a[e]);
+          hi[e] = std::max(hi[e], b[e]);
+        }
+      }
+  }
+  return any;
+}
+
+static bool any_physical(const BlockInfo& b) {
+  for (int d = 0; d < 3; ++d)
+    if (b.phys_lo[d] || b.phys_hi[d]) return true;
+  return false;
+}
+
+// clip task t's destination box (fine cells) to the fine cells covering coarse box [clo, chi)
+static void clip_to_coarse(XTask& t, const int clo[3], const int chi[3]) {
+  for (int d = 0; d < 3; ++d) {
+    const int a = std::max(t.lo[d], 2 * clo[d]), b = std::min(t.lo[d] + t.ext[d], 2 * chi[d]);
+    t.lo[d] = a;
+    t.ext[d] = std::max(b - a, 0);
+  }
+  t.ncell = t.ext[0] * t.ext[1] * t.ext[2];
+}
+
 static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>& cslot) {
   const int R = m->nranks, me = m->rank;
   for (Phase* ph : P.phases()) {
@@ -305,12 +364,32 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
       const BlockInfo& s = m->blocks[e.gid];
       bool dst_here = (b.rank == me), src_here = (s.rank == me);
       if (!dst_here && !src_here) continue;
+      bool clip = false;
+      int clo[3], chi[3];
       if (cyc && !b.has_coarser) {  // destination without coarse staging (all blocks of a uniform mesh)
         int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
         if (nz > 1) continue;                               // edges / corners: never read
         if (dst_here && src_here && e.dlevel == 0) continue;  // read directly by the stage kernel
+      } else if (cyc && b.has_coarser && e.dlevel >= 0 && !any_physical(b) && !getenv("PH_FULL_STAGING")) {
+        // staged block: the stage kernel reads local same-level faces directly (direct halo); other
+        // faces it reads whole; beyond that, only the ghosts a prolongation slope reads (through
+        // their restriction into the staging's first ghost layer) are needed
+        int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
+        const bool stage_reads = nz == 1 && !(dst_here && src_here && e.dlevel == 0);
+        if (!stage_reads) {
+          int kind[27];
+          for (int q = 0; q < 27; ++q) kind[q] = -2;
+          for (auto& f : b.nbrs) kind[(f.off[2] + 1) * 9 + (f.off[1] + 1) * 3 + (f.off[0] + 1)] = f.dlevel;
+          const int op[3] = {e.off[0], e.off[1], e.off[2]};
+          if (!staging_need(m, kind, op, clo, chi)) continue;
+          clip = true;
+        }
       }
       XTask t = entry_task(m, b, e);
+      if (clip) {
+        clip_to_coarse(t, clo, chi);
+        if (t.ncell == 0) continue;
+      }
       int cs = (t.kind == T_CCOPY) ? cslot[b.gid] : (int)b.local;
       if (dst_here && src_here) {
         t.dst_slot = cs;
@@ -453,6 +532,7 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
         for (const Box& bx : done)
           restrict_box(bx.i0, bx.ie - bx.i0, bx.j0, bx.je - bx.j0, bx.k0, bx.ke - bx.k0);
       }
+      const bool clip1 = cyc && !anyphys && !getenv("PH_FULL_STAGING");
       for (int q = 0; q < 27; ++q) {
         if (q == 13 || kind[q] == -2 || kind[q] == -1) continue;
         int o[3] = {q % 3 - 1, (q / 3) % 3 - 1, q / 9 - 1};
@@ -466,8 +546,17 @@ static void build_exchange(ph_mesh* m, Plan& P, bool cyc, const std::vector<int>
           else { r.lo[d] = 0; r.ext[d] = m->G.nc[d]; }
           r.so[d] = 0;
         }
+        if (clip1) {  // per-cycle plan: only the staging cells a prolongation slope reads (staging_need)
+          int clo[3], chi[3];
+          if (!staging_need(m, kind, o, clo, chi)) continue;
+          for (int d = 0; d < 3; ++d) {
+            const int a = std::max(r.lo[d], clo[d]), e2 = std::min(r.lo[d] + r.ext[d], chi[d]);
+            r.lo[d] = a;
+            r.ext[d] = std::max(e2 - a, 0);
+          }
+        }
         r.ncell = r.ext[0] * r.ext[1] * r.ext[2];
-        add_chunks(P.b1, r, m->G);
+        if (r.ncell > 0) add_chunks(P.b1, r, m->G);
       }
       for (int q = 0; q < 27 && anyphys; ++q) {
         if (q == 13) continue;
@@ -675,7 +764,9 @@ static ph_status build_plan(ph_mesh* m) {
       M.poff[f] = 0;
     }
     M.rfx = 0;
-    if (m->direct_halo && !b.has_coarser) {
+    // direct halo: every block (with coarse staging too, since round 2) reads its local same-level face
+    // neighbours' interiors; the per-cycle plan copies those faces only where the staging needs them
+    if (m->direct_halo && (!b.has_coarser || (!any_physical(b) && !getenv("PH_FULL_STAGING")))) {
       for (auto& e : b.nbrs) {
         int nz = (e.off[0] != 0) + (e.off[1] != 0) + (e.off[2] != 0);
         if (nz != 1 || e.dlevel != 0 || m->blocks[e.gid].rank != me) continue;
