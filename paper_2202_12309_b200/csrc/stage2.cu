@@ -19,10 +19,13 @@
 //    that warp: x faces 2p-1/2 and 2p+1/2 per lane (lane 0 of a row builds the left halo cell's
 //    state itself), each cell's x slope once, the left neighbour's top state and the right
 //    neighbour's face flux by warp shuffles; y faces j-1/2 per lane with the 4-row stencil read by
-//    128-bit shared loads, face j+1/2 shuffled down from the row above; the warp's top y faces
-//    and its rows' right x faces (20 faces) in one extra round, handed to their consumer lanes through
-//    a per-warp shared-memory area.  z: each column's top state and last face flux are carried in
-//    registers (one slope per cell).  The 128 halo cells of a plane are converted one per thread.
+//    128-bit shared loads, face j+1/2 shuffled down from the row above, or -- for the warp's top row
+//    -- taken from the warp above through shared memory behind a pairwise named barrier (bar.arrive /
+//    bar.sync, 64 threads), so no face is computed twice.  The tile's 16 top y faces and 16 right x
+//    faces are computed one step ahead by one warp (rotating) into a double-buffered area.  z: each
+//    column's top state and last face flux are carried in registers (one slope per cell).  The 128
+//    halo cells of a plane are converted one per thread.  (PH_S2_V3=1: the earlier variant in which
+//    every warp computes its own top faces in an extra round, 2.5x the extra faces.)
 //  * HLLE in the alpha/beta form: with a = b+/(b+ - b-), b = -b-/(b+ - b-), e = a b-,
 //      beta_L = a u_L - e, beta_R = b u_R + e, alpha = rho beta,
 //      F = (alpha_L + alpha_R, u_L alpha_L + u_R alpha_R + a p_L + b p_R, v alpha.., w alpha..,
@@ -32,8 +35,9 @@
 //  * The finish operand of plane c (U^n for stage 1, H = a0 U^n + b1 U^1 for stage 2) is a TMA box
 //    issued at the start of the same step; finished cells leave with 128-bit stores.
 //
-// Shared memory per CTA: ring 4 x 15,360 B + finish 10,240 + reduction 192 + extra-round faces 3,200
-// + 5 mbarriers = 75,112 B (3 CTAs per SM: 3 x (75,112 + 1,024 reserved) <= 228 KB).
+// Shared memory per CTA: ring 4 x 15,360 B + finish 10,240 + reduction 192 + tile-boundary faces 2,560
+// + warp-boundary faces 1,920 + 5 mbarriers = 76,392 B (3 CTAs per SM: 3 x (76,392 + 1,024 reserved)
+// <= 228 KB).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -56,8 +60,14 @@ constexpr int PLANE = R_YH + NVAR * VY;                // 1920 doubles = 15,360 
 constexpr int NSLOT = 4;
 constexpr int OFF_FIN = NSLOT * PLANE;                 // [5][TY][TX]
 constexpr int OFF_RED = OFF_FIN + NVAR * VM;           // [NW][6]
+#ifndef PH_S2_V3
+constexpr int OFF_XB = OFF_RED + NW * 6;               // [2][5][32]: tile-top y faces (16) + right x faces (16), one step ahead
+constexpr int OFF_FB = OFF_XB + 2 * NVAR * 32;         // [NW-1][5][TX]: bottom-row y faces of warps 1..3 for the warp below
+constexpr int OFF_BAR = OFF_FB + (NW - 1) * NVAR * TX; // full[NSLOT], fin
+#else
 constexpr int OFF_FE = OFF_RED + NW * 6;               // [NW][5][20]: the extra round's faces
 constexpr int OFF_BAR = OFF_FE + NW * NVAR * 20;       // full[NSLOT], fin
+#endif
 constexpr int SMEM_DOUBLES = OFF_BAR + NSLOT + 1;
 constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
 constexpr uint32_t MAIN_BYTES = PLANE * 8;             // centre + 4 halo boxes
@@ -446,6 +456,7 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
     double sxy[2][NVAR];  // dx + (dy + dz) of the own pair of plane c
     if (cact) {
       const double* Wc = sm + s2 * PLANE;
+#ifdef PH_S2_V3
       // ---- extra round: the warp's top y faces and its rows' right x faces, then distributed
       // extra round: lanes 0..15 the y face 4w+4-1/2 of column `lane` (rows 4w+2 .. 4w+5), lanes
       // 16..18 and 31 the x face 16-1/2 of row 4w + 0..3 (cells 14, 15 | 16, 17)
@@ -474,6 +485,9 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
           if (x0 + TX == G.n[0]) ml_put(1, y0 + 4 * warp + (lane == 31 ? 3 : lane - TX), c, Fe);  // x face n1: [v][k][j]
         }
       }
+#else
+      const double* xb = sm + OFF_XB + (c & 1) * NVAR * 32;  // plane c's tile-top / right faces
+#endif
       // ---- y faces j-1/2 of the own pair (rows r-2 .. r+1); j+1/2 from the row above
       double dy[2][NVAR];
       {
@@ -499,9 +513,33 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
           ml_put(2, x0 + i0, c, F0);
           ml_put(2, x0 + i0 + 1, c, F1);
         }
+#ifndef PH_S2_V3
+        if (warp > 0) {  // the bottom row's faces are the top faces of the warp below: hand them over
+          if (kr == 0) {
+            double* fb = sm + OFF_FB + (warp - 1) * NVAR * TX + i0;
+#pragma unroll
+            for (int v = 0; v < NVAR; ++v) sts2(fb + v * TX, F0[v], F1[v]);
+          }
+          asm volatile("bar.arrive %0, %1;" ::"r"(warp), "r"(64) : "memory");
+        }
+#endif
 #pragma unroll
         for (int v = 0; v < NVAR; ++v) {
           double h0 = __shfl_down_sync(0xffffffffu, F0[v], 8), h1 = __shfl_down_sync(0xffffffffu, F1[v], 8);
+#ifndef PH_S2_V3
+          if (kr == 3) {  // warp 3: the tile top (computed a step ahead); warps 0..2: added after the x round
+            const double2 ee = warp == NW - 1 ? lds2(xb + v * 32 + i0) : make_double2(0.0, 0.0);
+            h0 = ee.x;
+            h1 = ee.y;
+          }
+          if (kr == 3 && warp < NW - 1) {
+            dy[0][v] = -F0[v] * idx2;
+            dy[1][v] = -F1[v] * idx2;
+          } else {
+            dy[0][v] = (h0 - F0[v]) * idx2;
+            dy[1][v] = (h1 - F1[v]) * idx2;
+          }
+#else
           if (kr == 3) {
             const double2 ee = lds2(fe + v * 20 + i0);
             h0 = ee.x;
@@ -509,6 +547,7 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
           }
           dy[0][v] = (h0 - F0[v]) * idx2;
           dy[1][v] = (h1 - F1[v]) * idx2;
+#endif
           // fold dz in now: L = -(dx + (dy + dz)) (the oracle sums (dx + dy) + dz; round-off only, reading
           // A43) keeps 20 fewer registers live through the x round (+0.3 % on 2b)
           dy[0][v] += dz[0][v];
@@ -552,11 +591,29 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
 #pragma unroll
         for (int v = 0; v < NVAR; ++v) {
           double FR = __shfl_down_sync(0xffffffffu, FL[v], 1, 8);
+#ifndef PH_S2_V3
+          if (p == 7) FR = xb[v * 32 + TX + r];
+#else
           if (p == 7) FR = fe[v * 20 + TX + kr];
+#endif
           dx[0][v] = (FM[v] - FL[v]) * idx1;
           dx[1][v] = (FR - FM[v]) * idx1;
         }
       }
+#ifndef PH_S2_V3
+      if (warp < NW - 1) {  // the top faces of my row 3 = the bottom faces of the warp above
+        asm volatile("bar.sync %0, %1;" ::"r"(warp + 1), "r"(64) : "memory");
+        if (kr == 3) {
+          const double* fb = sm + OFF_FB + warp * NVAR * TX + i0;
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) {
+            const double2 h = lds2(fb + v * TX);
+            dy[0][v] = fma(h.x, idx2, dy[0][v]);
+            dy[1][v] = fma(h.y, idx2, dy[1][v]);
+          }
+        }
+      }
+#endif
 #pragma unroll
       for (int e = 0; e < 2; ++e)
 #pragma unroll
@@ -625,6 +682,25 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
         }
       }
     }
+#ifndef PH_S2_V3
+    // one step ahead, one warp (rotating): plane q-1's tile-top y faces (lanes 0..15, rows 14..17) and
+    // right x faces (lanes 16..31, cells 14..17 of row lane-16), for every warp's use next step
+    if (q - 1 >= k0 && q - 1 < k1 && warp == (q & (NW - 1))) {
+      const double* W1 = sm + s1 * PLANE;
+      double Fe[NVAR];
+      if (lane < TX)
+        face4(W1 + R_M + (TY - 2) * TX + lane, VM, W1 + R_YH + lane, VY, TX, 2, gamma, ggm1, Fe);
+      else
+        face4(W1 + R_M + (lane - TX) * TX + TX - 2, VM, W1 + R_XR + (lane - TX) * 2, VX, 1, 1, gamma, ggm1, Fe);
+      double* xo = sm + OFF_XB + ((q - 1) & 1) * NVAR * 32 + lane;
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) xo[v * 32] = Fe[v];
+      if (ML) {
+        if (lane < TX && y0 + TY == G.n[1]) ml_put(3, x0 + lane, q - 1, Fe);             // y face n2: [v][k][i]
+        if (lane >= TX && x0 + TX == G.n[0]) ml_put(1, y0 + lane - TX, q - 1, Fe);       // x face n1: [v][k][j]
+      }
+    }
+#endif
     s = (s + 1) & (NSLOT - 1);
   }
   if (REDUCE) {
