@@ -831,7 +831,11 @@ static ph_status setup_device(ph_mesh* m) {
   if (m->frbuf_n) TRY(dalloc(m, (void**)&m->frbuf, m->frbuf_n * sizeof(double)));
   if (m->sbuf_n) TRY(dalloc(m, (void**)&m->sbuf, m->sbuf_n * sizeof(double)));
   if (m->rbuf_n) TRY(dalloc(m, (void**)&m->rbuf, m->rbuf_n * sizeof(double)));
-  // stage launch geometry
+  // stage launch geometry.  A mesh of fewer than 8 stage2 tiles (16 x 16 columns) in total -- config 1,
+  // one 32^3 block, has 4 -- runs the round-1 kernel, whose lighter prologue suits the k-split CTAs of
+  // a few planes such a mesh needs (config 1: 24.9 vs 28.1 us per cycle).  Decided on the global block
+  // count, so every rank and every rank count pick the same kernel (N GPUs stay bitwise equal to one).
+  m->G.no_stage2 = ((int64_t)m->blocks.size() * (G.n[0] / 16) * (G.n[1] / 16) < 8) ? 1 : 0;
   int tile_x = TX, tile_y = TY;
   const bool full_tile = stage_tile(G, m->cfg.recon, m->fbuf != nullptr, &tile_x, &tile_y);
   m->ntx = (G.n[0] + tile_x - 1) / tile_x;

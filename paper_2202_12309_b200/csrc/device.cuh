@@ -25,6 +25,7 @@ struct Geom {
   double cfl;
   int exact;       // 1: high-order path computes in the oracle's exact operation order (NEXT 3)
   int wavespeed;   // HLLE wave speeds: 0 Davis, 1 Einfeldt (A4)
+  int no_stage2;   // 1: the mesh is too small to fill the GPU with stage2's 16x16 tiles (round-1 kernel)
 };
 
 // Per local block slot.

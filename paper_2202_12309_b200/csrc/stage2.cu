@@ -420,6 +420,25 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
     }
 
     double dz[2][NVAR];
+#if !defined(PH_S2_V3) && defined(PH_S2_XSTART)
+    // one step ahead, one warp (rotating): plane q-1's tile-top y faces (lanes 0..15, rows 14..17) and
+    // right x faces (lanes 16..31, cells 14..17 of row lane-16), for every warp's use next step
+    if (q - 1 >= k0 && q - 1 < k1 && warp == (q & (NW - 1))) {
+      const double* W1 = sm + s1 * PLANE;
+      double Fe[NVAR];
+      if (lane < TX)
+        face4(W1 + R_M + (TY - 2) * TX + lane, VM, W1 + R_YH + lane, VY, TX, 2, gamma, ggm1, Fe);
+      else
+        face4(W1 + R_M + (lane - TX) * TX + TX - 2, VM, W1 + R_XR + (lane - TX) * 2, VX, 1, 1, gamma, ggm1, Fe);
+      double* xo = sm + OFF_XB + ((q - 1) & 1) * NVAR * 32 + lane;
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) xo[v * 32] = Fe[v];
+      if (ML) {
+        if (lane < TX && y0 + TY == G.n[1]) ml_put(3, x0 + lane, q - 1, Fe);             // y face n2: [v][k][i]
+        if (lane >= TX && x0 + TX == G.n[0]) ml_put(1, y0 + lane - TX, q - 1, Fe);       // x face n1: [v][k][j]
+      }
+    }
+#endif
     // ---- z: slope of plane q-1 (own pair), face q-1 between planes q-2 and q-1
     if (idx >= 2) {
       const double* pm = sm + s2 * PLANE + own;
@@ -682,7 +701,7 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
         }
       }
     }
-#ifndef PH_S2_V3
+#if !defined(PH_S2_V3) && !defined(PH_S2_XSTART)
     // one step ahead, one warp (rotating): plane q-1's tile-top y faces (lanes 0..15, rows 14..17) and
     // right x faces (lanes 16..31, cells 14..17 of row lane-16), for every warp's use next step
     if (q - 1 >= k0 && q - 1 < k1 && warp == (q & (NW - 1))) {
@@ -780,6 +799,7 @@ static cudaError_t launch_t(int nctas, const StageArgs& a, const Maps& mp, const
 bool stage2_applies(const Geom& G, int recon, bool ml) {
   (void)ml;  // multilevel meshes too (flux slots, template ML)
   if (getenv("PH_STAGE_V1") || getenv("PH_NO_HBASE")) return false;  // it needs the stage-2 base pool H
+  if (G.no_stage2) return false;
   return recon == 0 && G.wavespeed == 0 && G.g == 2 && G.n[0] % s2::TX == 0 && G.n[1] % s2::TY == 0 &&
          G.n[0] >= s2::TX && G.n[1] >= s2::TY;
 }
