@@ -217,6 +217,11 @@ cudaError_t launch_rfx_reduce(const int2* faces, int nfaces, const double* U, co
 cudaError_t launch_tag(const double* U, const BlockMeta* meta, int nslots, unsigned long long* eps_bits,
                        double* partials, ErrWord* err, const Geom& G, cudaStream_t s);
 int tag_ctas_per_block(const Geom& G);
+// stage2.cu: the TMA-fed tag pass (16 x 16 tiles) for blocks whose x / y extents are multiples of 16
+bool tag2_applies(const Geom& G);
+int tag2_ctas_per_block(const Geom& G);
+cudaError_t launch_tag2(const double* U, const BlockMeta* meta, int nslots, unsigned long long* eps_bits,
+                        double* partials, ErrWord* err, const Geom& G, cudaStream_t s);
 cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, double* Unew, const double* rbuf,
                           double* sbuf, const Geom& G, cudaStream_t s);
 cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslots, const StageArgs& a, double* W,

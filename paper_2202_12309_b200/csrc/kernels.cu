@@ -1712,7 +1712,10 @@ __global__ void __launch_bounds__(TGT, 4) tag_kernel(const double* U, const Bloc
   }
 }
 
-int tag_ctas_per_block(const Geom& G) { return ((G.n[0] + TGX - 1) / TGX) * ((G.n[1] + TGY - 1) / TGY); }
+int tag_ctas_per_block(const Geom& G) {
+  if (tag2_applies(G)) return tag2_ctas_per_block(G);
+  return ((G.n[0] + TGX - 1) / TGX) * ((G.n[1] + TGY - 1) / TGY);
+}
 
 // new pool <- old pool (see RemeshTask): same-level move, 8-child prolongation of a refined parent
 // using the parent's valid ghosts for the slopes (A11), pairwise restriction of derefined
@@ -2053,6 +2056,7 @@ cudaError_t launch_tag(const double* U, const BlockMeta* meta, int nslots, unsig
   if (nslots <= 0) return cudaSuccess;
   cudaError_t e = cudaMemsetAsync(eps_bits, 0, sizeof(unsigned long long) * nslots, s);
   if (e != cudaSuccess) return e;
+  if (tag2_applies(G)) return launch_tag2(U, meta, nslots, eps_bits, partials, err, G, s);  // stage2.cu
   const int tiles = ((G.n[0] + TGX - 1) / TGX) * ((G.n[1] + TGY - 1) / TGY);
   tag_kernel<<<nslots * tiles, TGT, 0, s>>>(U, meta, eps_bits, partials, err, G);
   return cudaGetLastError();

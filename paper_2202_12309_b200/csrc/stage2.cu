@@ -794,6 +794,170 @@ static cudaError_t launch_t(int nctas, const StageArgs& a, const Maps& mp, const
   return cudaGetLastError();
 }
 
+// ------------------------------------------------------------------------------ AMR tag pass
+// tag2_kernel: the AMR indicator eps_B (O9, A14, arithmetic A46) of every block, fused with the dt /
+// totals partials of the unchanged mesh (a6, a10) -- the same per-cell formulas as tag_kernel
+// (kernels.cu), re-mapped like stage2: 16 x 16 tiles of x-pairs, planes by TMA (the same boxes and
+// direct halo) into a 2-slot cons ring, pressures into a 3-plane ring with a 1-cell halo, one
+// __syncthreads per plane.  Pressures and eps are bit-identical to tag_kernel's.
+constexpr int PW = TX + 2, PH = TY + 2, PPL = PW * PH;  // pressure plane with its 1-cell halo
+constexpr int T_OFF_P = 2 * PLANE;                      // [3][PH][PW]
+constexpr int T_OFF_RED = T_OFF_P + 3 * PPL;            // [NW][7]
+constexpr int T_OFF_BAR = T_OFF_RED + NW * 7;           // full[2]
+constexpr size_t TAG_SMEM = (T_OFF_BAR + 2) * sizeof(double);
+
+__global__ void __launch_bounds__(NTH, 4) tag2_kernel(const double* U, const BlockMeta* meta,
+                                                      unsigned long long* eps_bits, double* partials, ErrWord* err,
+                                                      Geom G, const __grid_constant__ Maps maps) {
+  extern __shared__ __align__(128) double sm[];
+  double* Pr = sm + T_OFF_P;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + T_OFF_BAR);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int kr = lane >> 3, r = (warp << 2) + kr, p = lane & 7, i0 = 2 * p;
+  const int ntx = G.n[0] / TX, nty = G.n[1] / TY;
+  int b = blockIdx.x;
+  const int txi = b % ntx;
+  b /= ntx;
+  const int tyi = b % nty;
+  const int slot = b / nty;
+  const BlockMeta& M = meta[slot];
+  const int x0 = txi * TX, y0 = tyi * TY, g = G.g, n3 = G.n[2];
+  const double gm1 = G.gm1, gamma = G.gamma;
+  const double idx1 = M.idx[0], idx2 = M.idx[1], idx3 = M.idx[2];
+  const int own = R_M + r * TX + i0;
+
+  auto issue_plane = [&](int q, int sl) {  // tid 0 only: main boxes for q in [0, n3), own rows for z halos
+    uint64_t* fb = bar + sl;
+    double* base = sm + sl * PLANE;
+    fence_proxy_async();
+    if (q >= 0 && q < n3) {
+      const int n1 = G.n[0], n2 = G.n[1];
+      const int nb0 = M.nb[0], nb1 = M.nb[1], nb2 = M.nb[2], nb3 = M.nb[3];
+      const bool dl = x0 == 0 && nb0 >= 0, dr = x0 + TX == n1 && nb1 >= 0;
+      const bool db = y0 == 0 && nb2 >= 0, dt = y0 + TY == n2 && nb3 >= 0;
+      mbar_expect_tx(fb, MAIN_BYTES);
+      const int z = q + g;
+      tma5(base + R_M, &maps.c, x0 + g, y0 + g, z, 0, slot, fb);
+      tma5(base + R_XL, &maps.xh, dl ? n1 - 2 + g : x0 - 2 + g, y0 + g, z, 0, dl ? nb0 : slot, fb);
+      tma5(base + R_XR, &maps.xh, dr ? g : x0 + TX + g, y0 + g, z, 0, dr ? nb1 : slot, fb);
+      tma5(base + R_YL, &maps.yh, x0 + g, db ? n2 - 2 + g : y0 - 2 + g, z, 0, db ? nb2 : slot, fb);
+      tma5(base + R_YH, &maps.yh, x0 + g, dt ? g : y0 + TY + g, z, 0, dt ? nb3 : slot, fb);
+    } else {
+      int bb = slot, qq = q;
+      const int zl = M.nb[4], zh = M.nb[5];
+      if (q < 0 && zl >= 0) { bb = zl; qq += n3; }
+      else if (q >= n3 && zh >= 0) { bb = zh; qq -= n3; }
+      mbar_expect_tx(fb, OWN_BYTES);
+      tma5(base + R_M, &maps.c, x0 + g, y0 + g, qq + g, 0, bb, fb);
+    }
+  };
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.c)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.xh)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.yh)) : "memory");
+    mbar_init(bar, 1);
+    mbar_init(bar + 1, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // pressure with the stage kernels' (and tag_kernel's) arithmetic; the dt / totals terms of own cells
+  double mx = 0.0, tmax = 0.0, ts[NVAR] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  auto pressure = [&](const double* u, int vs, int q, int j, int i, bool own_cell) -> double {
+    const double rho = u[0], m1 = u[vs], m2 = u[2 * vs], m3 = u[3 * vs], E = u[4 * vs];
+    const double fr = rcp_nr(rho);
+    const double w1 = m1 * fr, w2 = m2 * fr, w3 = m3 * fr;
+    const double fke = 0.5 * ((m1 * w1 + m2 * w2) + m3 * w3);
+    const double pr = gm1 * (E - fke);
+    if (own_cell) {
+      if (!(rho > 0.0) || !(pr > 0.0)) set_error(err, 0, M.gid, q, y0 + j, x0 + i);
+      const double cs = sound_speed(rho, pr, gamma);
+      const double s1 = (fabs(w1) + cs) * idx1, s2 = (fabs(w2) + cs) * idx2, s3 = (fabs(w3) + cs) * idx3;
+      tmax = dmax(tmax, dmax(s1, dmax(s2, s3)));
+      ts[0] += rho;
+      ts[1] += m1;
+      ts[2] += m2;
+      ts[3] += m3;
+      ts[4] += E;
+    }
+    return pr;
+  };
+  if (tid == 0) issue_plane(-1, 0);
+#pragma unroll 1
+  for (int q = -1; q <= n3; ++q) {
+    const int idx = q + 1, sl = idx & 1;
+    const double* Wq = sm + sl * PLANE;
+    double* Pq = Pr + (idx % 3) * PPL;
+    mbar_wait(bar + sl, (uint32_t)(idx >> 1) & 1u);
+    const bool mainp = q >= 0 && q < n3;
+    {  // own pair
+      const double pa = pressure(Wq + own, VM, q, r, i0, mainp), pb = pressure(Wq + own + 1, VM, q, r, i0 + 1, mainp);
+      Pq[(r + 1) * PW + i0 + 1] = pa;
+      Pq[(r + 1) * PW + i0 + 2] = pb;
+    }
+    if (mainp && tid < 64) {  // the 1-cell halo ring of the tile: x columns -1 / 16, y rows -1 / 16
+      int off, vs, pj, pi;
+      if (tid < 32) {
+        const int rr = tid & 15;
+        off = tid < 16 ? R_XL + rr * 2 + 1 : R_XR + rr * 2;
+        vs = VX;
+        pj = rr + 1;
+        pi = tid < 16 ? 0 : TX + 1;
+      } else {
+        const int t = tid - 32, col = t & 15;
+        off = t < 16 ? R_YL + TX + col : R_YH + col;
+        vs = VY;
+        pj = t < 16 ? 0 : TY + 1;
+        pi = col + 1;
+      }
+      Pq[pj * PW + pi] = pressure(Wq + off, vs, q, pj - 1, pi - 1, false);
+    }
+    ph_jitter(q + 7);
+    __syncthreads();  // plane q's pressures visible; slot sl free for plane q + 2
+    if (tid == 0 && q + 1 <= n3) issue_plane(q + 1, sl ^ 1);
+    const int c = q - 1;  // plane whose indicator is complete now
+    if (c >= 0) {
+      const double* Pm = Pr + ((idx + 1) % 3) * PPL;  // plane q-2
+      const double* P0 = Pr + ((idx + 2) % 3) * PPL;  // plane q-1
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int o = (r + 1) * PW + i0 + 1 + e;
+        const double g1 = 0.5 * (P0[o + 1] - P0[o - 1]);
+        const double g2 = 0.5 * (P0[o + PW] - P0[o - PW]);
+        const double g3 = 0.5 * (Pq[o] - Pm[o]);
+        const double ss = (g1 * g1 + g2 * g2) + g3 * g3;
+        const double ev = ss > 0.0 ? (ss * rsqrt_nr(ss)) * rcp_nr(P0[o]) : 0.0;
+        mx = fmax(mx, ev);
+      }
+    }
+    __syncthreads();  // the pressure ring slot of plane q-2 is rewritten next step (plane q+1)
+  }
+  for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+  if (lane == 0) atomicMax(eps_bits + slot, (unsigned long long)__double_as_longlong(mx));
+  if (partials) {  // deterministic: warp shuffles, then thread 0 in warp order
+    for (int off = 16; off > 0; off >>= 1) {
+      tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) ts[v] += __shfl_xor_sync(0xffffffffu, ts[v], off);
+    }
+    double* red = sm + T_OFF_RED;
+    if (lane == 0) {
+      red[warp * 7] = tmax;
+      for (int v = 0; v < NVAR; ++v) red[warp * 7 + 1 + v] = ts[v];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double m = 0.0, su[NVAR] = {0, 0, 0, 0, 0};
+      for (int w = 0; w < NW; ++w) {
+        m = fmax(m, red[w * 7]);
+        for (int v = 0; v < NVAR; ++v) su[v] += red[w * 7 + 1 + v];
+      }
+      double* o = partials + (int64_t)blockIdx.x * 6;
+      o[0] = m;
+      for (int v = 0; v < NVAR; ++v) o[1 + v] = su[v] * M.dV;
+    }
+  }
+}
+
 }  // namespace s2
 
 bool stage2_applies(const Geom& G, int recon, bool ml) {
@@ -802,6 +966,31 @@ bool stage2_applies(const Geom& G, int recon, bool ml) {
   if (G.no_stage2) return false;
   return recon == 0 && G.wavespeed == 0 && G.g == 2 && G.n[0] % s2::TX == 0 && G.n[1] % s2::TY == 0 &&
          G.n[0] >= s2::TX && G.n[1] >= s2::TY;
+}
+
+bool tag2_applies(const Geom& G) {
+  if (getenv("PH_STAGE_V1") || getenv("PH_TAG_V1")) return false;
+  return G.g == 2 && G.n[0] % s2::TX == 0 && G.n[1] % s2::TY == 0 && G.n[0] >= s2::TX && G.n[1] >= s2::TY;
+}
+
+int tag2_ctas_per_block(const Geom& G) { return (G.n[0] / s2::TX) * (G.n[1] / s2::TY); }
+
+cudaError_t launch_tag2(const double* U, const BlockMeta* meta, int nslots, unsigned long long* eps_bits,
+                        double* partials, ErrWord* err, const Geom& G, cudaStream_t s) {
+  s2::Maps mp;
+  cudaError_t e;
+  if ((e = s2::make_map(&mp.c, U, G, nslots, s2::TX, s2::TY)) != cudaSuccess) return e;
+  if ((e = s2::make_map(&mp.xh, U, G, nslots, 2, s2::TY)) != cudaSuccess) return e;
+  if ((e = s2::make_map(&mp.yh, U, G, nslots, s2::TX, 2)) != cudaSuccess) return e;
+  mp.f = mp.c;
+  static bool attr = false;
+  if (!attr) {
+    e = cudaFuncSetAttribute(s2::tag2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2::TAG_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  s2::tag2_kernel<<<nslots * tag2_ctas_per_block(G), s2::NTH, s2::TAG_SMEM, s>>>(U, meta, eps_bits, partials, err, G, mp);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_stage2(bool reduce, bool use_u0, int nctas, const StageArgs& a, const Geom& G, cudaStream_t s) {

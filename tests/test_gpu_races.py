@@ -35,7 +35,7 @@ for name in sys.argv[1].split(','):
 print(json.dumps(out))
 """
 
-CASES = "wave1,blast2,smr,amr,sod,ho"
+CASES = "wave1,blast2,smr,amr,amr16,sod,ho"
 
 
 def _run(lib):

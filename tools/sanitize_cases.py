@@ -6,6 +6,7 @@
   blast2  2 blocks of 64^3: stage2 with direct halo between blocks, both stages, H path
   smr     static 2-level mesh of 32^3 blocks: stage2 ML (flux slots), exchange phases, reflux, rfx_reduce
   amr     adaptive 3-level mesh of 8^3 blocks: the round-1 stage kernel, tag, remesh, prolong / restrict
+  amr16   adaptive 3-level mesh of 16^3 blocks: stage2 ML, the TMA tag pass (tag2), remesh
   sod     thin Sod with outflow / reflect walls (16^3 blocks): physical BCs in the exchange
   ho      PPM with nghost 3: the exact-arithmetic high-order path
 """
@@ -23,6 +24,8 @@ CASES = {
                  regions=[(1, -0.1, 0.1, -0.1, 0.1, -0.1, 0.1)]), 2, [10.0, 0.1, 0.1], 2),
     "amr": (dict(mesh_nx=(32,) * 3, block_nx=(8,) * 3, xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=2, refinement=2,
                  refine_tol=0.1, derefine_tol=0.025, derefine_interval=2), 2, [10.0, 0.1, 0.1], 3),
+    "amr16": (dict(mesh_nx=(64,) * 3, block_nx=(16,) * 3, xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=2, refinement=2,
+                   refine_tol=0.1, derefine_tol=0.025, derefine_interval=2), 2, [10.0, 0.1, 0.1], 3),
     "sod": (dict(mesh_nx=(64, 16, 16), block_nx=(16,) * 3, gamma=1.4, bc_inner=(1, 2, 0), bc_outer=(1, 2, 0)), 1,
             [0.5], 3),
     "ho": (dict(mesh_nx=(32,) * 3, block_nx=(16,) * 3, xmin=(-.5,) * 3, xmax=(.5,) * 3, recon=3, nghost=3), 2,
