@@ -1666,7 +1666,8 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
   if (cfg->recon >= PH_RECON_PPM && cfg->nghost != 3) return fail(PH_ERR_CONFIG, "PPM / WENO-Z need nghost = 3 (A8)");
   if (cfg->nghost == 3 && cfg->max_level > 0 && cfg->refinement != PH_REF_NONE)
     return fail(PH_ERR_CONFIG, "nghost = 3 is supported on uniform meshes only (reading A39)");
-  if (!(cfg->gamma > 1.0) || !(cfg->cfl > 0.0)) return fail(PH_ERR_CONFIG, "gamma must exceed 1 and cfl be positive");
+  if (!(cfg->gamma > 1.0) || !(cfg->gamma < 0x1p50) || !(cfg->cfl > 0.0))  // (gamma < 2^50: ddiv_k's range)
+    return fail(PH_ERR_CONFIG, "gamma must lie in (1, 2^50) and cfl be positive");
   if (cfg->nranks < 1 || cfg->nranks > 64 || cfg->rank < 0 || cfg->rank >= cfg->nranks)
     return fail(PH_ERR_INVALID_ARG, "bad rank / nranks");
   if (cfg->recon < 0 || cfg->recon > 4 || cfg->integrator < 0 || cfg->integrator > 1)

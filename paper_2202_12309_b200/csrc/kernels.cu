@@ -101,6 +101,7 @@ __device__ __forceinline__ void hlle(const double* wl, const double* wr, const G
 // nonlinear weights and PPM's extremum switch amplify round-off (a smoothness indicator that is 0
 // on one side and 1e-33 on the other changes a weight by 40 orders of magnitude), so the
 // high-order path computes bit for bit what the oracle computes: parity is then exact.
+
 __device__ __forceinline__ double slope_rn(double qm, double q0, double qp, int recon) {
   const double dl = __dsub_rn(q0, qm), dr = __dsub_rn(qp, q0);
   const bool same = (dl > 0.0 && dr > 0.0) || (dl < 0.0 && dr < 0.0);
@@ -132,8 +133,8 @@ __device__ __forceinline__ double ppm_dm_rn(double a, double b, double c) {
 // dm_m, dm_0, dm_p (cells c-1, c, c+1); split out so a line march can reuse each slope three times.
 __device__ __forceinline__ void ppm_lr_rn(double qm, double c, double qp, double dm_m, double dm_0, double dm_p,
                                           double& ql, double& qr) {
-  double L = __dsub_rn(__dadd_rn(qm, __dmul_rn(0.5, __dsub_rn(c, qm))), __ddiv_rn(__dsub_rn(dm_0, dm_m), 6.0));
-  double R = __dsub_rn(__dadd_rn(c, __dmul_rn(0.5, __dsub_rn(qp, c))), __ddiv_rn(__dsub_rn(dm_p, dm_0), 6.0));
+  double L = __dsub_rn(__dadd_rn(qm, __dmul_rn(0.5, __dsub_rn(c, qm))), ddiv_k(__dsub_rn(dm_0, dm_m), K6, RK6));
+  double R = __dsub_rn(__dadd_rn(c, __dmul_rn(0.5, __dsub_rn(qp, c))), ddiv_k(__dsub_rn(dm_p, dm_0), K6, RK6));
   if (__dmul_rn(__dsub_rn(R, c), __dsub_rn(c, L)) <= 0.0) {
     L = c;
     R = c;
@@ -166,9 +167,9 @@ __device__ __forceinline__ double wenoz_rn(double a, double b, double c, double 
   const double a0 = __dmul_rn(0.1, __dadd_rn(1.0, __dmul_rn(r0, r0)));
   const double a1 = __dmul_rn(0.6, __dadd_rn(1.0, __dmul_rn(r1, r1)));
   const double a2 = __dmul_rn(0.3, __dadd_rn(1.0, __dmul_rn(r2, r2)));
-  const double q0 = __ddiv_rn(__dadd_rn(__dsub_rn(__dmul_rn(2.0, a), __dmul_rn(7.0, b)), __dmul_rn(11.0, c)), 6.0);
-  const double q1 = __ddiv_rn(__dadd_rn(__dadd_rn(-b, __dmul_rn(5.0, c)), __dmul_rn(2.0, d)), 6.0);
-  const double q2 = __ddiv_rn(__dsub_rn(__dadd_rn(__dmul_rn(2.0, c), __dmul_rn(5.0, d)), e), 6.0);
+  const double q0 = ddiv_k(__dadd_rn(__dsub_rn(__dmul_rn(2.0, a), __dmul_rn(7.0, b)), __dmul_rn(11.0, c)), K6, RK6);
+  const double q1 = ddiv_k(__dadd_rn(__dadd_rn(-b, __dmul_rn(5.0, c)), __dmul_rn(2.0, d)), K6, RK6);
+  const double q2 = ddiv_k(__dsub_rn(__dadd_rn(__dmul_rn(2.0, c), __dmul_rn(5.0, d)), e), K6, RK6);
   return __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(a0, q0), __dmul_rn(a1, q1)), __dmul_rn(a2, q2)),
                    __dadd_rn(__dadd_rn(a0, a1), a2));
 }
@@ -188,10 +189,10 @@ __device__ __forceinline__ void recon_face6_rn(const double* q, double& wl, doub
   }
 }
 
-__device__ __forceinline__ void phys_rn(const double* W, double gm1, double* U, double* F) {
+__device__ __forceinline__ void phys_rn(const double* W, double gm1, double igm1, double* U, double* F) {
   const double rho = W[0], u = W[1], v = W[2], w = W[3], p = W[4];
   const double mu = __dmul_rn(rho, u);
-  const double E = __dadd_rn(__ddiv_rn(p, gm1), __dmul_rn(__dmul_rn(0.5, rho),
+  const double E = __dadd_rn(ddiv_k(p, gm1, igm1), __dmul_rn(__dmul_rn(0.5, rho),
                                                          __dadd_rn(__dmul_rn(u, u), __dadd_rn(__dmul_rn(v, v), __dmul_rn(w, w)))));
   U[0] = rho; U[1] = mu; U[2] = __dmul_rn(rho, v); U[3] = __dmul_rn(rho, w); U[4] = E;
   F[0] = mu; F[1] = __dadd_rn(__dmul_rn(mu, u), p); F[2] = __dmul_rn(mu, v); F[3] = __dmul_rn(mu, w);
@@ -208,8 +209,8 @@ __device__ __forceinline__ void hlle_rn(const double* WL, const double* WR, cons
   const double sr = a > b ? a : b;
   const double bp = sr > 0.0 ? sr : 0.0, bm = sl < 0.0 ? sl : 0.0;
   double UL[NVAR], FL[NVAR], UR[NVAR], FR[NVAR];
-  phys_rn(WL, G.gm1, UL, FL);
-  phys_rn(WR, G.gm1, UR, FR);
+  phys_rn(WL, G.gm1, G.inv_gm1, UL, FL);
+  phys_rn(WR, G.gm1, G.inv_gm1, UR, FR);
   const double inv = __ddiv_rn(1.0, __dsub_rn(bp, bm));
   const double bb = __dmul_rn(bp, bm);
 #pragma unroll

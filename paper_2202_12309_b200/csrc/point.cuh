@@ -84,4 +84,22 @@ __device__ __forceinline__ void ph_jitter(unsigned salt) {
 #endif
 }
 
+// x / d rounded to nearest -- bit-identical to __ddiv_rn(x, d) -- for a divisor fixed per launch (6 in
+// PPM / WENO-Z, gamma - 1 in E = p / (gamma - 1)) with rd = RN(1/d) (reading A47):
+//   q0 = RN(x rd) is within 1.5 ulp of x/d;
+//   q1 = RN(q0 + (x - q0 d) rd) is faithful (error 1/2 ulp plus ~2^-52 ulp);
+//   q2 = RN(q1 + r rd) with the residual r = x - q1 d exact (q1 faithful) is RN(x/d) by Markstein's theorem
+//   (q faithful and rd within half an ulp of 1/d).
+// 5 fp64 operations instead of the general division's reciprocal iteration and range checks.  The
+// theorem needs every step inside the normal range: 2^-900 < |x| < 2^900 and 2^-60 < d < 2^60 (the
+// callers' divisors); zero keeps its sign (x / d with d > 0), everything else takes __ddiv_rn.
+__device__ __forceinline__ double ddiv_k(double x, double d, double rd) {
+  const double ax = fabs(x);
+  if (!(ax > 0x1p-900 && ax < 0x1p900)) return ax == 0.0 ? x : __ddiv_rn(x, d);
+  double q = __dmul_rn(x, rd);
+  q = __fma_rn(__fma_rn(-q, d, x), rd, q);
+  return __fma_rn(__fma_rn(-q, d, x), rd, q);
+}
+constexpr double K6 = 6.0, RK6 = 1.0 / 6.0;  // RN(1/6), folded by the compiler
+
 }  // namespace ph
