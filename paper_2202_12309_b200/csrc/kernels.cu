@@ -1433,6 +1433,7 @@ __global__ void houpdate_kernel(StageArgs A, const double* Fx, const double* Fy,
   const int64_t fx = (int64_t)(G.n[0] + 1) * G.n[1] * G.n[2], fy = (int64_t)G.n[0] * (G.n[1] + 1) * G.n[2],
                 fz = (int64_t)G.n[0] * G.n[1] * (G.n[2] + 1);
   double tmax = -INFINITY, ts[NVAR] = {0, 0, 0, 0, 0};
+  double smax[3] = {-INFINITY, -INFINITY, -INFINITY};  // max over this thread's cells of |v_d| + c
   // x / dx == x * (1/dx) bit for bit when dx is a power of two (both are exact scalings): the IEEE
   // division (a ~20-instruction sequence) becomes one multiply, the result unchanged (A40 holds)
   bool p2[3];
@@ -1446,24 +1447,37 @@ __global__ void houpdate_kernel(StageArgs A, const double* Fx, const double* Fy,
     const int64_t iy = ((int64_t)k * (G.n[1] + 1) + j) * G.n[0] + i;
     const int64_t iz = ((int64_t)k * G.n[1] + j) * G.n[0] + i;
     double un[NVAR];
+    // every operand of the cell first (40 independent loads in flight per thread: the kernel is bound
+    // by memory latency, not by its arithmetic), then the update in the oracle's order
+    double xl[NVAR], xr[NVAR], yl[NVAR], yr[NVAR], zl[NVAR], zr[NVAR], ui[NVAR], u0[NVAR];
 #pragma unroll
     for (int v = 0; v < NVAR; ++v) {
       const double* px = Fx + (int64_t)slot * NVAR * fx + v * fx + ix;
       const double* py = Fy + (int64_t)slot * NVAR * fy + v * fy + iy;
       const double* pz = Fz + (int64_t)slot * NVAR * fz + v * fz + iz;
-      const double f1 = __dsub_rn(px[1], px[0]), f2 = __dsub_rn(py[G.n[0]], py[0]),
-                   f3 = __dsub_rn(pz[(int64_t)G.n[0] * G.n[1]], pz[0]);
+      xl[v] = __ldg(px);
+      xr[v] = __ldg(px + 1);
+      yl[v] = __ldg(py);
+      yr[v] = __ldg(py + G.n[0]);
+      zl[v] = __ldg(pz);
+      zr[v] = __ldg(pz + (int64_t)G.n[0] * G.n[1]);
+      ui[v] = A.Uin[cell + v * G.vstride];
+      u0[v] = USE_U0 ? A.U0[cell + v * G.vstride] : 0.0;
+    }
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) {
+      const double f1 = __dsub_rn(xr[v], xl[v]), f2 = __dsub_rn(yr[v], yl[v]), f3 = __dsub_rn(zr[v], zl[v]);
       const double d1 = p2[0] ? __dmul_rn(f1, M.idx[0]) : __ddiv_rn(f1, M.dx[0]);
       const double d2 = p2[1] ? __dmul_rn(f2, M.idx[1]) : __ddiv_rn(f2, M.dx[1]);
       const double d3 = p2[2] ? __dmul_rn(f3, M.idx[2]) : __ddiv_rn(f3, M.dx[2]);
       const double L = -__dadd_rn(__dadd_rn(d1, d2), d3);
       const double dtw = __dmul_rn(A.cdt, dt);
-      const double uin = A.Uin[cell + v * G.vstride];
+      const double uin = ui[v];
       double out;
       if (USE_U0 && A.b1 != 0.0)  // RK2 stage 2: 0.5 U0 + 0.5 (U1 + dt L)
-        out = __dadd_rn(__dmul_rn(0.5, A.U0[cell + v * G.vstride]), __dmul_rn(0.5, __dadd_rn(uin, __dmul_rn(dt, L))));
+        out = __dadd_rn(__dmul_rn(0.5, u0[v]), __dmul_rn(0.5, __dadd_rn(uin, __dmul_rn(dt, L))));
       else if (USE_U0)            // VL2 stage 2: U0 + dt L
-        out = __dadd_rn(A.U0[cell + v * G.vstride], __dmul_rn(dtw, L));
+        out = __dadd_rn(u0[v], __dmul_rn(dtw, L));
       else                        // stage 1: U0 + w dt L
         out = __dadd_rn(uin, __dmul_rn(dtw, L));
       un[v] = out;
@@ -1473,12 +1487,27 @@ __global__ void houpdate_kernel(StageArgs A, const double* Fx, const double* Fy,
       // exact CFL term, kept as -min(...) in the 'max' slot (finalize: dt = cfl * (-m), G.exact)
       double Wn[NVAR];
       cons2prim_rn(un[0], un[1], un[2], un[3], un[4], G.gm1, Wn);
-      tmax = fmax(tmax, -cfl_term_rn(Wn, M, G.gamma));
+      const double cs = __dsqrt_rn(__ddiv_rn(__dmul_rn(G.gamma, Wn[4]), Wn[0]));
+#pragma unroll
+      for (int d = 0; d < 3; ++d) smax[d] = fmax(smax[d], __dadd_rn(fabs(Wn[1 + d]), cs));
 #pragma unroll
       for (int v = 0; v < NVAR; ++v) ts[v] += un[v];
     }
   }
   if (REDUCE) {
+    // the oracle's min over cells of min_d RN(dx_d / s_d) (cfl_term_rn) == min_d RN(dx_d / max s_d): s ->
+    // RN(dx / s) is non-increasing, so the divisions move out of the cell loop (3 per thread instead of
+    // 3 per cell), the result bit-identical (A40); NaN speeds (a failed cell, flagged) are skipped by fmax
+    if (smax[0] > -INFINITY || smax[1] > -INFINITY || smax[2] > -INFINITY) {
+      double r = INFINITY;
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        if (smax[d] > -INFINITY) {
+          const double rd = __ddiv_rn(M.dx[d], smax[d]);
+          r = rd < r ? rd : r;
+        }
+      tmax = -r;
+    }
     __shared__ double red[32][6];
     for (int off = 16; off > 0; off >>= 1) {
       tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, off));
@@ -2014,7 +2043,9 @@ static cudaError_t launch_hoflux_r(const double* W, double* Fx, double* Fy, doub
   const char* pf = getenv("PH_HO_FACE");
   const char* pl = getenv("PH_HO_LINE");
   const bool all_face = pf && pf[0] == '1', all_line = pl && pl[0] == '1';
-  const bool line_x = all_line || (!all_face && R == 3);
+  // x: the per-face kernel for every reconstruction (its loads are coalesced along x; the x march's
+  // lanes walk 32 rows: PPM 1.43 vs 1.70 ms per launch after A47, r02_launches_ho_ppm.md)
+  const bool line_x = all_line;
   const bool line_yz = all_line || (!all_face && R != 4);
   if (line_x) launch_holine<0, R>(W, Fx, nslots, G, s);
   else launch_hoface<0, R>(W, Fx, nslots, G, s);
@@ -2027,6 +2058,8 @@ static cudaError_t launch_hoflux_r(const double* W, double* Fx, double* Fy, doub
   }
   return cudaGetLastError();
 }
+
+constexpr int HOU_T = 128;  // update kernel CTA (up to ~150 registers with the loads hoisted: 3 CTAs per SM)
 
 cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslots, const StageArgs& a, double* W,
                                    double* Fx, double* Fy, double* Fz, const Geom& G, cudaStream_t s) {
@@ -2043,11 +2076,11 @@ cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslo
   if (e != cudaSuccess) return e;
   const int grid = nslots * G.n[2];
   if (reduce) {
-    if (use_u0) houpdate_kernel<true, true><<<grid, 256, 0, s>>>(a, Fx, Fy, Fz, G);
-    else houpdate_kernel<true, false><<<grid, 256, 0, s>>>(a, Fx, Fy, Fz, G);
+    if (use_u0) houpdate_kernel<true, true><<<grid, HOU_T, 0, s>>>(a, Fx, Fy, Fz, G);
+    else houpdate_kernel<true, false><<<grid, HOU_T, 0, s>>>(a, Fx, Fy, Fz, G);
   } else {
-    if (use_u0) houpdate_kernel<false, true><<<grid, 256, 0, s>>>(a, Fx, Fy, Fz, G);
-    else houpdate_kernel<false, false><<<grid, 256, 0, s>>>(a, Fx, Fy, Fz, G);
+    if (use_u0) houpdate_kernel<false, true><<<grid, HOU_T, 0, s>>>(a, Fx, Fy, Fz, G);
+    else houpdate_kernel<false, false><<<grid, HOU_T, 0, s>>>(a, Fx, Fy, Fz, G);
   }
   return cudaGetLastError();
 }

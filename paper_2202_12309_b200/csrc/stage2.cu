@@ -110,6 +110,13 @@ __device__ __forceinline__ void tma5(void* dst, const CUtensorMap* map, int c0, 
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(su32(bar))
       : "memory");
 }
+// TMA box prefetch into L2 (no shared memory, no completion): the next step's loads then hit L2
+__device__ __forceinline__ void tma5_l2(const CUtensorMap* map, int c0, int c1, int c2, int c3, int c4) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %2, %3, %4, %5}];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ double2 lds2(const double* p) { return *reinterpret_cast<const double2*>(p); }
@@ -417,6 +424,14 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
         mbar_expect_tx(bar + NSLOT, OWN_BYTES);
         tma5(fin, &maps.f, x0 + g, y0 + g, c + g, 0, slot, bar + NSLOT);
       }
+#ifdef PH_S2_PF
+      // (A/B knob, off: 2b 1.03e10 with both prefetches vs 1.06e10 without) one step further ahead, into L2
+      // only: the finish operand of plane c+1 (and with PH_S2_PF=2 the centre box of plane q+2)
+#if PH_S2_PF > 1
+      if (q + 2 >= k0 && q + 2 < k1) tma5_l2(&maps.c, x0 + g, y0 + g, q + 2 + g, 0, slot);
+#endif
+      if (c + 1 >= k0 && c + 1 < k1) tma5_l2(&maps.f, x0 + g, y0 + g, c + 1 + g, 0, slot);
+#endif
     }
 
     double dz[2][NVAR];
