@@ -118,34 +118,37 @@ __device__ __forceinline__ double slope_rn(double qm, double q0, double qp, int 
   return dl > dr ? dl : dr;
 }
 
+// PPM's limited slope and interface values with selects in place of branches: every candidate is
+// computed (all are exact single operations on finite inputs) and the oracle's conditions pick one, so
+// the results are the oracle's bit for bit while the warp issues no data-dependent branches (the line
+// kernels' top stall was branch resolution)
 __device__ __forceinline__ double ppm_dm_rn(double a, double b, double c) {
   const double dl = __dsub_rn(b, a), dr = __dsub_rn(c, b);
   const bool same = (dl > 0.0 && dr > 0.0) || (dl < 0.0 && dr < 0.0);
-  if (!same) return 0.0;
   const double dq = __dmul_rn(0.5, __dsub_rn(c, a));
   double m = fabs(dq);
-  if (__dmul_rn(2.0, fabs(dl)) < m) m = __dmul_rn(2.0, fabs(dl));
-  if (__dmul_rn(2.0, fabs(dr)) < m) m = __dmul_rn(2.0, fabs(dr));
-  return dq > 0.0 ? m : -m;
+  const double tl = __dmul_rn(2.0, fabs(dl)), tr = __dmul_rn(2.0, fabs(dr));
+  m = tl < m ? tl : m;
+  m = tr < m ? tr : m;
+  const double r = dq > 0.0 ? m : -m;
+  return same ? r : 0.0;
 }
 
 // PPM interface values of one cell from its neighbours qm, c, qp and the three limited slopes
 // dm_m, dm_0, dm_p (cells c-1, c, c+1); split out so a line march can reuse each slope three times.
+// Oracle: if (R-c)(c-L) <= 0 then L = R = c; else if d m6 > d^2 then L = 3c - 2R; else if -d^2 > d m6
+// then R = 3c - 2L.
 __device__ __forceinline__ void ppm_lr_rn(double qm, double c, double qp, double dm_m, double dm_0, double dm_p,
                                           double& ql, double& qr) {
-  double L = __dsub_rn(__dadd_rn(qm, __dmul_rn(0.5, __dsub_rn(c, qm))), ddiv_k(__dsub_rn(dm_0, dm_m), K6, RK6));
-  double R = __dsub_rn(__dadd_rn(c, __dmul_rn(0.5, __dsub_rn(qp, c))), ddiv_k(__dsub_rn(dm_p, dm_0), K6, RK6));
-  if (__dmul_rn(__dsub_rn(R, c), __dsub_rn(c, L)) <= 0.0) {
-    L = c;
-    R = c;
-  } else {
-    const double d = __dsub_rn(R, L), m6 = __dmul_rn(6.0, __dsub_rn(c, __dmul_rn(0.5, __dadd_rn(L, R))));
-    const double dd = __dmul_rn(d, d), dm6 = __dmul_rn(d, m6);
-    if (dm6 > dd) L = __dsub_rn(__dmul_rn(3.0, c), __dmul_rn(2.0, R));
-    else if (-dd > dm6) R = __dsub_rn(__dmul_rn(3.0, c), __dmul_rn(2.0, L));
-  }
-  ql = L;
-  qr = R;
+  const double L = __dsub_rn(__dadd_rn(qm, __dmul_rn(0.5, __dsub_rn(c, qm))), ddiv_k(__dsub_rn(dm_0, dm_m), K6, RK6));
+  const double R = __dsub_rn(__dadd_rn(c, __dmul_rn(0.5, __dsub_rn(qp, c))), ddiv_k(__dsub_rn(dm_p, dm_0), K6, RK6));
+  const bool flat = __dmul_rn(__dsub_rn(R, c), __dsub_rn(c, L)) <= 0.0;
+  const double d = __dsub_rn(R, L), m6 = __dmul_rn(6.0, __dsub_rn(c, __dmul_rn(0.5, __dadd_rn(L, R))));
+  const double dd = __dmul_rn(d, d), dm6 = __dmul_rn(d, m6);
+  const bool fixl = dm6 > dd, fixr = !fixl && (-dd > dm6);
+  const double Lx = __dsub_rn(__dmul_rn(3.0, c), __dmul_rn(2.0, R)), Rx = __dsub_rn(__dmul_rn(3.0, c), __dmul_rn(2.0, L));
+  ql = flat ? c : (fixl ? Lx : L);
+  qr = flat ? c : (fixr ? Rx : R);
 }
 
 __device__ __forceinline__ void ppm_cell_rn(const double* q, double& ql, double& qr) {
@@ -1415,11 +1418,62 @@ template <int DIR, int RECON>
 __global__ void hoflux_kernel(const double* W, double* F, Geom G) {
   hoflux_body<DIR, RECON>(W, F, G);
 }
+
+// x fluxes with one cell per lane (PLM / PPM): each lane reconstructs its own cell's two interface values
+// once -- PPM's three limited slopes and L / R, PLM's one slope -- and face f (cells f-1 | f) takes R of
+// cell f-1 from the lane below by a shuffle, halving hoflux_kernel<0>'s reconstruction work (it builds
+// both cells of every face).  A warp holds 32 consecutive cells of the flattened sequence (row j, cell
+// -1..n0) and emits the faces whose left cell it also holds; consecutive warps overlap by one cell.
+// Same operations on the same operands as hoflux_kernel<0, RECON>: bit for bit (A40).
+template <int RECON>
+__global__ void __launch_bounds__(128) hofx_kernel(const double* W, double* F, Geom G) {
+  const int n0 = G.n[0], n1 = G.n[1], e0 = n0 + 1, RC = n0 + 2, total = n1 * RC;
+  const int k = blockIdx.x % G.n[2], slot = blockIdx.x / G.n[2];
+  const int nch = (total - 1 + 30) / 31;
+  const int64_t fvs = (int64_t)e0 * n1 * G.n[2];
+  double* fb = F + (int64_t)slot * NVAR * fvs + (int64_t)k * e0 * n1;
+  const double* wb = W + (int64_t)slot * G.bstride + (int64_t)(k + G.g) * G.N[1] * G.N[0];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int ch = warp; ch < nch; ch += nw) {
+    const int t = ch * 31 + lane;
+    const bool valid = t < total;
+    const int j = valid ? t / RC : 0, ci = valid ? t % RC - 1 : 0;
+    const double* p = wb + (int64_t)(j + G.g) * G.N[0] + (ci + G.g);
+    double L[NVAR], R[NVAR];
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) {
+      double q[5];
+#pragma unroll
+      for (int u = 0; u < 5; ++u) q[u] = (valid && (RECON == 3 || (u >= 1 && u <= 3))) ? p[v * G.vstride + (u - 2)] : 1.0;
+      if (RECON == 3) {
+        ppm_cell_rn(q, L[v], R[v]);
+      } else {
+        const double sl = slope_rn(q[1], q[2], q[3], RECON);
+        R[v] = __dadd_rn(q[2], __dmul_rn(0.5, sl));
+        L[v] = __dsub_rn(q[2], __dmul_rn(0.5, sl));
+      }
+    }
+    double wl[NVAR];
+#pragma unroll
+    for (int v = 0; v < NVAR; ++v) wl[v] = __shfl_up_sync(0xffffffffu, R[v], 1);
+    if (valid && lane > 0 && ci >= 0) {
+      double Fn[NVAR];
+      hlle_rn(wl, L, G, Fn);
+      double* fo = fb + (int64_t)j * e0 + ci;
+#pragma unroll
+      for (int v = 0; v < NVAR; ++v) fo[v * fvs] = Fn[v];
+    }
+  }
+}
 // PPM's march is capped at 128 registers (4 CTAs of 128 per SM; some spills): +2 % over 158-174
 // registers, 3 % over a 168-register cap.  A cap on the per-face WENO-Z kernel (80/72/64 registers)
 // loses 7/14/23 % (profiles/r01_ho_line_march.md).
+#ifndef PH_HOLINE_MINB
+#define PH_HOLINE_MINB 3  // CTAs per SM the PPM line march is compiled for (round 2, after the
+                          // branchless PPM: 3 -> 6.86, 4 -> 7.65, 2 -> 7.33 ms per cycle)
+#endif
 template <int DIR, int RECON>
-__global__ void __launch_bounds__(128, RECON == 3 ? 4 : 1) holine_kernel(const double* W, double* F, int nslots,
+__global__ void __launch_bounds__(128, RECON == 3 ? PH_HOLINE_MINB : 1) holine_kernel(const double* W, double* F, int nslots,
                                                                          int nseg, Geom G) {
   holine_body<DIR, RECON>(W, F, nslots, nseg, G);
 }
@@ -2043,11 +2097,13 @@ static cudaError_t launch_hoflux_r(const double* W, double* Fx, double* Fy, doub
   const char* pf = getenv("PH_HO_FACE");
   const char* pl = getenv("PH_HO_LINE");
   const bool all_face = pf && pf[0] == '1', all_line = pl && pl[0] == '1';
-  // x: the per-face kernel for every reconstruction (its loads are coalesced along x; the x march's
-  // lanes walk 32 rows: PPM 1.43 vs 1.70 ms per launch after A47, r02_launches_ho_ppm.md)
+  // x: PPM one cell per lane with the left state by shuffle (hofx_kernel: 0.80 ms vs 0.99 per face), the
+  // per-face kernel for PLM (its slope is cheap) and WENO-Z (nothing to share between a cell's two faces);
+  // the x march's lanes walk 32 rows (PPM 1.39 ms, r02_launches_ho_ppm.md)
   const bool line_x = all_line;
   const bool line_yz = all_line || (!all_face && R != 4);
   if (line_x) launch_holine<0, R>(W, Fx, nslots, G, s);
+  else if (R == 3 && !all_face) hofx_kernel<3><<<nslots * G.n[2], 128, 0, s>>>(W, Fx, G);
   else launch_hoface<0, R>(W, Fx, nslots, G, s);
   if (line_yz) {
     launch_holine<1, R>(W, Fy, nslots, G, s);
