@@ -369,7 +369,11 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
   const int qbeg = k0 - 2, qend = k1 + 2;
   if (tid == 0) issue_plane(qbeg, 0);
   int s = 0;
+#ifdef PH_S2_UNROLL2
+#pragma unroll 2
+#else
 #pragma unroll 1
+#endif
   for (int q = qbeg; q < qend; ++q) {
     const int idx = q - qbeg;
     const int s1 = (s + NSLOT - 1) & (NSLOT - 1);  // slot of plane q-1

@@ -116,9 +116,14 @@ def main():
             busy_all = intervals_union([(r["start_us"], r["start_us"] + r["dur_us"]) for r in rows])
             f.write(f"\nGPU busy {sum(e - s_ for s_, e in busy_all):.0f} us of {span:.0f} us span (idle gaps = host work / launch latency)\n")
             hin = sum(r["dur_us"] for r in halo)
-            hov = overlap(intervals_union([(r["start_us"], r["start_us"] + r["dur_us"]) for r in halo]), busy[si])
+            # overlap = halo time during which a stage kernel runs on another stream (0 on one stream)
+            hov = 0.0
+            for hs in {r["stream"] for r in halo}:
+                h_iv = intervals_union([(r["start_us"], r["start_us"] + r["dur_us"]) for r in halo if r["stream"] == hs])
+                st_iv = intervals_union([(r["start_us"], r["start_us"] + r["dur_us"]) for r in stage if r["stream"] != hs])
+                hov += overlap(h_iv, st_iv)
             f.write(f"\nhalo kernels (pack / put / signal / wait / NCCL): {hin:.0f} us, of which {hov:.0f} us "
-                    f"run while the interior stream computes\n")
+                    f"run while a stage kernel computes on another stream\n")
         print(open(a.out + ".md").read()[:1500])
     m.close()
     if world > 1:
