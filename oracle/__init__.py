@@ -14,7 +14,10 @@ Parity status per function ("Oracle pins"):
   AMR refinement criterion (A14: closed form on a linear pressure)  -> pinned
   physical BCs on fine ghosts and coarse staging, staging geometry at walls (A12)
                                                            -> pinned (method of images)
-  derefinement gate (A16)                                  -> parity unpinned by the paper
+  derefinement (A16 gate, family rule, 2:1 on derefinement) -> pinned (closed-form block counts,
+                                                              tests/test_oracle_exchange.py)
+  PPM / WENO-Z (A37 / A38; the paper names neither)        -> pinned by their textbook definitions
+                                                              (tests/test_oracle_highorder.py)
 """
 from __future__ import annotations
 

@@ -90,6 +90,40 @@ def test_amr_derefinement_gate(oracle_mod, P):
             assert np.all(S[v] == U[v])
 
 
+def test_derefinement_family_and_2to1_match_oracle(oracle_mod, P):
+    """The two derefinement pins of test_oracle_exchange.py (family rule: 71 blocks; one level per
+    remesh under 2:1: 309 -> 253 -> 64) on the GPU mesh (mesh.cpp normalize_flags + remesh), block lists,
+    neighbour lists and flags equal to the oracle's."""
+    import test_oracle_exchange as T
+    o, _ = T._deref_family_mesh(oracle_mod)
+    g, _ = T._deref_family_mesh(P, oracle_mod)
+    o.exchange()
+    o.compute_dt()
+    g.refresh()
+    o.step(1, 1e-9)
+    g.step(1, 1e-9)
+    _same_mesh(o, g)
+    assert g.num_blocks() == 71
+    assert np.array_equal(o.refine_flags(), g.refine_flags())
+    kw = dict(mesh_nx=(16, 16, 16), block_nx=(4, 4, 4), max_level=2, refinement=P.REF_ADAPTIVE,
+              regions=[(2, 0.3, 0.45, 0.3, 0.45, 0.3, 0.45)], derefine_interval=1, refine_tol=0.5,
+              derefine_tol=0.01)
+    o, g = oracle_mod.Mesh(**kw), P.Mesh(**kw)
+    U = oracle_mod.prim_to_cons([1.0, 0.0, 0.0, 0.0, 1.0], 5 / 3)
+    for m in (o, g):
+        for b in range(m.num_blocks()):
+            m.set_state(b, np.broadcast_to(U[:, None, None, None], (5, 4, 4, 4)))
+    o.exchange()
+    o.compute_dt()
+    g.refresh()
+    for want in (253, 64):
+        o.step(1)
+        g.step(1)
+        _same_mesh(o, g)
+        assert g.num_blocks() == want
+        assert np.array_equal(o.refine_flags(), g.refine_flags())
+
+
 def test_config3_amr_blast_full_size(oracle_mod, P):
     """BASELINE config 3: blast, 128^3 root grid of 32^3 blocks, 3 refinement levels, 10 cycles."""
     kw = dict(mesh_nx=(128,) * 3, block_nx=(32,) * 3, xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=3,

@@ -207,6 +207,67 @@ def test_derefinement_gate(oracle_mod):
             assert np.all(S[v] == U[v])
 
 
+def _deref_family_mesh(M, O=None):
+    """120 blocks: 56 roots of 4^3 cells + the 8 families (64 level-1 blocks) of the region [0.3, 0.7]^3;
+    uniform gas at rest except a pressure bump (p 1 -> 1.1) in the central 2^3 cells of one level-1
+    block, which gives that block eps = 0.5 * 0.1 / 1 = 0.05 (between derefine_tol 0.01 and refine_tol
+    0.5: flag 0) and leaves every other block's eps at 0 (the bump does not reach a neighbour's stencil,
+    and tlim = 1e-9 keeps it in place for the one cycle)."""
+    kw = dict(mesh_nx=(16, 16, 16), block_nx=(4, 4, 4), max_level=1, refinement=M.REF_ADAPTIVE,
+              regions=[(1, 0.3, 0.7, 0.3, 0.7, 0.3, 0.7)], derefine_interval=1, refine_tol=0.5, derefine_tol=0.01)
+    m = M.Mesh(**kw)
+    O = O or M  # input states from the oracle's prim -> cons (test input, both sides get the same bytes)
+    U = O.prim_to_cons([1.0, 0.0, 0.0, 0.0, 1.0], 5 / 3)
+    Ub = O.prim_to_cons([1.0, 0.0, 0.0, 0.0, 1.1], 5 / 3)
+    B = [b for b in m.blocks() if b["level"] == 1][0]
+    for b in range(m.num_blocks()):
+        S = np.array(np.broadcast_to(U[:, None, None, None], (5, 4, 4, 4)))
+        if b == B["gid"]:
+            S[:, 1:3, 1:3, 1:3] = Ub[:, None, None, None]
+        m.set_state(b, S)
+    return m, B
+
+
+def test_derefinement_needs_the_whole_family(oracle_mod):
+    """O9 / A15: a parent is re-formed only from all 8 of its children flagged -1; one child at flag 0
+    keeps its family.  Closed form: 7 families merge, 56 + 7 + 8 = 71 blocks."""
+    O = oracle_mod
+    m, B = _deref_family_mesh(O)
+    assert m.num_blocks() == 120 and m.level_counts(2) == [56, 64]
+    m.exchange()
+    m.compute_dt()
+    m.step(1, 1e-9)
+    fl = m.refine_flags()
+    assert sorted(np.unique(fl, return_counts=True)[1].tolist()) == [57, 63]  # the 63 other children flag -1
+    assert m.num_blocks() == 71 and m.level_counts(2) == [63, 8]
+    kept = [b for b in m.blocks() if b["level"] == 1]
+    assert {tuple(x >> 1 for x in b["lx"]) for b in kept} == {tuple(x >> 1 for x in B["lx"])}
+
+
+def test_derefinement_one_level_per_remesh_and_2to1(oracle_mod):
+    """A15 (2:1 over faces, edges and corners) on derefinement: a family may merge only if no leaf
+    adjacent to it is finer than its children.  The level-2 region [0.3, 0.45]^3 covers root block
+    (1,1,1) entirely (64 level-2 blocks); 2:1 refines its 26 root neighbours to level 1 (208 blocks);
+    37 roots stay: 309.  With uniform gas and the gate open every cycle, the first remesh merges the 8
+    level-2 families (their neighbours are level 1) but none of the 26 level-1 families (each touches a
+    level-2 leaf): 37 + 208 + 8 = 253; the second merges all 27 level-1 families: 64."""
+    O = oracle_mod
+    kw = dict(mesh_nx=(16, 16, 16), block_nx=(4, 4, 4), max_level=2, refinement=O.REF_ADAPTIVE,
+              regions=[(2, 0.3, 0.45, 0.3, 0.45, 0.3, 0.45)], derefine_interval=1, refine_tol=0.5,
+              derefine_tol=0.01)
+    m = O.Mesh(**kw)
+    assert m.num_blocks() == 309 and m.level_counts(3) == [37, 208, 64]
+    U = O.prim_to_cons([1.0, 0.0, 0.0, 0.0, 1.0], 5 / 3)
+    for b in range(m.num_blocks()):
+        m.set_state(b, np.broadcast_to(U[:, None, None, None], (5, 4, 4, 4)))
+    m.exchange()
+    m.compute_dt()
+    m.step(1)
+    assert m.num_blocks() == 253 and m.level_counts(3) == [37, 216, 0]
+    m.step(1)
+    assert m.num_blocks() == 64 and m.level_counts(3) == [64, 0, 0]
+
+
 @pytest.mark.parametrize("axis", [0, 1])
 def test_refinement_indicator_closed_form_on_a_linear_pressure(oracle_mod, axis):
     """A14: eps_B = max over the block of |grad p| / p with central differences (half the difference of
