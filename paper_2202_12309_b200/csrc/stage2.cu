@@ -530,6 +530,64 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
       double dy[2][NVAR];
       {
         double wl[2][NVAR], wr[2][NVAR];
+#if defined(PH_S2_YS) && !defined(PH_S2_V3)
+        // each row's y slope once: my row's bottom state (face r-1/2) and top state (face r+1/2, for
+        // the row above); the top state of row r-1 comes from the lane 8 below (same warp), from the
+        // warp below through shared memory (kr == 0; the buffer the warp above later reuses for its
+        // bottom-face hand-over, FB), or for warp 0 from the y-halo rows -2, -1.  Same operations on
+        // the same operands as the 4-row stencil: bit for bit.
+        {
+          double tp[2][NVAR];
+          int yo[3], yv[3];
+#pragma unroll
+          for (int t = 0; t < 3; ++t) row_at(r - 1 + t, i0, yo[t], yv[t]);
+          double2 bm[NVAR];
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) {
+            const double2 b = lds2(Wc + yo[0] + v * yv[0]), cc = lds2(Wc + yo[1] + v * yv[1]),
+                          d = lds2(Wc + yo[2] + v * yv[2]);
+            bm[v] = b;
+            mm_states(cc.x - b.x, d.x - cc.x, cc.x, wr[0][v], tp[0][v]);
+            mm_states(cc.y - b.y, d.y - cc.y, cc.y, wr[1][v], tp[1][v]);
+          }
+          if (warp < NW - 1) {  // my row 3's top state for the warp above
+            if (kr == 3) {
+              double* ts = sm + OFF_FB + warp * NVAR * TX + i0;
+#pragma unroll
+              for (int v = 0; v < NVAR; ++v) sts2(ts + v * TX, tp[0][v], tp[1][v]);
+            }
+            asm volatile("bar.arrive %0, %1;" ::"r"(NW + 1 + warp), "r"(64) : "memory");
+          }
+#pragma unroll
+          for (int v = 0; v < NVAR; ++v) {
+            wl[0][v] = __shfl_up_sync(0xffffffffu, tp[0][v], 8);
+            wl[1][v] = __shfl_up_sync(0xffffffffu, tp[1][v], 8);
+          }
+          if (warp == 0) {
+            if (kr == 0) {  // row -1 from the y-halo rows -2, -1 and row 0
+#pragma unroll
+              for (int v = 0; v < NVAR; ++v) {
+                const double2 a = lds2(Wc + R_YL + i0 + v * VY), b = bm[v],
+                              cc = lds2(Wc + R_M + i0 + v * VM);
+                double t;
+                mm_states(b.x - a.x, cc.x - b.x, b.x, t, wl[0][v]);
+                mm_states(b.y - a.y, cc.y - b.y, b.y, t, wl[1][v]);
+              }
+            }
+          } else {
+            asm volatile("bar.sync %0, %1;" ::"r"(NW + warp), "r"(64) : "memory");
+            if (kr == 0) {
+              const double* ts = sm + OFF_FB + (warp - 1) * NVAR * TX + i0;
+#pragma unroll
+              for (int v = 0; v < NVAR; ++v) {
+                const double2 h = lds2(ts + v * TX);
+                wl[0][v] = h.x;
+                wl[1][v] = h.y;
+              }
+            }
+          }
+        }
+#else
         int yo[4], yv[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) row_at(r - 2 + t, i0, yo[t], yv[t]);
@@ -543,6 +601,7 @@ __global__ void __launch_bounds__(NTH, PH_S2_MINB) stage2_kernel(StageArgs A, Ge
           mm_states(b.y - a.y, cc.y - b.y, b.y, t, wl[1][v]);
           mm_states(cc.y - b.y, d.y - cc.y, cc.y, wr[1][v], t);
         }
+#endif
         double FF[2][NVAR];
         hlle_ab2<2>(wl, wr, gamma, ggm1, FF);
         const double(&F0)[NVAR] = FF[0];
