@@ -111,10 +111,12 @@ typedef struct {
   void* (*dev_alloc)(size_t bytes, void* ctx); /* optional device allocator (torch caching allocator) */
   void (*dev_free)(void* ptr, void* ctx);
   void* alloc_ctx;
-  int32_t halo_transport;           /* ph_halo_transport (ABI 2).  Peer memory applies to uniform or
-                                       static multilevel nghost-2 meshes with nranks > 1; its receive
-                                       buffers come from cudaMalloc (CUDA IPC), not dev_alloc.
-                                       The full exchange (ph_refresh, ph_exchange) stays on NCCL. */
+  int32_t halo_transport;           /* ph_halo_transport (ABI 2).  Peer memory applies to nghost-2
+                                       meshes (uniform, static multilevel or adaptive: a remesh
+                                       rebuilds the receive regions and mappings, collectively) with
+                                       nranks > 1; its receive buffers come from cudaMalloc (CUDA IPC),
+                                       not dev_alloc.  The full exchange (ph_refresh, ph_exchange) and
+                                       the remesh's block migration stay on NCCL. */
   int32_t wavespeed;                /* ph_wavespeed (ABI 3); 0 = Davis */
 } ph_config;
 

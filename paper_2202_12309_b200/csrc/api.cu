@@ -159,6 +159,7 @@ struct ph_mesh {
   unsigned long long** d_pflags = nullptr;          // device [R]: every rank's flag array
   unsigned long long* my_flags = nullptr;           // [64] in my region, written by peers
   unsigned long long* d_ctr = nullptr;              // [2] signal / wait epoch counters (device)
+  void* d_peer_rec = nullptr;                       // device [R + 1] set-up records (allgather)
   unsigned long long send_mask = 0, recv_mask = 0;  // peers I put to / receive from per exchange
   bool fused_put = false;  // the boundary blocks' stage kernel stores the faces itself (no put kernel)
   // boundary-first schedule of the multi-GPU cycle: B (high priority) runs boundary blocks and the
@@ -893,6 +894,24 @@ static ph_status setup_device(ph_mesh* m) {
  * *ok = false and the halo stays on NCCL.  On success the per-cycle pack tasks become puts: each
  * writes at the offset the receiving rank's unpack task reads.  Flags are zeroed before the
  * agreement, so no peer can signal into them earlier. */
+static void host_barrier(ph_mesh* m);
+
+/* Undo setup_peer (collective): nobody may still write into my region or read through a mapping when
+ * it goes -- every rank drains its stream and meets the others before and after unmapping. */
+static void teardown_peer(ph_mesh* m) {
+  if (!m->peer_region) return;
+  cudaStreamSynchronize(m->stream);
+  host_barrier(m);
+  for (void* p : m->peer_open)
+    if (p) cudaIpcCloseMemHandle(p);
+  m->peer_open.clear();
+  host_barrier(m);
+  cudaFree(m->peer_region);
+  m->peer_region = nullptr;
+  m->my_flags = nullptr;
+  m->peer = false;
+}
+
 static ph_status setup_peer(ph_mesh* m, bool* ok_out) {
   *ok_out = false;
   const int R = m->nranks, me = m->rank;
@@ -927,8 +946,8 @@ static ph_status setup_peer(ph_mesh* m, bool* ok_out) {
     if (PL.send_cnt[p] > 0) m->send_mask |= 1ull << p;
     if (PL.recv_cnt[p] > 0) m->recv_mask |= 1ull << p;
   }
-  void* dbuf = nullptr;
-  TRY(dalloc(m, &dbuf, (size_t)(R + 1) * sizeof(Rec), true));
+  if (!m->d_peer_rec) TRY(dalloc(m, &m->d_peer_rec, (size_t)(R + 1) * sizeof(Rec), true));  // once (remesh re-runs this)
+  void* dbuf = m->d_peer_rec;
   CU(cudaMemcpyAsync((char*)dbuf + (size_t)R * sizeof(Rec), &mine, sizeof(Rec), cudaMemcpyHostToDevice, m->stream));
   NC(ncclAllGather((char*)dbuf + (size_t)R * sizeof(Rec), dbuf, sizeof(Rec), ncclUint8, m->comm, m->stream));
   std::vector<Rec> all(R);
@@ -971,10 +990,12 @@ static ph_status setup_peer(ph_mesh* m, bool* ok_out) {
   }
   m->my_rbuf[0] = h0[me];
   m->my_rbuf[1] = h1[me];
-  TRY(dalloc(m, (void**)&m->d_prbuf[0], R * sizeof(double*), true));
-  TRY(dalloc(m, (void**)&m->d_prbuf[1], R * sizeof(double*), true));
-  TRY(dalloc(m, (void**)&m->d_pflags, R * sizeof(void*), true));
-  TRY(dalloc(m, (void**)&m->d_ctr, 2 * sizeof(unsigned long long), true));
+  if (!m->d_prbuf[0]) {
+    TRY(dalloc(m, (void**)&m->d_prbuf[0], R * sizeof(double*), true));
+    TRY(dalloc(m, (void**)&m->d_prbuf[1], R * sizeof(double*), true));
+    TRY(dalloc(m, (void**)&m->d_pflags, R * sizeof(void*), true));
+    TRY(dalloc(m, (void**)&m->d_ctr, 2 * sizeof(unsigned long long), true));
+  }
   CU(cudaMemcpyAsync(m->d_prbuf[0], h0.data(), R * sizeof(double*), cudaMemcpyHostToDevice, m->stream));
   CU(cudaMemcpyAsync(m->d_prbuf[1], h1.data(), R * sizeof(double*), cudaMemcpyHostToDevice, m->stream));
   CU(cudaMemcpyAsync(m->d_pflags, fl.data(), R * sizeof(void*), cudaMemcpyHostToDevice, m->stream));
@@ -1394,7 +1415,9 @@ static ph_status one_cycle(ph_mesh* m) {
  * the new blocks in gid order, so buffer offsets agree without a handshake. */
 static ph_status remesh(ph_mesh* m, const std::unordered_set<LocKey>& leaves, bool move) {
   const int R = m->nranks, me = m->rank;
-  if (m->peer) return fail(PH_ERR_STATE, "remesh of a peer-halo mesh (peer halo is for static uniform meshes)");
+  // peer halo (AMR): the plan changes, so the receive regions, offsets and mappings are rebuilt after it
+  const bool had_peer = m->peer && !m->host_only;  // (host-only meshes: plan only, nothing mapped)
+  if (had_peer) teardown_peer(m);
   if (m->graph_exec) {
     cudaGraphExecDestroy(m->graph_exec);
     m->graph_exec = nullptr;
@@ -1412,6 +1435,13 @@ static ph_status remesh(ph_mesh* m, const std::unordered_set<LocKey>& leaves, bo
     return fail(PH_ERR_STATE, ex.what());
   }
   TRY(build_plan(m));
+  if (had_peer) {
+    bool ok = false;
+    TRY(setup_peer(m, &ok));
+    m->peer = ok;
+    if (!ok && m->cfg.halo_transport == PH_HALO_PEER)
+      return fail(PH_ERR_UNSUPPORTED, "peer halo: a rank cannot map its peers' memory after the remesh");
+  }
   TRY(setup_device(m));
   if (move) {
     const Geom& G = m->G;
@@ -1746,14 +1776,14 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
   }
   bool uniform = true;
   for (auto& b : m->blocks) uniform = uniform && b.loc.level == 0;
-  // peer transport: uniform or static multilevel meshes (the plan is fixed: AMR rebuilds it on remesh)
+  // peer transport: uniform, static multilevel and adaptive meshes (AMR re-runs the set-up at each remesh)
   (void)uniform;
-  const bool peer_cfg = m->nranks > 1 && cfg->refinement != PH_REF_ADAPTIVE && !m->no_direct_halo &&
+  const bool peer_cfg = m->nranks > 1 && !m->no_direct_halo &&
                         G.g == 2 && cfg->halo_transport != PH_HALO_NCCL;
   if (cfg->halo_transport == PH_HALO_PEER && !peer_cfg) {
     delete m->tree;
     delete m;
-    return fail(PH_ERR_UNSUPPORTED, "peer halo needs nranks > 1 and a non-adaptive nghost-2 mesh with the direct halo");
+    return fail(PH_ERR_UNSUPPORTED, "peer halo needs nranks > 1 and an nghost-2 mesh with the direct halo");
   }
   ph_status st = build_plan(m);
   if (st != PH_OK) {
@@ -1830,16 +1860,7 @@ ph_status ph_mesh_destroy(ph_mesh* m) {
   if (m->graph_exec) cudaGraphExecDestroy(m->graph_exec);
   if (m->ev_fork) cudaEventDestroy(m->ev_fork);
   if (m->ev_join) cudaEventDestroy(m->ev_join);
-  if (m->peer_region) {
-    // nobody may still read my pools when I unmap / free: rendezvous before and after unmapping
-    cudaStreamSynchronize(m->stream);
-    host_barrier(m);
-    for (void* p : m->peer_open)
-      if (p) cudaIpcCloseMemHandle(p);
-    host_barrier(m);
-    cudaFree(m->peer_region);
-    m->peer_region = nullptr;
-  }
+  teardown_peer(m);  // nobody may still read my pools when I unmap / free
   free_all(m);
   for (auto& p : m->t_stage) (void)p;
   for (cudaEvent_t e : m->ev_pool) cudaEventDestroy(e);

@@ -26,9 +26,10 @@ def _port():
     return p
 
 
-CASES = [(c, "auto") for c in ("smr2", "smr3_walls", "amr2", "wenoz")]
-# static multilevel meshes with the NCCL halo too (auto picks peer memory for them now)
-CASES += [(c, "nccl") for c in ("smr2", "smr3_walls")]
+CASES = [(c, "auto") for c in ("smr2", "smr3_walls", "amr2", "wenoz")] + [("amr16", "peer")]
+# multilevel and adaptive meshes with the NCCL halo too (auto picks peer memory for them: an AMR remesh
+# rebuilds the peer regions)
+CASES += [(c, "nccl") for c in ("smr2", "smr3_walls", "amr2")]
 # uniform meshes: both halo transports (NCCL pack/send/unpack, and peer memory read in place)
 CASES += [(c, h) for c in ("blast", "sod_walls", "wave64", "tiny") for h in ("nccl", "peer")]
 # the fused put: the boundary blocks' stage kernel stores its faces into the peers' buffers itself
@@ -55,7 +56,7 @@ def _run(world, cases, fused):
 
 # shards: multilevel / AMR / high order, uniform with both transports, the fused put (own env)
 SHARDS = {
-    "multilevel": [c for c in CASES if c[0] in ("smr2", "smr3_walls", "amr2", "wenoz")],
+    "multilevel": [c for c in CASES if c[0] in ("smr2", "smr3_walls", "amr2", "amr16", "wenoz")],
     "uniform": [c for c in CASES if c[0] in ("blast", "sod_walls", "wave64", "tiny") and c[1] != "peer-fused"],
     "fused": [c for c in CASES if c[1] == "peer-fused"],
 }

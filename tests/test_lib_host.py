@@ -168,13 +168,14 @@ def test_peer_halo_plan(P):
             for key in ("cyc_send_doubles_to", "cyc_recv_doubles_from", "cyc_send_hash_to", "cyc_recv_hash_from"):
                 assert i[key] == j[key]
             assert sum(i["cyc_send_doubles_to"]) > 0
-    # static multilevel meshes are eligible (fixed plan); not: one rank, adaptive, nghost 3, NCCL forced,
-    # no direct halo
+    # static multilevel and adaptive meshes are eligible (a remesh rebuilds the peer regions); not: one
+    # rank, nghost 3, NCCL forced, no direct halo
     ml = dict(max_level=1, refinement=1, regions=[(1, 0.1, 0.3, 0.1, 0.3, 0.1, 0.3)])
     assert P.Mesh(host_only=True, rank=0, nranks=2, mesh_nx=(64,) * 3, block_nx=(16,) * 3, **ml).plan_info()["peer_halo"]
-    assert not P.Mesh(host_only=True, mesh_nx=(64,) * 3, block_nx=(16,) * 3).plan_info()["peer_halo"]
     amr = dict(max_level=1, refinement=P.REF_ADAPTIVE)
-    for extra in (amr, dict(nghost=3, recon=P.PPM), dict(direct_halo=False), dict(halo_transport=P.HALO_NCCL)):
+    assert P.Mesh(host_only=True, rank=0, nranks=2, mesh_nx=(64,) * 3, block_nx=(16,) * 3, **amr).plan_info()["peer_halo"]
+    assert not P.Mesh(host_only=True, mesh_nx=(64,) * 3, block_nx=(16,) * 3).plan_info()["peer_halo"]
+    for extra in (dict(nghost=3, recon=P.PPM), dict(direct_halo=False), dict(halo_transport=P.HALO_NCCL)):
         i = P.Mesh(host_only=True, rank=0, nranks=2, mesh_nx=(64,) * 3, block_nx=(16,) * 3, **extra).plan_info()
         assert not i["peer_halo"]
     # requiring it where it cannot apply is an error, as is an unknown transport

@@ -38,6 +38,10 @@ CASES = {
     "amr2": dict(kw=dict(mesh_nx=(32, 32, 32), block_nx=(8, 8, 8), xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=2,
                          refinement=2, refine_tol=0.1, derefine_tol=0.025, derefine_interval=2),
                  problem=2, params=[10.0, 0.1, 0.1], cycles=10),
+    # AMR with 16^3 blocks: stage2's multilevel variant, the TMA tag pass, remesh + migration
+    "amr16": dict(kw=dict(mesh_nx=(64, 64, 64), block_nx=(16, 16, 16), xmin=(-.5,) * 3, xmax=(.5,) * 3, max_level=2,
+                          refinement=2, refine_tol=0.1, derefine_tol=0.025, derefine_interval=2),
+                  problem=2, params=[10.0, 0.1, 0.1], cycles=8),
 }
 
 
