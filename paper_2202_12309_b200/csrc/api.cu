@@ -112,6 +112,8 @@ struct ph_mesh {
   Plan plan[2];
   bool no_direct_halo = false;  // config: force materialised ghosts every exchange
   bool ghosts_stale = false;
+  bool w_ready = false;     // nghost-3 path: Wpool holds the primitives of U0 incl. ghosts (A49)
+  bool ho_fold = true;      // nghost-3 path: the update writes W, the per-cycle exchange moves W (PH_HO_NOFOLD=1: off)
   bool ho = false;                      // nghost 3: generic high-order path (NEXT 3)
   double *Wpool = nullptr, *Fxb = nullptr, *Fyb = nullptr, *Fzb = nullptr;
   double* Hpool = nullptr;  // stage-2 base H = a0 U^n + b1 U^1 (uniform full-tile minmod path)
@@ -1214,9 +1216,11 @@ static ph_status run_stage(ph_mesh* m, const double* Uin, double* Uout, double a
       t1 = pool_event(m);
       CU(cudaEventRecord(t0, m->stream));
     }
-    CU(launch_highorder_stage(m->cfg.recon, reduce, a0 != 0.0, nloc, A, m->Wpool, m->Fxb, m->Fyb, m->Fzb, m->G,
-                              m->stream));
-    m->launches += 5;
+    const bool w_ready = m->ho_fold && m->w_ready;
+    CU(launch_highorder_stage(m->cfg.recon, reduce, a0 != 0.0, nloc, A, m->Wpool, m->Fxb, m->Fyb, m->Fzb, w_ready,
+                              m->ho_fold, m->G, m->stream));
+    m->launches += w_ready ? 4 : 5;
+    m->w_ready = false;  // W now holds the new interior; its ghosts arrive with the W exchange
     if (m->timing) {
       CU(cudaEventRecord(t1, m->stream));
       m->t_stage.push_back({t0, t1});
@@ -1374,13 +1378,22 @@ static ph_status one_cycle(ph_mesh* m) {
   // are reduced after the reflux (no standalone pass over the whole pool)
   const bool ml_fuse = m->multilevel && !adaptive && !m->ho && !getenv("PH_NO_ML_FUSE");
   const bool red2 = fuse_reduce || ml_fuse;
+  // nghost-3 path: the update kernels write the primitives of their output and the per-cycle exchange
+  // moves W instead of U (reading A49: W of exchanged U == exchanged W, bit for bit); U's ghosts are
+  // then refreshed only on demand (ghosts_stale)
+  const bool wx = m->ho && m->ho_fold;
+  auto xchg = [&](double* U) -> ph_status {
+    TRY(exchange(m, wx ? m->Wpool : U, 1));
+    if (wx) m->w_ready = true;
+    return PH_OK;
+  };
   if (m->cfg.integrator == PH_INT_VL2) {
     TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, 0.5, false, 1));
-    TRY(exchange(m, m->U1, 1));
+    TRY(xchg(m->U1));
     TRY(run_stage(m, m->U1, m->U0, 1.0, 0.0, 1.0, red2, 2));
   } else {
     TRY(run_stage(m, m->U0, m->U1, 0.0, 1.0, 1.0, false, 1));
-    TRY(exchange(m, m->U1, 1));
+    TRY(xchg(m->U1));
     TRY(run_stage(m, m->U1, m->U0, 0.5, 0.5, 0.5, red2, 2));
   }
   if (ml_fuse && !m->rfx_faces.empty()) {
@@ -1388,7 +1401,7 @@ static ph_status one_cycle(ph_mesh* m) {
                          m->partials + (int64_t)m->stage_ctas * 6, m->d_err, m->G, m->stream));
     m->launches++;
   }
-  TRY(exchange(m, m->U0, 1));
+  TRY(xchg(m->U0));
   bool tag_partials = false;  // the tag pass also reduced dt / totals of the unchanged mesh
   if (adaptive) {
     // O5 step 6: tag after the cycle, remesh, exchange; dt and totals on the new mesh.  The cycle
@@ -1414,6 +1427,7 @@ static ph_status one_cycle(ph_mesh* m) {
  * on their sending rank and sent as octants.  Per (sender, receiver) pair both ranks enumerate
  * the new blocks in gid order, so buffer offsets agree without a handshake. */
 static ph_status remesh(ph_mesh* m, const std::unordered_set<LocKey>& leaves, bool move) {
+  m->w_ready = false;
   const int R = m->nranks, me = m->rank;
   // peer halo (AMR): the plan changes, so the receive regions, offsets and mappings are rebuilt after it
   const bool had_peer = m->peer && !m->host_only;  // (host-only meshes: plan only, nothing mapped)
@@ -1738,6 +1752,7 @@ ph_status ph_mesh_create(const ph_config* cfg, ph_mesh** out) {
   m->host_only = cfg->host_only != 0;
   m->no_direct_halo = cfg->no_direct_halo != 0;
   m->use_graph = !(getenv("PH_NO_GRAPH") && atoi(getenv("PH_NO_GRAPH")) != 0);
+  m->ho_fold = !(getenv("PH_HO_NOFOLD") && atoi(getenv("PH_HO_NOFOLD")) != 0);
   if (getenv("PH_PACK_STREAMS")) m->pack_streams = atoi(getenv("PH_PACK_STREAMS"));
   Geom& G = m->G;
   G.g = cfg->nghost;
@@ -1893,6 +1908,7 @@ static ph_status need_device(const ph_mesh* m) {
 
 ph_status ph_exchange(ph_mesh* m) {
   PH_API_BEGIN
+  if (m) m->w_ready = false;  // U0 changes (or is re-exchanged): W is rebuilt at the next step
   TRY(need_device(m));
   TRY(exchange(m, m->U0, 0));
   return check_err(m);
@@ -1901,6 +1917,7 @@ ph_status ph_exchange(ph_mesh* m) {
 
 ph_status ph_refresh(ph_mesh* m) {
   PH_API_BEGIN
+  if (m) m->w_ready = false;  // U0 changes (or is re-exchanged): W is rebuilt at the next step
   TRY(need_device(m));
   TRY(exchange(m, m->U0, 0));
   TRY(standalone_reduce(m, m->U0, 0));
@@ -1911,6 +1928,7 @@ ph_status ph_refresh(ph_mesh* m) {
 
 ph_status ph_set_problem(ph_mesh* m, int32_t problem, const double* p, int32_t np) {
   PH_API_BEGIN
+  if (m) m->w_ready = false;  // U0 changes (or is re-exchanged): W is rebuilt at the next step
   TRY(need_device(m));
   PgenArgs P{};
   P.problem = problem;
@@ -1965,6 +1983,7 @@ static int64_t slot_of(const ph_mesh* m, int64_t gid) {
 
 ph_status ph_set_state(ph_mesh* m, int64_t gid, const double* cons, int64_t nelem) {
   PH_API_BEGIN
+  if (m) m->w_ready = false;  // U0 changes (or is re-exchanged): W is rebuilt at the next step
   TRY(need_device(m));
   int64_t s = slot_of(m, gid);
   if (s == -2) return fail(PH_ERR_INVALID_ARG, "bad gid");
@@ -2021,6 +2040,7 @@ ph_status ph_get_state_full(const ph_mesh* mc, int64_t gid, double* out, int64_t
 
 ph_status ph_set_state_full(ph_mesh* m, int64_t gid, const double* in, int64_t nelem) {
   PH_API_BEGIN
+  if (m) m->w_ready = false;  // U0 changes (or is re-exchanged): W is rebuilt at the next step
   TRY(need_device(m));
   int64_t s = slot_of(m, gid);
   if (s == -2) return fail(PH_ERR_INVALID_ARG, "bad gid");
@@ -2043,6 +2063,12 @@ ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) 
   // remesh), on a private stream forked from / joined to the caller's stream (the legacy default
   // stream cannot be captured).  Adaptive meshes (host-side remesh decisions) and kernel-timing
   // runs stay eager on the caller's stream.
+  const int32_t ncycles_req = ncycles;
+  if (m->ho && m->ho_fold && !m->w_ready && ncycles > 0) {  // W from U0 first (prim_kernel): one eager cycle,
+    TRY(one_cycle(m));                                     // so the captured graph can assume W is ready
+    --ncycles;
+    m->ghosts_stale = true;
+  }
   const bool graph_ok = m->use_graph && !m->timing && m->cfg.refinement != PH_REF_ADAPTIVE && ncycles > 0;
   if (graph_ok) {
     if (!m->gstream) {
@@ -2089,7 +2115,7 @@ ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) 
   } else {
     for (int c = 0; c < ncycles; ++c) TRY(one_cycle(m));
   }
-  if (ncycles > 0 && m->direct_halo) m->ghosts_stale = true;
+  if (ncycles > 0 && (m->direct_halo || (m->ho && m->ho_fold))) m->ghosts_stale = true;
   if (info) {
     TRY(check_err(m));
     CycleState st;
@@ -2098,7 +2124,7 @@ ph_status ph_step(ph_mesh* m, int32_t ncycles, double tlim, ph_step_info* info) 
     info->t = st.t;
     info->dt = st.dt;
     int64_t cells = (int64_t)m->blocks.size() * m->G.n[0] * m->G.n[1] * m->G.n[2];
-    info->zone_cycles = cells * ncycles;
+    info->zone_cycles = cells * ncycles_req;
   }
   return PH_OK;
   PH_API_END
@@ -2122,6 +2148,7 @@ ph_status ph_sync(ph_mesh* m) {
 ph_status ph_step_host_async(ph_mesh* m, const double* host_in, double* host_out, int64_t nelem, int32_t ncycles,
                              double tlim) {
   PH_API_BEGIN
+  if (m) m->w_ready = false;
   TRY(need_device(m));
   // an adaptive mesh may remesh inside ph_step: the local block set (and so the layout of host_out)
   // would change under the copy-back

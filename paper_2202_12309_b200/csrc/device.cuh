@@ -225,7 +225,8 @@ cudaError_t launch_tag2(const double* U, const BlockMeta* meta, int nslots, unsi
 cudaError_t launch_remesh(const RemeshTask* t, int ntasks, const double* Uold, double* Unew, const double* rbuf,
                           double* sbuf, const Geom& G, cudaStream_t s);
 cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslots, const StageArgs& a, double* W,
-                                   double* Fx, double* Fy, double* Fz, const Geom& G, cudaStream_t s);
+                                   double* Fx, double* Fy, double* Fz, bool w_ready, bool w_out, const Geom& G,
+                                   cudaStream_t s);
 size_t stage_smem_bytes();
 // stage2.cu: the round-2 uniform-mesh stage kernel (16 x 16 tiles, bulk-copy plane ring); applies to
 // minmod + Davis on uniform levels with n1, n2 multiples of 16 and nghost 2 (PH_STAGE_V1=1 disables it)

@@ -1479,7 +1479,8 @@ __global__ void __launch_bounds__(128, RECON == 3 ? PH_HOLINE_MINB : 1) holine_k
 }
 
 template <bool REDUCE, bool USE_U0>
-__global__ void houpdate_kernel(StageArgs A, const double* Fx, const double* Fy, const double* Fz, Geom G) {
+__global__ void houpdate_kernel(StageArgs A, const double* Fx, const double* Fy, const double* Fz, double* Wout,
+                                Geom G) {
   const int k = blockIdx.x % G.n[2];
   const int slot = blockIdx.x / G.n[2];
   const BlockMeta& M = A.meta[slot];
@@ -1537,10 +1538,20 @@ __global__ void houpdate_kernel(StageArgs A, const double* Fx, const double* Fy,
       un[v] = out;
       A.Uout[cell + v * G.vstride] = out;
     }
+    double Wn[NVAR];
+    if (REDUCE || Wout) {
+      // the primitives of the new state (prim_kernel's exact arithmetic): the next stage's W interior
+      // (its ghosts come from exchanging W: bit-identical to converting exchanged U, reading A49);
+      // an invalid cell is reported for the stage that converts it next, as prim_kernel would
+      if (!cons2prim_rn(un[0], un[1], un[2], un[3], un[4], G.gm1, Wn) && Wout)
+        set_error(A.err, A.stage == 1 ? 2 : 1, M.gid, k, j, i);
+      if (Wout) {
+#pragma unroll
+        for (int v = 0; v < NVAR; ++v) Wout[cell + v * G.vstride] = Wn[v];
+      }
+    }
     if (REDUCE) {
       // exact CFL term, kept as -min(...) in the 'max' slot (finalize: dt = cfl * (-m), G.exact)
-      double Wn[NVAR];
-      cons2prim_rn(un[0], un[1], un[2], un[3], un[4], G.gm1, Wn);
       const double cs = __dsqrt_rn(__ddiv_rn(__dmul_rn(G.gamma, Wn[4]), Wn[0]));
 #pragma unroll
       for (int d = 0; d < 3; ++d) smax[d] = fmax(smax[d], __dadd_rn(fabs(Wn[1 + d]), cs));
@@ -2118,9 +2129,10 @@ static cudaError_t launch_hoflux_r(const double* W, double* Fx, double* Fy, doub
 constexpr int HOU_T = 128;  // update kernel CTA (up to ~150 registers with the loads hoisted: 3 CTAs per SM)
 
 cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslots, const StageArgs& a, double* W,
-                                   double* Fx, double* Fy, double* Fz, const Geom& G, cudaStream_t s) {
+                                   double* Fx, double* Fy, double* Fz, bool w_ready, bool w_out, const Geom& G,
+                                   cudaStream_t s) {
   if (nslots <= 0) return cudaSuccess;
-  prim_kernel<<<nslots * G.N[2], 256, 0, s>>>(a.Uin, W, a.meta, a.err, a.stage, G);
+  if (!w_ready) prim_kernel<<<nslots * G.N[2], 256, 0, s>>>(a.Uin, W, a.meta, a.err, a.stage, G);
   cudaError_t e;
   switch (recon) {
     case 0: e = launch_hoflux_r<0>(W, Fx, Fy, Fz, nslots, G, s); break;
@@ -2132,11 +2144,11 @@ cudaError_t launch_highorder_stage(int recon, bool reduce, bool use_u0, int nslo
   if (e != cudaSuccess) return e;
   const int grid = nslots * G.n[2];
   if (reduce) {
-    if (use_u0) houpdate_kernel<true, true><<<grid, HOU_T, 0, s>>>(a, Fx, Fy, Fz, G);
-    else houpdate_kernel<true, false><<<grid, HOU_T, 0, s>>>(a, Fx, Fy, Fz, G);
+    if (use_u0) houpdate_kernel<true, true><<<grid, HOU_T, 0, s>>>(a, Fx, Fy, Fz, w_out ? W : nullptr, G);
+    else houpdate_kernel<true, false><<<grid, HOU_T, 0, s>>>(a, Fx, Fy, Fz, w_out ? W : nullptr, G);
   } else {
-    if (use_u0) houpdate_kernel<false, true><<<grid, HOU_T, 0, s>>>(a, Fx, Fy, Fz, G);
-    else houpdate_kernel<false, false><<<grid, HOU_T, 0, s>>>(a, Fx, Fy, Fz, G);
+    if (use_u0) houpdate_kernel<false, true><<<grid, HOU_T, 0, s>>>(a, Fx, Fy, Fz, w_out ? W : nullptr, G);
+    else houpdate_kernel<false, false><<<grid, HOU_T, 0, s>>>(a, Fx, Fy, Fz, w_out ? W : nullptr, G);
   }
   return cudaGetLastError();
 }
