@@ -156,6 +156,14 @@ __device__ __forceinline__ void ppm_cell_rn(const double* q, double& ql, double&
   ppm_lr_rn(q[1], q[2], q[3], dm_m, dm_0, dm_p, ql, qr);
 }
 
+// WENO-Z's general divisions: inlined (default) or one out-of-line copy (PH_WENO_DIV_CALL, A/B knob: the
+// per-face kernel inlines 43 IEEE division sequences and stalls on instruction fetch)
+#ifdef PH_WENO_DIV_CALL
+__device__ __noinline__ double wdiv(double a, double b) { return __ddiv_rn(a, b); }
+#else
+__device__ __forceinline__ double wdiv(double a, double b) { return __ddiv_rn(a, b); }
+#endif
+
 __device__ __forceinline__ double wenoz_rn(double a, double b, double c, double d, double e) {
   const double t0 = __dadd_rn(__dsub_rn(a, __dmul_rn(2.0, b)), c), u0 = __dadd_rn(__dsub_rn(a, __dmul_rn(4.0, b)), __dmul_rn(3.0, c));
   const double t1 = __dadd_rn(__dsub_rn(b, __dmul_rn(2.0, c)), d), u1 = __dsub_rn(b, d);
@@ -165,15 +173,15 @@ __device__ __forceinline__ double wenoz_rn(double a, double b, double c, double 
   const double b1 = __dadd_rn(__dmul_rn(k13, __dmul_rn(t1, t1)), __dmul_rn(0.25, __dmul_rn(u1, u1)));
   const double b2 = __dadd_rn(__dmul_rn(k13, __dmul_rn(t2, t2)), __dmul_rn(0.25, __dmul_rn(u2, u2)));
   const double tau = fabs(__dsub_rn(b0, b2));
-  const double r0 = __ddiv_rn(tau, __dadd_rn(b0, 1e-40)), r1 = __ddiv_rn(tau, __dadd_rn(b1, 1e-40)),
-               r2 = __ddiv_rn(tau, __dadd_rn(b2, 1e-40));
+  const double r0 = wdiv(tau, __dadd_rn(b0, 1e-40)), r1 = wdiv(tau, __dadd_rn(b1, 1e-40)),
+               r2 = wdiv(tau, __dadd_rn(b2, 1e-40));
   const double a0 = __dmul_rn(0.1, __dadd_rn(1.0, __dmul_rn(r0, r0)));
   const double a1 = __dmul_rn(0.6, __dadd_rn(1.0, __dmul_rn(r1, r1)));
   const double a2 = __dmul_rn(0.3, __dadd_rn(1.0, __dmul_rn(r2, r2)));
   const double q0 = ddiv_k(__dadd_rn(__dsub_rn(__dmul_rn(2.0, a), __dmul_rn(7.0, b)), __dmul_rn(11.0, c)), K6, RK6);
   const double q1 = ddiv_k(__dadd_rn(__dadd_rn(-b, __dmul_rn(5.0, c)), __dmul_rn(2.0, d)), K6, RK6);
   const double q2 = ddiv_k(__dsub_rn(__dadd_rn(__dmul_rn(2.0, c), __dmul_rn(5.0, d)), e), K6, RK6);
-  return __ddiv_rn(__dadd_rn(__dadd_rn(__dmul_rn(a0, q0), __dmul_rn(a1, q1)), __dmul_rn(a2, q2)),
+  return wdiv(__dadd_rn(__dadd_rn(__dmul_rn(a0, q0), __dmul_rn(a1, q1)), __dmul_rn(a2, q2)),
                    __dadd_rn(__dadd_rn(a0, a1), a2));
 }
 
